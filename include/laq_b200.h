@@ -1,0 +1,282 @@
+/*
+ * laq_b200.h — C-ABI of the B200-native LAQ hot path.
+ *
+ * The reference (arxiv 2306.08367 artifact, /root/reference/proj) exposes a
+ * C++20 operator API over host std::vectors (proj/include/laq/*.hpp).  This
+ * header is the drop-in boundary underneath it: plain C, plain pointers and
+ * sizes, no C++ or torch types.  Every entry point names the reference
+ * function it replaces as  file:line  (paths relative to proj/).
+ *
+ * Conventions
+ *  - Every call returns an int status: LAQ_OK or one of the LAQ_ERR_* codes,
+ *    which map 1:1 onto the laq::Error subclasses of include/laq/error.hpp:10-74
+ *    (the C++ shim in integration/ rethrows the matching type).  The message of
+ *    the last failure on a context is available from laq_ctx_last_error().
+ *  - "d_" arguments are DEVICE pointers owned by the caller; "h_" arguments are
+ *    host pointers.  Scratch memory is owned by the context.
+ *  - A context is bound to one device and one CUDA stream; calls on one context
+ *    are serialised on that stream (asynchronous unless the call must return a
+ *    data-dependent size through an h_ pointer, in which case it synchronises).
+ *    Separate contexts are reentrant.
+ *  - There is no CPU fallback: when the CUDA kernels cannot run, calls fail
+ *    with LAQ_ERR_CUDA.
+ */
+#ifndef LAQ_B200_H
+#define LAQ_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (error.hpp:10-74) ---------------------------------- */
+enum laq_status {
+  LAQ_OK = 0,
+  LAQ_ERR_GENERIC = 1,        /* laq::Error            error.hpp:10  */
+  LAQ_ERR_INDEX = 2,          /* laq::IndexError       error.hpp:15  */
+  LAQ_ERR_SHAPE = 3,          /* laq::ShapeError       error.hpp:20  */
+  LAQ_ERR_FORMAT = 4,         /* laq::FormatError      error.hpp:25  */
+  LAQ_ERR_NAME = 5,           /* laq::NameError        error.hpp:30  */
+  LAQ_ERR_TYPE = 6,           /* laq::TypeError        error.hpp:35  */
+  LAQ_ERR_MAPPING = 7,        /* laq::MappingError     error.hpp:40  */
+  LAQ_ERR_DOMAIN = 8,         /* laq::DomainError      error.hpp:45  */
+  LAQ_ERR_DUPLICATE_KEY = 9,  /* laq::DuplicateKeyError error.hpp:51 */
+  LAQ_ERR_TREE = 10,          /* laq::TreeError        error.hpp:56  */
+  LAQ_ERR_MODEL = 11,         /* laq::ModelError       error.hpp:61  */
+  LAQ_ERR_GEN = 12,           /* laq::GenError         error.hpp:66  */
+  LAQ_ERR_CAPACITY = 13,      /* laq::CapacityError    error.hpp:71  */
+  LAQ_ERR_CUDA = 100,         /* device / driver failure (no reference equivalent) */
+  LAQ_ERR_UNSUPPORTED = 101   /* valid input outside this build's device paths */
+};
+
+typedef struct laq_ctx laq_ctx;
+typedef struct laq_star laq_star;
+typedef struct laq_plan laq_plan;
+
+/* ---- context ----------------------------------------------------------- */
+int laq_ctx_create(int device, laq_ctx** out);
+int laq_ctx_destroy(laq_ctx* ctx);
+/* Bind the context to an existing cudaStream_t (NULL = the legacy stream). */
+int laq_ctx_set_stream(laq_ctx* ctx, void* cuda_stream);
+int laq_ctx_synchronize(laq_ctx* ctx);
+const char* laq_ctx_last_error(const laq_ctx* ctx);
+/* Number of kernels this context has launched (bench/gpu_launches evidence). */
+int64_t laq_ctx_launch_count(const laq_ctx* ctx);
+/* Library build string (arch, version). */
+const char* laq_version(void);
+
+/* ---- key encoding (laqops.hpp:54-78) ----------------------------------- */
+
+/* build_key_domain (laqops.cpp:142-155): ascending distinct union of keys_r and
+ * keys_s into d_out_sorted (capacity n_r + n_s); size to *h_out_size.
+ * LAQ_ERR_DOMAIN on a negative key. Synchronises. */
+int laq_build_key_domain(laq_ctx* ctx, const int64_t* d_keys_r, int64_t n_r,
+                         const int64_t* d_keys_s, int64_t n_s, int64_t* d_out_sorted,
+                         int64_t* h_out_size);
+
+/* update_key_domain (laqops.cpp:157-171): merge new keys into a sorted domain.
+ * d_out capacity d + n_new. Synchronises. */
+int laq_update_key_domain(laq_ctx* ctx, const int64_t* d_domain, int64_t d,
+                          const int64_t* d_new_keys, int64_t n_new, int64_t* d_out,
+                          int64_t* h_out_size);
+
+/* KeyDomain::position over a batch (laqops.cpp:123-127) — the col_idx of
+ * key_matrix(RowsByDomain) (laqops.cpp:181-195).  LAQ_ERR_DOMAIN if a key is
+ * absent.  d_domain must be ascending and distinct. */
+int laq_key_positions(laq_ctx* ctx, const int64_t* d_keys, int64_t n, const int64_t* d_domain,
+                      int64_t d, int64_t* d_pos);
+
+/* key_matrix(DomainByRows) (laqops.cpp:196-218): CSR d x n, counting sort by
+ * domain position, columns ascending per row.  d_values may be NULL (all 1.0);
+ * rows whose value is exactly 0.0 are validated but not stored (laqops.cpp:188-190),
+ * so d_col_idx/d_out_values capacity is n and *h_nnz receives the stored count.
+ * d_out_values may be NULL when d_values is NULL. Synchronises. */
+int laq_key_matrix_dbr(laq_ctx* ctx, const int64_t* d_keys, int64_t n, const int64_t* d_domain,
+                       int64_t d, const double* d_values, int64_t* d_row_ptr, int64_t* d_col_idx,
+                       double* d_out_values, int64_t* h_nnz);
+
+/* ---- join-MM (laqops.hpp:80-110) --------------------------------------- */
+
+/* mm_join (laqops.cpp:222-231): equi-join as spmm(key_matrix(R), key_matrix(S)^T),
+ * many-to-many, COO in canonical (r asc, s asc) order.  If capacity is too small
+ * returns LAQ_ERR_CAPACITY with *h_nnz = required entries and writes nothing.
+ * Synchronises. */
+int laq_mm_join(laq_ctx* ctx, const int64_t* d_keys_r, int64_t n_r, const int64_t* d_keys_s,
+                int64_t n_s, int64_t* d_out_r, int64_t* d_out_s, int64_t capacity, int64_t* h_nnz);
+
+/* multiway_star_join (laqops.cpp:233-319): per fact row, the unique matching
+ * row of every dimension; rows missing any dimension drop out.  Outputs, in
+ * ascending fact-row order: d_survivors[m] (fact row) and d_dim_rows[j][m]
+ * (row of dim j).  Capacities n_fact.  LAQ_ERR_DUPLICATE_KEY on a duplicate
+ * pk (laqops.cpp:252-254).  d_survivors may be NULL. Synchronises. */
+int laq_star_join(laq_ctx* ctx, int32_t n_links, const int64_t* const* d_fks, int64_t n_fact,
+                  const int64_t* const* d_pks, const int64_t* h_pk_rows, int64_t* d_survivors,
+                  int64_t* const* d_dim_rows, int64_t* h_nnz);
+
+/* ---- dense / fused prediction (fusion.hpp:8-18, mlops.hpp:74) ----------- */
+
+/* dense_matmul (matrix.cpp:158-174) / predict_linear (mlops.cpp:248-250):
+ * C[m x n] = A[m x k] * B[k x n], fp64 row-major, sequential-k fp64 sums. */
+int laq_dense_matmul(laq_ctx* ctx, const double* d_a, int64_t m, int64_t k, const double* d_b,
+                     int64_t n, double* d_c);
+
+/* prefuse_linear (fusion.cpp:50-62) + linear_partial (fusion.cpp:31-36):
+ * P_j = B_j * (M_j * L) where M_j is the placement of dim j's k_j columns into
+ * the global width k (h_placements[j][c] = global column of local column c).
+ * Placements must tile [0,k) exactly: LAQ_ERR_MAPPING on overlap, LAQ_ERR_SHAPE
+ * on gaps (check_placements, fusion.cpp:11-25). fp64. */
+int laq_prefuse_linear(laq_ctx* ctx, int32_t n_dims, const double* const* d_dims,
+                       const int64_t* h_dim_rows, const int64_t* h_dim_cols,
+                       const int64_t* const* h_placements, const double* d_L, int64_t k,
+                       int64_t l, double* const* d_partials);
+
+/* apply_fused_linear (fusion.cpp:64-77): Y[m] = ((P_0[i_0[m]] + P_1[i_1[m]]) + ...)
+ * in the reference's association order, fp64.  d_idx[j] are the I_j row maps
+ * (one source row per target row). */
+int laq_apply_fused_linear(laq_ctx* ctx, int32_t n_parts, const int64_t* const* d_idx, int64_t rows,
+                           const double* const* d_partials, const int64_t* h_partial_rows,
+                           int64_t l, double* d_out);
+
+/* materialize (laqops.cpp:338-374): T[m, place_j(c)] = B_j[i_j[m], c], fp64,
+ * the non-fused plan's target table.  LAQ_ERR_MAPPING on overlapping targets. */
+int laq_materialize(laq_ctx* ctx, int32_t n_parts, const int64_t* const* d_idx, int64_t rows,
+                    const double* const* d_dims, const int64_t* h_dim_rows,
+                    const int64_t* h_dim_cols, const int64_t* const* h_placements, int64_t k,
+                    double* d_out);
+
+/* Fused join + predict (north_star; PipelineRunner::run_fused cli.cpp:336-346
+ * composed with prepare_joins cli.cpp:279-293): one pass over the fact keys
+ * that probes every dimension, drops misses, and writes Y[m] = sum_j P_j[row_j]
+ * for the m-th surviving fact row in ascending order.  d_survivors may be NULL.
+ * Keys are int32 (range-checked narrowing of the reference's int64 keys).
+ * Synchronises to report *h_nnz. */
+int laq_fused_star_predict(laq_ctx* ctx, int32_t n_links, const int32_t* const* d_fks,
+                           int64_t n_fact, const int32_t* const* d_pks, const int64_t* h_pk_rows,
+                           const double* const* d_partials, int64_t l, double* d_out,
+                           int64_t* d_survivors, int64_t* h_nnz);
+
+/* Lower-level form of laq_fused_star_predict for repeated execution (CUDA-graph
+ * capturable, no host sync): build the per-dimension probe tables once ... */
+typedef struct laq_probe laq_probe;
+int laq_probe_build(laq_ctx* ctx, int32_t n_links, const int32_t* const* d_pks,
+                    const int64_t* h_pk_rows, laq_probe** out);
+/* ... then stream the fact keys; the survivor count is written to d_nnz (device). */
+int laq_probe_fused_predict(laq_ctx* ctx, const laq_probe* probe, const int32_t* const* d_fks,
+                            int64_t n_fact, const double* const* d_partials, int64_t l,
+                            double* d_out, int64_t* d_survivors, int64_t* d_nnz);
+int laq_probe_destroy(laq_probe* probe);
+
+/* ---- aggregate-MM (laqops.hpp:112-166) --------------------------------- */
+
+/* groupby_sum_single (laqops.cpp:376-413): join R and S on key, sum R's values
+ * per S group; groups = distinct group_s ascending, zero-sum groups included.
+ * Output capacity n_s.  Synchronises. */
+int laq_groupby_sum_single(laq_ctx* ctx, const int64_t* d_keys_r, const double* d_vals_r,
+                           int64_t n_r, const int64_t* d_keys_s, const int64_t* d_group_s,
+                           int64_t n_s, int64_t* d_out_groups, double* d_out_sums,
+                           int64_t* h_n_groups);
+
+/* groupby_sum_multi (laqops.cpp:415-455): present tuples only, ascending.
+ * d_out_keys is n_cols x capacity (column-major: key c of group g at
+ * [c*capacity + g]); capacity n. Synchronises. */
+int laq_groupby_sum_multi(laq_ctx* ctx, int32_t n_cols, const int64_t* const* d_cols,
+                          const double* d_vals, int64_t n, int64_t* d_out_keys, double* d_out_sums,
+                          int64_t capacity, int64_t* h_n_groups);
+
+/* ---- star schema + query plan driver (storage.hpp:75-100, cli.cpp:73-138) ---- */
+
+enum laq_col_kind { LAQ_COL_KEY = 0, LAQ_COL_INT = 1, LAQ_COL_FLOAT = 2 }; /* storage.hpp:14 */
+
+/* A StarSchema resident in HBM: integer columns are narrowed to int32 on the
+ * device (range-checked; LAQ_ERR_CAPACITY if a value does not fit). */
+int laq_star_create(laq_ctx* ctx, laq_star** out);
+int laq_star_destroy(laq_star* star);
+/* Add a table from HOST columns: key/int kinds are int64 (the reference's
+ * IntColumn, storage.hpp:35) when int_width == 8, or already-narrowed int32
+ * when int_width == 4; float columns are double.  The table added with
+ * is_fact=1 is the fact table.  Key columns must be non-negative
+ * (LAQ_ERR_FORMAT, storage.cpp:54-56).  Synchronises. */
+int laq_star_add_table(laq_star* star, const char* name, int32_t is_fact, int64_t rows,
+                       int32_t n_cols, const char* const* col_names, const int32_t* col_kinds,
+                       int32_t int_width, const void* const* h_cols);
+/* Same, from int32 DEVICE columns already narrowed (no copy; caller keeps them alive). */
+int laq_star_add_table_device(laq_star* star, const char* name, int32_t is_fact, int64_t rows,
+                              int32_t n_cols, const char* const* col_names,
+                              const int32_t* col_kinds, const int32_t* const* d_cols);
+/* StarSchema link (storage.hpp:75-81); checks pk uniqueness (storage.cpp:200-214). */
+int laq_star_add_link(laq_star* star, const char* fact_fk, const char* dim_name,
+                      const char* dim_pk);
+
+/* Query description (benchgen.hpp:296-326).  Predicates are Predicate kinds
+ * (predicate.hpp:15-28) over integer columns. */
+enum laq_pred_kind {
+  LAQ_PRED_LT = 0, LAQ_PRED_LE = 1, LAQ_PRED_EQ = 2, LAQ_PRED_GE = 3, LAQ_PRED_GT = 4,
+  LAQ_PRED_BETWEEN = 5, LAQ_PRED_INSET = 6
+};
+typedef struct {
+  int32_t target;        /* -1 = fact, else index into joins */
+  const char* column;
+  int32_t kind;          /* laq_pred_kind */
+  int32_t is_float;      /* 1: float constants (TypeError against int columns) */
+  int64_t lo, hi;        /* integer constants (hi used by BETWEEN) */
+  const int64_t* set;    /* INSET values */
+  int64_t set_len;
+} laq_filter_desc;
+typedef struct { const char* fact_fk; const char* dim_name; const char* dim_pk; } laq_link_desc;
+typedef struct { int32_t target; const char* column; } laq_group_desc;
+typedef struct {
+  int32_t n_joins;
+  const laq_link_desc* joins;
+  int32_t n_filters;
+  const laq_filter_desc* filters;
+  const char* measure;
+  int32_t n_group;
+  const laq_group_desc* group_by;
+  int32_t order_by;
+} laq_query_desc;
+
+/* Prepare a plan: resolves names (LAQ_ERR_NAME), types (LAQ_ERR_TYPE) and the
+ * dense group-id space; *h_n_groups = number of group-id slots G. */
+int laq_query_prepare(laq_ctx* ctx, const laq_star* star, const laq_query_desc* q, laq_plan** out,
+                      int64_t* h_n_groups);
+/* Enqueue the plan on the context stream (no host sync; graph-capturable):
+ * rebuild the per-link probe tables from the dimension filters, then one
+ * fused scan of the fact table that accumulates, per group id, d_acc[2g] =
+ * surviving row count and d_acc[2g+1] = SUM(measure) (exact int64).  d_acc
+ * (2*G int64) is zeroed by the call unless accumulate != 0. */
+int laq_plan_execute(laq_ctx* ctx, laq_plan* plan, int64_t* d_acc, int32_t accumulate);
+/* The two halves of laq_plan_execute, for per-kernel timing: rebuild the
+ * per-link code tables (dimension filters), then the fused fact scan. */
+int laq_plan_build_codes(laq_ctx* ctx, laq_plan* plan);
+int laq_plan_scan(laq_ctx* ctx, laq_plan* plan, int64_t* d_acc, int32_t accumulate);
+/* Bytes of fact columns the scan streams per row (the roofline unit). */
+int64_t laq_plan_bytes_per_row(const laq_plan* plan);
+/* Turn an accumulator (host copy, e.g. after an all-reduce) into the
+ * run_query_laq result rows [group cols..., sum] (row-major), present groups
+ * only, ascending (groupby_sum_multi + sort_rows; laqops.cpp:415-478).  A plain
+ * Sum query yields one 1x1 row (cli.cpp:103-107). */
+int laq_plan_emit(const laq_plan* plan, const int64_t* h_acc, double* h_out, int64_t capacity,
+                  int64_t* h_rows, int64_t* h_cols);
+int laq_plan_destroy(laq_plan* plan);
+
+/* run_query_laq (cli.cpp:73-138) in one call: prepare + execute + emit. */
+int laq_run_query(laq_ctx* ctx, const laq_star* star, const laq_query_desc* q, double* h_out,
+                  int64_t capacity, int64_t* h_rows, int64_t* h_cols);
+
+/* measure_selectivity (benchgen.cpp:366-411) on the device: surviving fact
+ * rows / fact rows. Synchronises. */
+int laq_measure_selectivity(laq_ctx* ctx, const laq_star* star, const laq_query_desc* q,
+                            double* h_out);
+
+/* ---- fusion cost model (fusion.hpp:56-76; fusion.cpp:259-302) ----------- */
+int laq_speedup_ratio_linear(int64_t i, int64_t k, int64_t l, const int64_t* dim_rows,
+                             int32_t n_dims, double* h_out);
+int laq_speedup_ratio_tree(int64_t i, int64_t k, int64_t l, int64_t p, const int64_t* dim_rows,
+                           int32_t n_dims, double* h_out);
+int laq_decide_fusion(double ratio, double threshold, int32_t* h_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LAQ_B200_H */

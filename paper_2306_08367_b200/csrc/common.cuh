@@ -1,0 +1,136 @@
+// Shared host/device plumbing for the LAQ sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "laq_b200.h"
+
+namespace laq {
+
+// Host-side error carrying a laq_status; converted to a return code at the
+// C-ABI boundary (guard()).
+struct Err {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] inline void fail(int code, std::string msg) { throw Err{code, std::move(msg)}; }
+
+#define LAQ_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      ::laq::fail(LAQ_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+
+constexpr int kNumSMs = 148;  // B200
+
+}  // namespace laq
+
+struct laq_ctx {
+  int device = 0;
+  int sm_count = laq::kNumSMs;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int64_t launches = 0;
+  // Small pinned host staging for data-dependent sizes / flags.
+  int64_t* h_pinned = nullptr;
+  // Device flag words (error flags, counters) reused by synchronous calls.
+  int64_t* d_flags = nullptr;
+};
+
+namespace laq {
+
+// Run f() and translate exceptions into a status + ctx->err.
+template <class F>
+int guard(laq_ctx* ctx, F&& f) {
+  try {
+    if (ctx) LAQ_CUDA(cudaSetDevice(ctx->device));
+    f();
+    return LAQ_OK;
+  } catch (const Err& e) {
+    if (ctx) ctx->err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->err = e.what();
+    return LAQ_ERR_GENERIC;
+  }
+}
+
+// Launch bookkeeping: every kernel launch goes through this so the context can
+// report how many of OUR kernels ran (bench.py "gpu_launches").
+inline void launched(laq_ctx* ctx) {
+  ++ctx->launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) fail(LAQ_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
+inline void sync(laq_ctx* ctx) { LAQ_CUDA(cudaStreamSynchronize(ctx->stream)); }
+
+// Stream-ordered device scratch that frees itself (cudaMallocAsync pool).
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(laq_ctx* ctx, size_t count) : n(count), s(ctx->stream) {
+    if (count) LAQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    reset();
+    p = o.p; n = o.n; s = o.s; o.p = nullptr;
+    return *this;
+  }
+  ~DevBuf() { reset(); }
+  void reset() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+  }
+  T* get() const { return p; }
+};
+
+// Persistent device allocation (plans, probe tables): plain cudaMalloc.
+template <class T>
+struct DevMem {
+  T* p = nullptr;
+  size_t n = 0;
+  DevMem() = default;
+  explicit DevMem(size_t count) : n(count) {
+    if (count) LAQ_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
+  }
+  DevMem(const DevMem&) = delete;
+  DevMem& operator=(const DevMem&) = delete;
+  DevMem(DevMem&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; }
+  DevMem& operator=(DevMem&& o) noexcept {
+    if (p) cudaFree(p);
+    p = o.p; n = o.n; o.p = nullptr;
+    return *this;
+  }
+  ~DevMem() { if (p) cudaFree(p); }
+  T* get() const { return p; }
+};
+
+inline int grid_for(int64_t n, int per_block, int max_blocks) {
+  int64_t b = (n + per_block - 1) / per_block;
+  if (b < 1) b = 1;
+  if (b > max_blocks) b = max_blocks;
+  return static_cast<int>(b);
+}
+
+// ---- shared helpers implemented in util.cu -----------------------------
+// min/max of an int64 or int32 array (device reduce, synchronises).
+void minmax_i64(laq_ctx* ctx, const int64_t* d, int64_t n, int64_t* mn, int64_t* mx);
+void minmax_i32(laq_ctx* ctx, const int32_t* d, int64_t n, int64_t* mn, int64_t* mx);
+// Exclusive scan of int64 counts (in place allowed); returns total (synchronises
+// only when h_total != nullptr).
+void exclusive_scan_i64(laq_ctx* ctx, const int64_t* d_in, int64_t* d_out, int64_t n, int64_t* h_total);
+
+}  // namespace laq

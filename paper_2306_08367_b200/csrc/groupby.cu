@@ -1,0 +1,233 @@
+// Aggregate-MM: groupby_sum_single (laqops.cpp:376-413) and
+// groupby_sum_multi (laqops.cpp:415-455) on the device.
+//
+// groupby_sum_single = spmm(valued key_matrix(R), key->group matrix) then a
+// ones reduction.  The key->group matrix is built as sorted (key, group) runs
+// with multiplicities (csr_from_triplets sums duplicates); each R row probes
+// its key's run and adds v * multiplicity into its groups.
+//
+// groupby_sum_multi = sort-unique over tuples + segmented sum in row order.
+// Tuples are ranked per column (distinct values -> dense ranks), packed into
+// one mixed-radix code (first column most significant = lexicographic
+// order), stably radix-sorted with the row index, and every segment is summed
+// sequentially in ascending row order by one thread — the reference's exact
+// accumulation order, so fp64 sums are bit-identical.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "probe.cuh"
+
+namespace laq {
+namespace {
+
+// Index of v in the sorted distinct array d[0..n) (lower bound); -1 if absent.
+__device__ __forceinline__ int64_t find_sorted(const int64_t* __restrict__ d, int64_t n, int64_t v) {
+  int64_t a = 0, b = n;
+  while (a < b) {
+    const int64_t m = (a + b) >> 1;
+    if (__ldg(d + m) < v) a = m + 1; else b = m;
+  }
+  return (a < n && __ldg(d + a) == v) ? a : -1;
+}
+
+__global__ void rank_kernel(const int64_t* __restrict__ v, int64_t n, const int64_t* __restrict__ distinct,
+                            int64_t nd, int64_t stride, int64_t* code, int accumulate) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = find_sorted(distinct, nd, v[i]);
+    code[i] = (accumulate ? code[i] : 0) + r * stride;
+  }
+}
+
+__global__ void segsum_kernel(const int64_t* __restrict__ seg_off, int64_t n_seg, const int64_t* __restrict__ rows,
+                              const double* __restrict__ vals, double* __restrict__ out) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_seg; s += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int64_t t = seg_off[s]; t < seg_off[s + 1]; ++t) acc = __dadd_rn(acc, __ldg(vals + rows[t]));
+    out[s] = acc;
+  }
+}
+
+__global__ void decode_kernel(const int64_t* __restrict__ codes, int64_t g, const int64_t* __restrict__ distinct,
+                              int64_t stride, int64_t range, int64_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = distinct[(codes[i] / stride) % range];
+}
+
+// (key index * G + group index) codes for the S side of groupby_sum_single.
+__global__ void pair_code_kernel(const int64_t* __restrict__ ks, const int64_t* __restrict__ gs, int64_t n,
+                                 const int64_t* __restrict__ dk, int64_t nk, const int64_t* __restrict__ dg,
+                                 int64_t G, int64_t* code) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    code[i] = find_sorted(dk, nk, ks[i]) * G + find_sorted(dg, G, gs[i]);
+}
+
+__global__ void single_accumulate(const int64_t* __restrict__ kr, const double* __restrict__ vr, int64_t nr,
+                                  const int64_t* __restrict__ dk, int64_t nk, const int64_t* __restrict__ key_run_off,
+                                  const int64_t* __restrict__ pair_codes, const int64_t* __restrict__ pair_cnt,
+                                  int64_t G, double* sums) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nr; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = vr[i];
+    if (v == 0.0) continue;  // key_matrix skips zero values (laqops.cpp:188-190)
+    const int64_t kp = find_sorted(dk, nk, kr[i]);
+    if (kp < 0) continue;
+    for (int64_t t = key_run_off[kp]; t < key_run_off[kp + 1]; ++t)
+      atomicAdd(sums + pair_codes[t] % G, __dmul_rn(v, static_cast<double>(pair_cnt[t])));
+  }
+}
+
+__global__ void key_of_pair(const int64_t* __restrict__ codes, int64_t n, int64_t G, int64_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = codes[i] / G;
+}
+
+__global__ void iota_kernel(int64_t* out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = i;
+}
+
+int64_t run_length(laq_ctx* ctx, const int64_t* sorted, int64_t n, int64_t* uniq, int64_t* counts) {
+  if (n == 0) return 0;
+  int64_t* d_runs = ctx->d_flags + 48;
+  size_t b = 0;
+  LAQ_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, b, sorted, uniq, counts, d_runs, n, ctx->stream));
+  DevBuf<char> tmp(ctx, b);
+  LAQ_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.get(), b, sorted, uniq, counts, d_runs, n, ctx->stream));
+  ++ctx->launches;
+  LAQ_CUDA(cudaMemcpyAsync(ctx->h_pinned, d_runs, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  return ctx->h_pinned[0];
+}
+
+void sort_keys(laq_ctx* ctx, const int64_t* kin, int64_t* kout, int64_t n) {
+  if (n == 0) return;
+  size_t b = 0;
+  LAQ_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, b, kin, kout, n, 0, 64, ctx->stream));
+  DevBuf<char> tmp(ctx, b);
+  LAQ_CUDA(cub::DeviceRadixSort::SortKeys(tmp.get(), b, kin, kout, n, 0, 64, ctx->stream));
+  ++ctx->launches;
+}
+
+void sort_pairs(laq_ctx* ctx, const int64_t* kin, int64_t* kout, const int64_t* vin, int64_t* vout, int64_t n) {
+  if (n == 0) return;
+  size_t b = 0;
+  LAQ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, kin, kout, vin, vout, n, 0, 64, ctx->stream));
+  DevBuf<char> tmp(ctx, b);
+  LAQ_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), b, kin, kout, vin, vout, n, 0, 64, ctx->stream));
+  ++ctx->launches;
+}
+
+// Sorted distinct values of a column (signed int64; radix sort is signed-aware).
+int64_t distinct_of(laq_ctx* ctx, const int64_t* col, int64_t n, DevBuf<int64_t>& out) {
+  out = DevBuf<int64_t>(ctx, std::max<int64_t>(n, 1));
+  if (n == 0) return 0;
+  DevBuf<int64_t> sorted(ctx, n);
+  sort_keys(ctx, col, sorted.get(), n);
+  int64_t* d_num = ctx->d_flags + 49;
+  size_t b = 0;
+  LAQ_CUDA(cub::DeviceSelect::Unique(nullptr, b, sorted.get(), out.get(), d_num, n, ctx->stream));
+  DevBuf<char> tmp(ctx, b);
+  LAQ_CUDA(cub::DeviceSelect::Unique(tmp.get(), b, sorted.get(), out.get(), d_num, n, ctx->stream));
+  ++ctx->launches;
+  LAQ_CUDA(cudaMemcpyAsync(ctx->h_pinned, d_num, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  return ctx->h_pinned[0];
+}
+
+}  // namespace
+}  // namespace laq
+
+using namespace laq;
+
+extern "C" {
+
+int laq_groupby_sum_single(laq_ctx* ctx, const int64_t* kr, const double* vr, int64_t nr, const int64_t* ks,
+                           const int64_t* gs, int64_t ns, int64_t* out_groups, double* out_sums, int64_t* h_n) {
+  return guard(ctx, [&] {
+    // build_key_domain(keys_r, keys_s): negative keys are a DomainError.
+    int64_t mn, mx;
+    if (nr) { minmax_i64(ctx, kr, nr, &mn, &mx); if (mn < 0) fail(LAQ_ERR_DOMAIN, "negative join key " + std::to_string(mn)); }
+    if (ns) { minmax_i64(ctx, ks, ns, &mn, &mx); if (mn < 0) fail(LAQ_ERR_DOMAIN, "negative join key " + std::to_string(mn)); }
+    // Groups: distinct group_s ascending (laqops.cpp:385-387).
+    DevBuf<int64_t> groups, dkeys;
+    const int64_t G = distinct_of(ctx, gs, ns, groups);
+    *h_n = G;
+    if (G == 0) return;
+    const int64_t NK = distinct_of(ctx, ks, ns, dkeys);
+    if (NK > 0 && G > INT64_MAX / NK) fail(LAQ_ERR_UNSUPPORTED, "groupby_sum_single: key x group space overflows");
+    // key->group matrix with multiplicities (csr_from_triplets sums duplicates).
+    DevBuf<int64_t> codes(ctx, ns), sorted(ctx, ns), uniq(ctx, ns), cnt(ctx, ns);
+    const int g = ctx->sm_count * 8;
+    pair_code_kernel<<<grid_for(ns, 256, g), 256, 0, ctx->stream>>>(ks, gs, ns, dkeys.get(), NK, groups.get(), G,
+                                                                    codes.get());
+    launched(ctx);
+    sort_keys(ctx, codes.get(), sorted.get(), ns);
+    const int64_t npairs = run_length(ctx, sorted.get(), ns, uniq.get(), cnt.get());
+    // Per key index: the range of its (group, multiplicity) pairs.
+    DevBuf<int64_t> kop(ctx, npairs), kuniq(ctx, npairs), kcnt(ctx, npairs), key_off(ctx, NK + 1);
+    key_of_pair<<<grid_for(npairs, 256, g), 256, 0, ctx->stream>>>(uniq.get(), npairs, G, kop.get());
+    launched(ctx);
+    const int64_t nk2 = run_length(ctx, kop.get(), npairs, kuniq.get(), kcnt.get());
+    if (nk2 != NK) fail(LAQ_ERR_GENERIC, "groupby_sum_single: key runs mismatch");
+    int64_t total = 0;
+    exclusive_scan_i64(ctx, kcnt.get(), key_off.get(), NK, &total);
+    ctx->h_pinned[8] = total;
+    LAQ_CUDA(cudaMemcpyAsync(key_off.get() + NK, &ctx->h_pinned[8], sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+    LAQ_CUDA(cudaMemsetAsync(out_sums, 0, G * sizeof(double), ctx->stream));
+    if (nr) {
+      single_accumulate<<<grid_for(nr, 256, g), 256, 0, ctx->stream>>>(kr, vr, nr, dkeys.get(), NK, key_off.get(),
+                                                                       uniq.get(), cnt.get(), G, out_sums);
+      launched(ctx);
+    }
+    LAQ_CUDA(cudaMemcpyAsync(out_groups, groups.get(), G * sizeof(int64_t), cudaMemcpyDeviceToDevice, ctx->stream));
+    sync(ctx);
+  });
+}
+
+int laq_groupby_sum_multi(laq_ctx* ctx, int32_t n_cols, const int64_t* const* d_cols, const double* d_vals, int64_t n,
+                          int64_t* d_out_keys, double* d_out_sums, int64_t capacity, int64_t* h_n_groups) {
+  return guard(ctx, [&] {
+    if (n_cols < 1) fail(LAQ_ERR_SHAPE, "groupby_sum_multi: no group columns");
+    *h_n_groups = 0;
+    if (n == 0) return;
+    const int g = ctx->sm_count * 8;
+    std::vector<DevBuf<int64_t>> distinct(n_cols);
+    std::vector<int64_t> nd(n_cols), stride(n_cols);
+    for (int c = 0; c < n_cols; ++c) nd[c] = distinct_of(ctx, d_cols[c], n, distinct[c]);
+    int64_t s = 1;
+    for (int c = n_cols - 1; c >= 0; --c) {
+      stride[c] = s;
+      if (s > (INT64_MAX / 2) / nd[c]) fail(LAQ_ERR_UNSUPPORTED, "groupby_sum_multi: tuple space exceeds 2^62");
+      s *= nd[c];
+    }
+    DevBuf<int64_t> code(ctx, n), iota(ctx, n), scode(ctx, n), srow(ctx, n);
+    for (int c = 0; c < n_cols; ++c) {
+      rank_kernel<<<grid_for(n, 256, g), 256, 0, ctx->stream>>>(d_cols[c], n, distinct[c].get(), nd[c], stride[c],
+                                                               code.get(), c > 0);
+      launched(ctx);
+    }
+    iota_kernel<<<grid_for(n, 256, g), 256, 0, ctx->stream>>>(iota.get(), n);
+    launched(ctx);
+    // Stable: rows stay ascending within a tuple (laqops.cpp:424-429).
+    sort_pairs(ctx, code.get(), scode.get(), iota.get(), srow.get(), n);
+    DevBuf<int64_t> uniq(ctx, n), cnt(ctx, n), off(ctx, n + 1);
+    const int64_t G = run_length(ctx, scode.get(), n, uniq.get(), cnt.get());
+    if (G > capacity) fail(LAQ_ERR_CAPACITY, "groupby_sum_multi: output capacity");
+    int64_t total = 0;
+    exclusive_scan_i64(ctx, cnt.get(), off.get(), G, &total);
+    ctx->h_pinned[8] = total;
+    LAQ_CUDA(cudaMemcpyAsync(off.get() + G, &ctx->h_pinned[8], sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+    segsum_kernel<<<grid_for(G, 128, g), 128, 0, ctx->stream>>>(off.get(), G, srow.get(), d_vals, d_out_sums);
+    launched(ctx);
+    for (int c = 0; c < n_cols; ++c) {
+      decode_kernel<<<grid_for(G, 256, g), 256, 0, ctx->stream>>>(uniq.get(), G, distinct[c].get(), stride[c], nd[c],
+                                                                 d_out_keys + c * capacity);
+      launched(ctx);
+    }
+    sync(ctx);
+    *h_n_groups = G;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,335 @@
+// K1 domain_build and the general (many-to-many) join-MM.
+//
+// build_key_domain (laqops.cpp:142-155) is "sorted distinct union".  For key
+// ranges up to 2^31 we never sort: a bitmap over [min, max] (atomicOr), a
+// per-word popcount, an exclusive scan of the counts, and an emit pass that
+// writes each set bit's key at  offset[word] + popc(word & lower bits)  --
+// ascending order for free, and that same rank is KeyDomain::position.
+// Wider key spaces fall back to an on-device radix sort + unique.
+//
+// mm_join (laqops.cpp:222-231) = spmm(key_matrix(R), key_matrix(S)^T): S is
+// bucketed by key with a stable radix sort (the DomainByRows CSR of S:
+// buckets ascending, rows ascending within a bucket), each R row probes its
+// bucket, a scan of bucket sizes gives output offsets, and the pairs are
+// written in canonical (r asc, s asc) order.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "probe.cuh"
+
+namespace laq {
+namespace {
+
+__global__ void bitmap_set(const int64_t* __restrict__ k, int64_t n, int64_t base, unsigned* bits) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = k[i] - base;
+    atomicOr(bits + (o >> 5), 1u << (o & 31));
+  }
+}
+
+__global__ void bitmap_popc(const unsigned* __restrict__ bits, int64_t words, int64_t* cnt) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x)
+    cnt[w] = __popc(bits[w]);
+}
+
+__global__ void bitmap_emit(const unsigned* __restrict__ bits, const int64_t* __restrict__ off, int64_t words,
+                            int64_t base, int64_t* out) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
+    unsigned b = bits[w];
+    int64_t o = off[w];
+    while (b) {
+      const int bit = __ffs(b) - 1;
+      out[o++] = base + w * 32 + bit;
+      b &= b - 1;
+    }
+  }
+}
+
+__global__ void copy_i64(const int64_t* __restrict__ a, int64_t na, const int64_t* __restrict__ b, int64_t nb,
+                         int64_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < na + nb; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = i < na ? a[i] : b[i - na];
+}
+
+// Sorted distinct keys of the concatenation a ++ b into out; returns count.
+int64_t distinct_sorted(laq_ctx* ctx, const int64_t* a, int64_t na, const int64_t* b, int64_t nb, int64_t* out,
+                        const char* what) {
+  const int64_t n = na + nb;
+  if (n == 0) return 0;
+  int64_t mn = INT64_MAX, mx = INT64_MIN, t0, t1;
+  if (na) { minmax_i64(ctx, a, na, &t0, &t1); mn = std::min(mn, t0); mx = std::max(mx, t1); }
+  if (nb) { minmax_i64(ctx, b, nb, &t0, &t1); mn = std::min(mn, t0); mx = std::max(mx, t1); }
+  if (mn < 0) fail(LAQ_ERR_DOMAIN, std::string(what) + std::to_string(mn));
+  const int64_t range = mx - mn + 1;
+  if (range <= (int64_t{1} << 31)) {
+    const int64_t words = (range + 31) / 32;
+    DevBuf<unsigned> bits(ctx, words);
+    DevBuf<int64_t> cnt(ctx, words);
+    LAQ_CUDA(cudaMemsetAsync(bits.get(), 0, words * sizeof(unsigned), ctx->stream));
+    const int g = ctx->sm_count * 8;
+    if (na) { bitmap_set<<<grid_for(na, 256, g), 256, 0, ctx->stream>>>(a, na, mn, bits.get()); launched(ctx); }
+    if (nb) { bitmap_set<<<grid_for(nb, 256, g), 256, 0, ctx->stream>>>(b, nb, mn, bits.get()); launched(ctx); }
+    bitmap_popc<<<grid_for(words, 256, g), 256, 0, ctx->stream>>>(bits.get(), words, cnt.get());
+    launched(ctx);
+    int64_t total = 0;
+    exclusive_scan_i64(ctx, cnt.get(), cnt.get(), words, &total);
+    bitmap_emit<<<grid_for(words, 256, g), 256, 0, ctx->stream>>>(bits.get(), cnt.get(), words, mn, out);
+    launched(ctx);
+    return total;
+  }
+  // Wide key space: radix sort + unique.
+  DevBuf<int64_t> cat(ctx, n), sorted(ctx, n);
+  copy_i64<<<grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(a, na, b, nb, cat.get());
+  launched(ctx);
+  size_t bytes = 0;
+  LAQ_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, cat.get(), sorted.get(), n, 0, 64, ctx->stream));
+  DevBuf<char> tmp(ctx, bytes);
+  LAQ_CUDA(cub::DeviceRadixSort::SortKeys(tmp.get(), bytes, cat.get(), sorted.get(), n, 0, 64, ctx->stream));
+  ++ctx->launches;
+  int64_t* d_num = ctx->d_flags + 40;
+  size_t b2 = 0;
+  LAQ_CUDA(cub::DeviceSelect::Unique(nullptr, b2, sorted.get(), out, d_num, n, ctx->stream));
+  DevBuf<char> tmp2(ctx, b2);
+  LAQ_CUDA(cub::DeviceSelect::Unique(tmp2.get(), b2, sorted.get(), out, d_num, n, ctx->stream));
+  ++ctx->launches;
+  LAQ_CUDA(cudaMemcpyAsync(ctx->h_pinned, d_num, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  return ctx->h_pinned[0];
+}
+
+__global__ void positions_kernel(const int64_t* __restrict__ keys, int64_t n, const ProbeView pv, int64_t* pos,
+                                 int* missing) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = keys[i] < 0 ? -1 : pv.row(keys[i]);
+    if (r < 0) atomicOr(missing, 1);
+    pos[i] = r;
+  }
+}
+
+// Positions of keys in a sorted distinct domain (DomainError if absent).
+void positions(laq_ctx* ctx, const int64_t* keys, int64_t n, const int64_t* domain, int64_t d, int64_t* pos,
+               Probe& probe_out) {
+  build_probe(ctx, domain, nullptr, d, probe_out, "key domain has duplicate keys");
+  int* missing = reinterpret_cast<int*>(ctx->d_flags + 41);
+  LAQ_CUDA(cudaMemsetAsync(missing, 0, sizeof(int), ctx->stream));
+  if (n) {
+    positions_kernel<<<grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(keys, n, probe_out.view(), pos,
+                                                                                  missing);
+    launched(ctx);
+  }
+  LAQ_CUDA(cudaMemcpyAsync(ctx->h_pinned, missing, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  if (*reinterpret_cast<int*>(ctx->h_pinned)) fail(LAQ_ERR_DOMAIN, "key not in domain");
+}
+
+__global__ void iota_i64(int64_t* out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = i;
+}
+
+__global__ void histogram_kernel(const int64_t* __restrict__ pos, int64_t n, unsigned long long* cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(cnt + pos[i], 1ull);
+}
+
+__global__ void nonzero_flags(const double* __restrict__ v, int64_t n, char* flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    flags[i] = v[i] != 0.0;
+}
+
+__global__ void gather_values(const double* __restrict__ v, const int64_t* __restrict__ idx, int64_t m, double* out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = v ? v[idx[t]] : 1.0;
+}
+
+// mm_join: per R row, bucket lookup; write pairs.
+__global__ void mm_count(const int64_t* __restrict__ r, int64_t nr, const ProbeView pv, const int64_t* __restrict__ run_off,
+                         int64_t* cnt, int64_t* run_of_r) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nr; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = pv.row(r[i]);
+    run_of_r[i] = u;
+    cnt[i] = u < 0 ? 0 : run_off[u + 1] - run_off[u];
+  }
+}
+
+__global__ void mm_write(int64_t nr, const int64_t* __restrict__ run_of_r, const int64_t* __restrict__ run_off,
+                         const int64_t* __restrict__ s_sorted_idx, const int64_t* __restrict__ out_off, int64_t* out_r,
+                         int64_t* out_s) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nr; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t u = run_of_r[i];
+    if (u < 0) continue;
+    int64_t o = out_off[i];
+    for (int64_t t = run_off[u]; t < run_off[u + 1]; ++t, ++o) {
+      out_r[o] = i;
+      out_s[o] = s_sorted_idx[t];
+    }
+  }
+}
+
+}  // namespace
+
+// Shared with groupby.cu: S rows bucketed by key (stable), distinct keys probe.
+struct Buckets {
+  DevBuf<int64_t> sorted_keys, sorted_idx, uniq, run_off;
+  int64_t n_uniq = 0;
+  Probe probe;  // over uniq keys: row = run index
+};
+
+void bucket_by_key(laq_ctx* ctx, const int64_t* keys, int64_t n, Buckets& b) {
+  b.sorted_keys = DevBuf<int64_t>(ctx, std::max<int64_t>(n, 1));
+  b.sorted_idx = DevBuf<int64_t>(ctx, std::max<int64_t>(n, 1));
+  b.uniq = DevBuf<int64_t>(ctx, std::max<int64_t>(n, 1));
+  b.run_off = DevBuf<int64_t>(ctx, n + 1);
+  if (n == 0) {
+    LAQ_CUDA(cudaMemsetAsync(b.run_off.get(), 0, sizeof(int64_t), ctx->stream));
+    b.n_uniq = 0;
+    build_probe(ctx, b.uniq.get(), nullptr, 0, b.probe, "");
+    return;
+  }
+  DevBuf<int64_t> iota(ctx, n);
+  iota_i64<<<grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(iota.get(), n);
+  launched(ctx);
+  size_t bytes = 0;
+  LAQ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, b.sorted_keys.get(), iota.get(), b.sorted_idx.get(), n,
+                                           0, 64, ctx->stream));
+  DevBuf<char> tmp(ctx, bytes);
+  LAQ_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, keys, b.sorted_keys.get(), iota.get(), b.sorted_idx.get(),
+                                           n, 0, 64, ctx->stream));
+  ++ctx->launches;
+  DevBuf<int64_t> counts(ctx, n);
+  int64_t* d_runs = ctx->d_flags + 42;
+  size_t b2 = 0;
+  LAQ_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, b2, b.sorted_keys.get(), b.uniq.get(), counts.get(), d_runs, n,
+                                              ctx->stream));
+  DevBuf<char> tmp2(ctx, b2);
+  LAQ_CUDA(cub::DeviceRunLengthEncode::Encode(tmp2.get(), b2, b.sorted_keys.get(), b.uniq.get(), counts.get(), d_runs,
+                                              n, ctx->stream));
+  ++ctx->launches;
+  LAQ_CUDA(cudaMemcpyAsync(ctx->h_pinned, d_runs, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  b.n_uniq = ctx->h_pinned[0];
+  int64_t total = 0;
+  exclusive_scan_i64(ctx, counts.get(), b.run_off.get(), b.n_uniq, &total);
+  ctx->h_pinned[8] = total;
+  LAQ_CUDA(cudaMemcpyAsync(b.run_off.get() + b.n_uniq, &ctx->h_pinned[8], sizeof(int64_t), cudaMemcpyHostToDevice,
+                           ctx->stream));
+  sync(ctx);
+  build_probe(ctx, b.uniq.get(), nullptr, b.n_uniq, b.probe, "");
+}
+
+}  // namespace laq
+
+using namespace laq;
+
+extern "C" {
+
+int laq_build_key_domain(laq_ctx* ctx, const int64_t* r, int64_t nr, const int64_t* s, int64_t ns, int64_t* out,
+                         int64_t* h_size) {
+  return guard(ctx, [&] { *h_size = distinct_sorted(ctx, r, nr, s, ns, out, "negative join key "); });
+}
+
+int laq_update_key_domain(laq_ctx* ctx, const int64_t* dom, int64_t d, const int64_t* nk, int64_t nn, int64_t* out,
+                          int64_t* h_size) {
+  // Merging into a sorted distinct domain == the distinct union (laqops.cpp:157-171).
+  return guard(ctx, [&] { *h_size = distinct_sorted(ctx, dom, d, nk, nn, out, "negative join key "); });
+}
+
+int laq_key_positions(laq_ctx* ctx, const int64_t* keys, int64_t n, const int64_t* domain, int64_t d, int64_t* pos) {
+  return guard(ctx, [&] {
+    Probe p;
+    positions(ctx, keys, n, domain, d, pos, p);
+  });
+}
+
+int laq_key_matrix_dbr(laq_ctx* ctx, const int64_t* keys, int64_t n, const int64_t* domain, int64_t d,
+                       const double* values, int64_t* row_ptr, int64_t* col_idx, double* out_values, int64_t* h_nnz) {
+  return guard(ctx, [&] {
+    // Counting sort by domain position; rows ascending within a position
+    // (laqops.cpp:196-218).  Entries with value exactly 0.0 are validated but not stored.
+    DevBuf<int64_t> pos(ctx, std::max<int64_t>(n, 1));
+    Probe p;
+    positions(ctx, keys, n, domain, d, pos.get(), p);
+    // Keep-mask compaction (stable) for valued matrices.
+    DevBuf<int64_t> kpos(ctx, std::max<int64_t>(n, 1)), kidx(ctx, std::max<int64_t>(n, 1));
+    int64_t m = n;
+    DevBuf<int64_t> iota(ctx, std::max<int64_t>(n, 1));
+    if (n) {
+      iota_i64<<<grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(iota.get(), n);
+      launched(ctx);
+    }
+    if (values && n) {
+      DevBuf<char> flags(ctx, n);
+      nonzero_flags<<<grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(values, n, flags.get());
+      launched(ctx);
+      int64_t* d_cnt = ctx->d_flags + 43;
+      size_t b = 0;
+      LAQ_CUDA(cub::DeviceSelect::Flagged(nullptr, b, pos.get(), flags.get(), kpos.get(), d_cnt, n, ctx->stream));
+      DevBuf<char> t(ctx, b);
+      LAQ_CUDA(cub::DeviceSelect::Flagged(t.get(), b, pos.get(), flags.get(), kpos.get(), d_cnt, n, ctx->stream));
+      LAQ_CUDA(cub::DeviceSelect::Flagged(t.get(), b, iota.get(), flags.get(), kidx.get(), d_cnt, n, ctx->stream));
+      ctx->launches += 2;
+      LAQ_CUDA(cudaMemcpyAsync(ctx->h_pinned, d_cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+      sync(ctx);
+      m = ctx->h_pinned[0];
+    } else if (n) {
+      LAQ_CUDA(cudaMemcpyAsync(kpos.get(), pos.get(), n * sizeof(int64_t), cudaMemcpyDeviceToDevice, ctx->stream));
+      LAQ_CUDA(cudaMemcpyAsync(kidx.get(), iota.get(), n * sizeof(int64_t), cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    // Stable sort of (pos, row) by pos -> col_idx; histogram + scan -> row_ptr.
+    DevBuf<int64_t> spos(ctx, std::max<int64_t>(m, 1));
+    if (m) {
+      size_t bytes = 0;
+      LAQ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kpos.get(), spos.get(), kidx.get(), col_idx, m, 0, 64,
+                                               ctx->stream));
+      DevBuf<char> tmp(ctx, bytes);
+      LAQ_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, kpos.get(), spos.get(), kidx.get(), col_idx, m, 0, 64,
+                                               ctx->stream));
+      ++ctx->launches;
+    }
+    DevBuf<unsigned long long> cnt(ctx, d + 1);
+    LAQ_CUDA(cudaMemsetAsync(cnt.get(), 0, (d + 1) * sizeof(unsigned long long), ctx->stream));
+    if (m) {
+      histogram_kernel<<<grid_for(m, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(kpos.get(), m, cnt.get());
+      launched(ctx);
+    }
+    exclusive_scan_i64(ctx, reinterpret_cast<int64_t*>(cnt.get()), row_ptr, d + 1, nullptr);
+    if (out_values && m) {
+      gather_values<<<grid_for(m, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(values, col_idx, m, out_values);
+      launched(ctx);
+    }
+    sync(ctx);
+    *h_nnz = m;
+  });
+}
+
+int laq_mm_join(laq_ctx* ctx, const int64_t* r, int64_t nr, const int64_t* s, int64_t ns, int64_t* out_r,
+                int64_t* out_s, int64_t capacity, int64_t* h_nnz) {
+  return guard(ctx, [&] {
+    // Domain validation as build_key_domain(keys_r, keys_s) (negative keys).
+    int64_t mn, mx;
+    if (nr) { minmax_i64(ctx, r, nr, &mn, &mx); if (mn < 0) fail(LAQ_ERR_DOMAIN, "negative join key " + std::to_string(mn)); }
+    if (ns) { minmax_i64(ctx, s, ns, &mn, &mx); if (mn < 0) fail(LAQ_ERR_DOMAIN, "negative join key " + std::to_string(mn)); }
+    Buckets b;
+    bucket_by_key(ctx, s, ns, b);
+    DevBuf<int64_t> cnt(ctx, std::max<int64_t>(nr, 1)), run_of_r(ctx, std::max<int64_t>(nr, 1)),
+        off(ctx, std::max<int64_t>(nr, 1));
+    int64_t total = 0;
+    if (nr) {
+      mm_count<<<grid_for(nr, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(r, nr, b.probe.view(), b.run_off.get(),
+                                                                              cnt.get(), run_of_r.get());
+      launched(ctx);
+      exclusive_scan_i64(ctx, cnt.get(), off.get(), nr, &total);
+    }
+    *h_nnz = total;
+    if (total > capacity) fail(LAQ_ERR_CAPACITY, "mm_join: output capacity " + std::to_string(capacity) + " < " + std::to_string(total));
+    if (nr && total) {
+      mm_write<<<grid_for(nr, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(nr, run_of_r.get(), b.run_off.get(),
+                                                                              b.sorted_idx.get(), off.get(), out_r, out_s);
+      launched(ctx);
+      sync(ctx);
+    }
+  });
+}
+
+}  // extern "C"

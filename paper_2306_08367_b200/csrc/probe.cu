@@ -1,0 +1,547 @@
+// K2 star_probe + K3 fused_gather_sum: the star join evaluated as probes into
+// one-hot key tables (probe.cuh), stable survivor compaction with a
+// single-pass decoupled look-back scan, and the fused join+predict
+//   Y[m] = ((P_0[row_0(m)] + P_1[row_1(m)]) + ...)
+// for the m-th surviving fact row (fusion.cpp:64-77 association order; the
+// one-hot gathers are exact, so the result is bit-identical to the reference).
+//
+// HBM traffic per fact row: 4*J bytes of int32 keys in, 8*l bytes of fp64
+// predictions out (partials P_j are L2/L1 resident: r_j*l*8 bytes each).
+#include <cub/block/block_scan.cuh>
+
+#include <algorithm>
+
+#include "probe.cuh"
+
+namespace laq {
+
+namespace {
+
+constexpr int kMaxLinks = 8;
+constexpr int kBlock = 256;
+constexpr int kItems = 8;               // consecutive fact rows per thread
+constexpr int kTile = kBlock * kItems;  // 2048 rows per tile
+
+// ---------------------------------------------------------------------------
+// probe construction
+// ---------------------------------------------------------------------------
+
+template <class K>
+__global__ void direct_insert(const K* __restrict__ pk, int64_t n, int64_t base, int32_t* rows, int32_t* row_slot,
+                              int* dup) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = static_cast<int64_t>(pk[r]) - base;
+    const int32_t prev = atomicCAS(rows + s, -1, static_cast<int32_t>(r));
+    if (prev != -1) atomicOr(dup, 1);
+    row_slot[r] = static_cast<int32_t>(s);
+  }
+}
+
+template <class K>
+__global__ void hash_insert(const K* __restrict__ pk, int64_t n, int64_t cap, unsigned long long* keys, int32_t* rows,
+                            int32_t* row_slot, int* dup) {
+  const uint64_t mask = static_cast<uint64_t>(cap) - 1;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t key = static_cast<int64_t>(pk[r]);
+    uint64_t h = static_cast<uint64_t>(key) * 0x9E3779B97F4A7C15ull;
+    h ^= h >> 29;
+    for (uint64_t s = h & mask;; s = (s + 1) & mask) {
+      const unsigned long long prev = atomicCAS(keys + s, ~0ull, static_cast<unsigned long long>(key));
+      if (prev == ~0ull) {
+        rows[s] = static_cast<int32_t>(r);
+        row_slot[r] = static_cast<int32_t>(s);
+        break;
+      }
+      if (prev == static_cast<unsigned long long>(key)) {
+        atomicOr(dup, 1);
+        row_slot[r] = static_cast<int32_t>(s);
+        break;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+void build_probe(laq_ctx* ctx, const int64_t* d_pk64, const int32_t* d_pk32, int64_t n, Probe& out,
+                 const std::string& what) {
+  out = Probe();
+  out.n_rows = n;
+  if (n == 0) return;  // DIRECT with size 0: every probe misses
+  if (n > INT32_MAX) fail(LAQ_ERR_CAPACITY, "dimension has more than 2^31 rows");
+  int64_t mn, mx;
+  if (d_pk64) minmax_i64(ctx, d_pk64, n, &mn, &mx);
+  else minmax_i32(ctx, d_pk32, n, &mn, &mx);
+  if (mn < 0) fail(LAQ_ERR_DOMAIN, "negative join key " + std::to_string(mn));
+  const int64_t range = mx - mn + 1;
+  int* dup = reinterpret_cast<int*>(ctx->d_flags + 8);
+  LAQ_CUDA(cudaMemsetAsync(dup, 0, sizeof(int), ctx->stream));
+  out.row_slot = DevMem<int32_t>(n);
+  const int grid = grid_for(n, 256, ctx->sm_count * 8);
+  if (range <= std::max<int64_t>(4 * n, int64_t{1} << 20) && range < (int64_t{1} << 31)) {
+    out.kind = PROBE_DIRECT;
+    out.base = mn;
+    out.size = range;
+    out.rows = DevMem<int32_t>(range);
+    LAQ_CUDA(cudaMemsetAsync(out.rows.get(), 0xFF, range * sizeof(int32_t), ctx->stream));
+    if (d_pk64) direct_insert<<<grid, 256, 0, ctx->stream>>>(d_pk64, n, mn, out.rows.get(), out.row_slot.get(), dup);
+    else direct_insert<<<grid, 256, 0, ctx->stream>>>(d_pk32, n, mn, out.rows.get(), out.row_slot.get(), dup);
+    launched(ctx);
+  } else {
+    int64_t cap = 1024;
+    while (cap < 2 * n) cap <<= 1;
+    out.kind = PROBE_HASH;
+    out.size = cap;
+    out.keys = DevMem<int64_t>(cap);
+    out.rows = DevMem<int32_t>(cap);
+    LAQ_CUDA(cudaMemsetAsync(out.keys.get(), 0xFF, cap * sizeof(int64_t), ctx->stream));
+    LAQ_CUDA(cudaMemsetAsync(out.rows.get(), 0xFF, cap * sizeof(int32_t), ctx->stream));
+    auto* k = reinterpret_cast<unsigned long long*>(out.keys.get());
+    if (d_pk64) hash_insert<<<grid, 256, 0, ctx->stream>>>(d_pk64, n, cap, k, out.rows.get(), out.row_slot.get(), dup);
+    else hash_insert<<<grid, 256, 0, ctx->stream>>>(d_pk32, n, cap, k, out.rows.get(), out.row_slot.get(), dup);
+    launched(ctx);
+  }
+  LAQ_CUDA(cudaMemcpyAsync(ctx->h_pinned, dup, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  if (*reinterpret_cast<int*>(ctx->h_pinned) != 0) fail(LAQ_ERR_DUPLICATE_KEY, what);
+}
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// the star compaction kernel (K2, optionally fused with K3)
+// ---------------------------------------------------------------------------
+
+template <class K>
+struct StarArgs {
+  int n_links;
+  int64_t n;
+  const K* fk[kMaxLinks];
+  ProbeView probe[kMaxLinks];
+  // outputs (each optional)
+  int64_t* survivors;
+  int64_t* rows64[kMaxLinks];
+  int32_t* rows32[kMaxLinks];
+  // fused predict (l <= 8): y[m*l + c] = sum_j partial[j][row_j*l + c]
+  const double* partial[kMaxLinks];
+  int64_t l;
+  double* y;
+  // decoupled look-back
+  unsigned long long* tile_state;
+  int* tile_counter;
+  int64_t* nnz;  // device: total survivors (written by the last tile)
+  int64_t n_tiles;
+  int* err;      // bit 0: negative key among live rows
+};
+
+constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+template <class K>
+__device__ __forceinline__ void load_keys(const K* __restrict__ p, int64_t row0, int64_t n, int64_t (&k)[kItems]) {
+  if (row0 + kItems <= n && (reinterpret_cast<uintptr_t>(p + row0) & 15) == 0) {
+    if constexpr (sizeof(K) == 4) {
+      const int4 a = __ldcs(reinterpret_cast<const int4*>(p + row0));
+      const int4 b = __ldcs(reinterpret_cast<const int4*>(p + row0) + 1);
+      k[0] = a.x; k[1] = a.y; k[2] = a.z; k[3] = a.w; k[4] = b.x; k[5] = b.y; k[6] = b.z; k[7] = b.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < kItems; i += 2) {
+        const longlong2 v = __ldcs(reinterpret_cast<const longlong2*>(p + row0 + i));
+        k[i] = v.x;
+        k[i + 1] = v.y;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) k[i] = row0 + i < n ? static_cast<int64_t>(p[row0 + i]) : -1;
+  }
+}
+
+template <class K, int NL, bool kPredict>
+__global__ void __launch_bounds__(kBlock) star_kernel(const StarArgs<K> a) {
+  using Scan = cub::BlockScan<int, kBlock>;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ int64_t s_tile;
+  __shared__ unsigned long long s_prefix;
+
+  if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t row0 = tile * kTile + static_cast<int64_t>(threadIdx.x) * kItems;
+
+  int32_t rows[NL][kItems];
+  bool alive[kItems];
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) alive[i] = row0 + i < a.n;
+
+  int neg = 0;
+#pragma unroll
+  for (int j = 0; j < NL; ++j) {
+    int64_t keys[kItems];
+    load_keys<K>(a.fk[j], row0, a.n, keys);
+    const ProbeView pv = a.probe[j];
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      int32_t r = -1;
+      if (alive[i]) {
+        if (keys[i] < 0) neg = 1;
+        r = pv.row(keys[i]);
+        alive[i] = r >= 0;
+      }
+      rows[j][i] = r;
+    }
+  }
+  if (neg) atomicOr(a.err, 1);
+
+  int count = 0;
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) count += alive[i] ? 1 : 0;
+  int excl, total;
+  Scan(scan_tmp).ExclusiveSum(count, excl, total);
+
+  if (threadIdx.x == 0) {
+    unsigned long long prefix = 0;
+    if (tile == 0) {
+      atomicExch(a.tile_state, kFlagInc | static_cast<unsigned long long>(total));
+    } else {
+      atomicExch(a.tile_state + tile, kFlagAgg | static_cast<unsigned long long>(total));
+      int64_t p = tile - 1;
+      while (true) {
+        const unsigned long long s = *reinterpret_cast<volatile unsigned long long*>(a.tile_state + p);
+        const unsigned long long f = s & ~kValMask;
+        if (f == 0) continue;  // predecessor not published yet
+        prefix += s & kValMask;
+        if (f == kFlagInc) break;
+        --p;
+      }
+      atomicExch(a.tile_state + tile, kFlagInc | (prefix + static_cast<unsigned long long>(total)));
+    }
+    if (tile == a.n_tiles - 1) *a.nnz = static_cast<int64_t>(prefix) + total;
+    s_prefix = prefix;
+  }
+  __syncthreads();
+  int64_t pos = static_cast<int64_t>(s_prefix) + excl;
+
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    if (!alive[i]) continue;
+    if (a.survivors) a.survivors[pos] = row0 + i;
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+      if (a.rows64[j]) a.rows64[j][pos] = rows[j][i];
+      if (a.rows32[j]) a.rows32[j][pos] = rows[j][i];
+    }
+    if constexpr (kPredict) {
+      for (int64_t c = 0; c < a.l; ++c) {
+        double acc = __dadd_rn(0.0, __ldg(a.partial[0] + static_cast<int64_t>(rows[0][i]) * a.l + c));  // 0 + 1*x (spmm_dense)
+#pragma unroll
+        for (int j = 1; j < NL; ++j) acc = __dadd_rn(acc, __ldg(a.partial[j] + static_cast<int64_t>(rows[j][i]) * a.l + c));
+        __stcs(a.y + pos * a.l + c, acc);
+      }
+    }
+    ++pos;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// apply_fused_linear over explicit row maps (fusion.cpp:64-77)
+// ---------------------------------------------------------------------------
+
+template <class I>
+struct ApplyArgs {
+  int n_parts;
+  int64_t rows;
+  int64_t l;
+  const I* idx[kMaxLinks];
+  const double* partial[kMaxLinks];
+  double* out;
+};
+
+// l <= 8: one thread per target row.
+template <class I>
+__global__ void apply_rows_kernel(const ApplyArgs<I> a) {
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < a.rows; m += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r[kMaxLinks];
+    for (int j = 0; j < a.n_parts; ++j) r[j] = static_cast<int64_t>(a.idx[j][m]);
+    for (int64_t c = 0; c < a.l; ++c) {
+      double acc = __dadd_rn(0.0, __ldg(a.partial[0] + r[0] * a.l + c));  // 0 + 1*x (spmm_dense)
+      for (int j = 1; j < a.n_parts; ++j) acc = __dadd_rn(acc, __ldg(a.partial[j] + r[j] * a.l + c));
+      __stcs(a.out + m * a.l + c, acc);
+    }
+  }
+}
+
+// l > 8: one warp per target row, lanes across the output width.
+template <class I>
+__global__ void apply_warp_kernel(const ApplyArgs<I> a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t m = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; m < a.rows; m += warps) {
+    int64_t r[kMaxLinks];
+    for (int j = 0; j < a.n_parts; ++j) r[j] = static_cast<int64_t>(a.idx[j][m]);
+    for (int64_t c = lane; c < a.l; c += 32) {
+      double acc = __dadd_rn(0.0, __ldg(a.partial[0] + r[0] * a.l + c));  // 0 + 1*x (spmm_dense)
+      for (int j = 1; j < a.n_parts; ++j) acc = __dadd_rn(acc, __ldg(a.partial[j] + r[j] * a.l + c));
+      __stcs(a.out + m * a.l + c, acc);
+    }
+  }
+}
+
+template <class I>
+void launch_apply(laq_ctx* ctx, const ApplyArgs<I>& a) {
+  if (a.rows == 0 || a.l == 0) return;
+  if (a.l <= 8) {
+    apply_rows_kernel<I><<<grid_for(a.rows, 256, ctx->sm_count * 16), 256, 0, ctx->stream>>>(a);
+  } else {
+    apply_warp_kernel<I><<<grid_for(a.rows, 8, ctx->sm_count * 16), 256, 0, ctx->stream>>>(a);
+  }
+  launched(ctx);
+}
+
+// ---------------------------------------------------------------------------
+// materialize (laqops.cpp:338-374): T[m, tgt] = B_j[i_j[m], src]
+// ---------------------------------------------------------------------------
+
+__global__ void materialize_kernel(const int64_t* __restrict__ idx, int64_t rows, const double* __restrict__ dim,
+                                   int64_t dim_cols, const int32_t* __restrict__ place, int64_t k,
+                                   double* __restrict__ out) {
+  const int64_t total = rows * dim_cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = e / dim_cols, c = e - m * dim_cols;
+    out[m * k + place[c]] = __dadd_rn(0.0, __ldg(dim + idx[m] * dim_cols + c));  // target += 1*x
+  }
+}
+
+}  // namespace
+
+// Lookback scratch sized for n fact rows.
+struct StarScratch {
+  DevMem<unsigned long long> tile_state;
+  DevMem<int> counter;
+  int64_t cap_tiles = 0;
+  void ensure(int64_t tiles) {
+    if (tiles <= cap_tiles) return;
+    tile_state = DevMem<unsigned long long>(tiles);
+    counter = DevMem<int>(1);
+    cap_tiles = tiles;
+  }
+};
+
+template <class K>
+void run_star(laq_ctx* ctx, StarArgs<K>& a, StarScratch& scratch, bool predict) {
+  a.n_tiles = (a.n + kTile - 1) / kTile;
+  if (a.n_tiles == 0) {
+    LAQ_CUDA(cudaMemsetAsync(a.nnz, 0, sizeof(int64_t), ctx->stream));
+    return;
+  }
+  scratch.ensure(a.n_tiles);
+  a.tile_state = scratch.tile_state.get();
+  a.tile_counter = scratch.counter.get();
+  LAQ_CUDA(cudaMemsetAsync(a.tile_state, 0, a.n_tiles * sizeof(unsigned long long), ctx->stream));
+  LAQ_CUDA(cudaMemsetAsync(a.tile_counter, 0, sizeof(int), ctx->stream));
+  const unsigned g = static_cast<unsigned>(a.n_tiles);
+  cudaStream_t s = ctx->stream;
+#define LAQ_STAR_CASE(N)                                                   \
+  case N:                                                                  \
+    if (predict) star_kernel<K, N, true><<<g, kBlock, 0, s>>>(a);          \
+    else star_kernel<K, N, false><<<g, kBlock, 0, s>>>(a);                 \
+    break;
+  switch (a.n_links) {
+    LAQ_STAR_CASE(1) LAQ_STAR_CASE(2) LAQ_STAR_CASE(3) LAQ_STAR_CASE(4)
+    LAQ_STAR_CASE(5) LAQ_STAR_CASE(6) LAQ_STAR_CASE(7) LAQ_STAR_CASE(8)
+    default: fail(LAQ_ERR_UNSUPPORTED, "star join supports 1..8 dimensions");
+  }
+#undef LAQ_STAR_CASE
+  launched(ctx);
+}
+
+}  // namespace laq
+
+using namespace laq;
+
+struct laq_probe {
+  int n_links = 0;
+  Probe probes[kMaxLinks];
+  StarScratch scratch;
+  DevMem<int> err;
+};
+
+extern "C" {
+
+int laq_star_join(laq_ctx* ctx, int32_t n_links, const int64_t* const* d_fks, int64_t n_fact,
+                  const int64_t* const* d_pks, const int64_t* h_pk_rows, int64_t* d_survivors,
+                  int64_t* const* d_dim_rows, int64_t* h_nnz) {
+  return guard(ctx, [&] {
+    if (n_links < 0 || n_links > kMaxLinks) fail(LAQ_ERR_UNSUPPORTED, "star join supports up to 8 dimensions");
+    if (n_links == 0) {  // nothing to join: every fact row survives
+      *h_nnz = n_fact;
+      fail(LAQ_ERR_UNSUPPORTED, "star join with no dimensions");
+    }
+    Probe probes[kMaxLinks];
+    for (int j = 0; j < n_links; ++j)
+      build_probe(ctx, d_pks[j], nullptr, h_pk_rows[j], probes[j], "multiway_star_join: duplicate keys in dim " + std::to_string(j));
+    StarArgs<int64_t> a{};
+    a.n_links = n_links;
+    a.n = n_fact;
+    for (int j = 0; j < n_links; ++j) {
+      a.fk[j] = d_fks[j];
+      a.probe[j] = probes[j].view();
+      a.rows64[j] = d_dim_rows ? d_dim_rows[j] : nullptr;
+    }
+    a.survivors = d_survivors;
+    a.nnz = ctx->d_flags + 16;
+    a.err = reinterpret_cast<int*>(ctx->d_flags + 17);
+    LAQ_CUDA(cudaMemsetAsync(a.err, 0, sizeof(int), ctx->stream));
+    StarScratch scratch;
+    run_star(ctx, a, scratch, false);
+    LAQ_CUDA(cudaMemcpyAsync(ctx->h_pinned, ctx->d_flags + 16, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    if (ctx->h_pinned[1] & 1) fail(LAQ_ERR_DOMAIN, "negative join key");
+    *h_nnz = ctx->h_pinned[0];
+  });
+}
+
+int laq_probe_build(laq_ctx* ctx, int32_t n_links, const int32_t* const* d_pks, const int64_t* h_pk_rows,
+                    laq_probe** out) {
+  return guard(ctx, [&] {
+    if (n_links < 1 || n_links > kMaxLinks) fail(LAQ_ERR_UNSUPPORTED, "fused star predict supports 1..8 dimensions");
+    auto* p = new laq_probe();
+    try {
+      p->n_links = n_links;
+      for (int j = 0; j < n_links; ++j)
+        build_probe(ctx, nullptr, d_pks[j], h_pk_rows[j], p->probes[j],
+                    "multiway_star_join: duplicate keys in dim " + std::to_string(j));
+      p->err = DevMem<int>(1);
+    } catch (...) {
+      delete p;
+      throw;
+    }
+    *out = p;
+  });
+}
+
+int laq_probe_destroy(laq_probe* p) {
+  delete p;
+  return LAQ_OK;
+}
+
+int laq_probe_fused_predict(laq_ctx* ctx, const laq_probe* probe, const int32_t* const* d_fks, int64_t n_fact,
+                            const double* const* d_partials, int64_t l, double* d_out, int64_t* d_survivors,
+                            int64_t* d_nnz) {
+  return guard(ctx, [&] {
+    if (l < 1 || l > 8) fail(LAQ_ERR_UNSUPPORTED, "fused single-pass predict handles l <= 8 (use star join + apply)");
+    auto* p = const_cast<laq_probe*>(probe);
+    StarArgs<int32_t> a{};
+    a.n_links = p->n_links;
+    a.n = n_fact;
+    for (int j = 0; j < p->n_links; ++j) {
+      a.fk[j] = d_fks[j];
+      a.probe[j] = p->probes[j].view();
+      a.partial[j] = d_partials[j];
+    }
+    a.l = l;
+    a.y = d_out;
+    a.survivors = d_survivors;
+    a.nnz = d_nnz;
+    a.err = p->err.get();
+    run_star(ctx, a, p->scratch, true);
+  });
+}
+
+int laq_fused_star_predict(laq_ctx* ctx, int32_t n_links, const int32_t* const* d_fks, int64_t n_fact,
+                           const int32_t* const* d_pks, const int64_t* h_pk_rows, const double* const* d_partials,
+                           int64_t l, double* d_out, int64_t* d_survivors, int64_t* h_nnz) {
+  laq_probe* p = nullptr;
+  int rc = laq_probe_build(ctx, n_links, d_pks, h_pk_rows, &p);
+  if (rc) return rc;
+  rc = guard(ctx, [&] {
+    if (l <= 8) {
+      int rc2 = laq_probe_fused_predict(ctx, p, d_fks, n_fact, d_partials, l, d_out, d_survivors, ctx->d_flags + 20);
+      if (rc2) fail(rc2, ctx->err);
+    } else {
+      // Wide outputs: compaction pass writing int32 row maps, then the warp-wide gather-sum.
+      StarArgs<int32_t> a{};
+      a.n_links = n_links;
+      a.n = n_fact;
+      std::vector<DevBuf<int32_t>> maps;
+      for (int j = 0; j < n_links; ++j) {
+        maps.emplace_back(ctx, static_cast<size_t>(std::max<int64_t>(n_fact, 1)));
+        a.fk[j] = d_fks[j];
+        a.probe[j] = p->probes[j].view();
+        a.rows32[j] = maps.back().get();
+      }
+      a.survivors = d_survivors;
+      a.nnz = ctx->d_flags + 20;
+      a.err = p->err.get();
+      run_star(ctx, a, p->scratch, false);
+      LAQ_CUDA(cudaMemcpyAsync(ctx->h_pinned, ctx->d_flags + 20, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+      sync(ctx);
+      ApplyArgs<int32_t> ap{};
+      ap.n_parts = n_links;
+      ap.rows = ctx->h_pinned[0];
+      ap.l = l;
+      for (int j = 0; j < n_links; ++j) {
+        ap.idx[j] = maps[j].get();
+        ap.partial[j] = d_partials[j];
+      }
+      ap.out = d_out;
+      launch_apply(ctx, ap);
+    }
+    LAQ_CUDA(cudaMemcpyAsync(ctx->h_pinned, ctx->d_flags + 20, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    *h_nnz = ctx->h_pinned[0];
+  });
+  laq_probe_destroy(p);
+  return rc;
+}
+
+int laq_apply_fused_linear(laq_ctx* ctx, int32_t n_parts, const int64_t* const* d_idx, int64_t rows,
+                           const double* const* d_partials, const int64_t* h_partial_rows, int64_t l,
+                           double* d_out) {
+  return guard(ctx, [&] {
+    (void)h_partial_rows;
+    if (n_parts < 1) fail(LAQ_ERR_SHAPE, "apply_fused_linear: map/partial list lengths");
+    if (n_parts > kMaxLinks) fail(LAQ_ERR_UNSUPPORTED, "apply_fused_linear supports up to 8 partials");
+    ApplyArgs<int64_t> a{};
+    a.n_parts = n_parts;
+    a.rows = rows;
+    a.l = l;
+    for (int j = 0; j < n_parts; ++j) {
+      a.idx[j] = d_idx[j];
+      a.partial[j] = d_partials[j];
+    }
+    a.out = d_out;
+    launch_apply(ctx, a);
+  });
+}
+
+int laq_materialize(laq_ctx* ctx, int32_t n_parts, const int64_t* const* d_idx, int64_t rows,
+                    const double* const* d_dims, const int64_t* h_dim_rows, const int64_t* h_dim_cols,
+                    const int64_t* const* h_placements, int64_t k, double* d_out) {
+  return guard(ctx, [&] {
+    (void)h_dim_rows;
+    if (n_parts < 1) fail(LAQ_ERR_SHAPE, "materialize: input list lengths");
+    std::vector<char> claimed(static_cast<size_t>(k), 0);
+    for (int j = 0; j < n_parts; ++j)
+      for (int64_t c = 0; c < h_dim_cols[j]; ++c) {
+        const int64_t t = h_placements[j][c];
+        if (t < 0 || t >= k) fail(LAQ_ERR_MAPPING, "column map: target index " + std::to_string(t) + " out of range");
+        if (claimed[t]) fail(LAQ_ERR_MAPPING, "materialize: overlapping target column " + std::to_string(t));
+        claimed[t] = 1;
+      }
+    if (rows == 0 || k == 0) return;
+    LAQ_CUDA(cudaMemsetAsync(d_out, 0, rows * k * sizeof(double), ctx->stream));
+    for (int j = 0; j < n_parts; ++j) {
+      if (h_dim_cols[j] == 0) continue;
+      std::vector<int32_t> pl(h_placements[j], h_placements[j] + h_dim_cols[j]);
+      DevBuf<int32_t> dpl(ctx, pl.size());
+      LAQ_CUDA(cudaMemcpyAsync(dpl.get(), pl.data(), pl.size() * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+      materialize_kernel<<<grid_for(rows * h_dim_cols[j], 256, ctx->sm_count * 16), 256, 0, ctx->stream>>>(
+          d_idx[j], rows, d_dims[j], h_dim_cols[j], dpl.get(), k, d_out);
+      launched(ctx);
+      sync(ctx);  // pl (host) must outlive the async copy
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,190 @@
+"""A StarSchema resident in HBM and the query plan driver on it.
+
+  DeviceStar.run_query(q)          run_query_laq          cli.cpp:73-138
+  DeviceStar.measure_selectivity   measure_selectivity    benchgen.cpp:366-411
+  DeviceStar.gen_queries(group)    gen_queries            benchgen.cpp:413-457 (device-tuned dials)
+  DeviceStar.prepare(q) -> Plan    prepared form: execute() enqueues the fused
+                                   scan into an int64 accumulator (no host sync,
+                                   CUDA-graph capturable, all-reduce friendly);
+                                   emit() turns the accumulator into result rows.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _abi, errors, query
+from .device import context
+
+
+class Plan:
+    def __init__(self, star: "DeviceStar", q: query.QuerySpec):
+        self.star = star
+        self.q = q
+        self.ctx = star.ctx
+        self._holder = query.QueryDescHolder(q)
+        h = C.c_void_p()
+        g = C.c_int64()
+        self.ctx.check(self.ctx.lib.laq_query_prepare(self.ctx.h, star.h, C.byref(self._holder.desc), C.byref(h),
+                                                      C.byref(g)))
+        self.h = h
+        self.n_groups = g.value
+        self.acc = torch.zeros(2 * self.n_groups, dtype=torch.int64, device="cuda")
+
+    def execute(self, acc: torch.Tensor | None = None, accumulate: bool = False) -> torch.Tensor:
+        acc = self.acc if acc is None else acc
+        self.ctx.bind_stream()
+        self.ctx.check(self.ctx.lib.laq_plan_execute(self.ctx.h, self.h, acc.data_ptr(), 1 if accumulate else 0))
+        return acc
+
+    def build_codes(self):
+        self.ctx.check(self.ctx.lib.laq_plan_build_codes(self.ctx.h, self.h))
+
+    def scan(self, acc: torch.Tensor | None = None, accumulate: bool = False) -> torch.Tensor:
+        acc = self.acc if acc is None else acc
+        self.ctx.check(self.ctx.lib.laq_plan_scan(self.ctx.h, self.h, acc.data_ptr(), 1 if accumulate else 0))
+        return acc
+
+    @property
+    def bytes_per_row(self) -> int:
+        return int(self.ctx.lib.laq_plan_bytes_per_row(self.h))
+
+    def emit(self, acc_host: np.ndarray) -> np.ndarray:
+        acc_host = np.ascontiguousarray(acc_host, np.int64)
+        cap = max(1, 2 * self.n_groups) * (len(self.q.group_by) + 1)
+        out = np.zeros(cap, np.float64)
+        rows, cols = C.c_int64(), C.c_int64()
+        rc = self.ctx.lib.laq_plan_emit(self.h, acc_host.ctypes.data_as(_abi.i64p),
+                                        out.ctypes.data_as(_abi.f64p), cap, C.byref(rows), C.byref(cols))
+        errors.raise_for(rc, "laq_plan_emit failed")
+        return out[: rows.value * cols.value].reshape(rows.value, cols.value).copy()
+
+    def run(self) -> np.ndarray:
+        acc = self.execute()
+        return self.emit(acc.cpu().numpy())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.laq_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DeviceStar:
+    """laq_star: tables uploaded once (int32 device layout), probes cached per link."""
+
+    def __init__(self, ctx=None):
+        self.ctx = ctx or context()
+        h = C.c_void_p()
+        self.ctx.check(self.ctx.lib.laq_star_create(self.ctx.h, C.byref(h)))
+        self.h = h
+        self._keep = []
+        self.rows = {}
+
+    @classmethod
+    def from_tables(cls, tables: dict, kinds: dict, links, fact="lineorder", row_range=None, ctx=None):
+        """tables: {name: {col: np.ndarray}} (int64/int32 ints, float64 floats);
+        kinds: {name: {col: 0 key | 1 int | 2 float}}; row_range=(b, e) uploads
+        only that slice of the fact table (row sharding)."""
+        s = cls(ctx)
+        order = [fact] + [t for t in tables if t != fact]
+        for name in order:
+            cols = tables[name]
+            if name == fact and row_range is not None:
+                b, e = row_range
+                cols = {c: a[b:e] for c, a in cols.items()}
+            s.add_table(name, cols, kinds[name], is_fact=(name == fact))
+        for l in links:
+            s.add_link(*l)
+        return s
+
+    def add_table(self, name, cols: dict, kinds: dict, is_fact=False):
+        names = list(cols)
+        rows = len(cols[names[0]]) if names else 0
+        width = 8
+        arrays = []
+        for c in names:
+            a = cols[c]
+            if kinds[c] == 2:
+                a = np.ascontiguousarray(a, np.float64)
+            elif a.dtype == np.int32:
+                width = 4
+            arrays.append(a)
+        conv = []
+        for c, a in zip(names, arrays):
+            if kinds[c] != 2:
+                a = np.ascontiguousarray(a, np.int32 if width == 4 else np.int64)
+            conv.append(a)
+        self._keep.append(conv)
+        cn = (C.c_char_p * len(names))(*[c.encode() for c in names])
+        kd = (C.c_int32 * len(names))(*[kinds[c] for c in names])
+        ptrs = (C.c_void_p * len(names))(*[a.ctypes.data for a in conv])
+        self.ctx.check(self.ctx.lib.laq_star_add_table(self.star_h, name.encode(), 1 if is_fact else 0, rows,
+                                                       len(names), cn, kd, width, ptrs))
+        self._keep.pop()  # host columns were copied to the device
+        self.rows[name] = rows
+
+    def add_table_device(self, name, cols: dict, kinds: dict, is_fact=False):
+        """int32 CUDA tensors, used in place (caller keeps them alive)."""
+        names = list(cols)
+        rows = cols[names[0]].numel()
+        self._keep.append(cols)
+        cn = (C.c_char_p * len(names))(*[c.encode() for c in names])
+        kd = (C.c_int32 * len(names))(*[kinds[c] for c in names])
+        ptrs = _abi.ptr_array([cols[c].data_ptr() for c in names])
+        self.ctx.check(self.ctx.lib.laq_star_add_table_device(self.star_h, name.encode(), 1 if is_fact else 0, rows,
+                                                              len(names), cn, kd, ptrs))
+        self.rows[name] = rows
+
+    @property
+    def star_h(self):
+        return self.h
+
+    def add_link(self, fact_fk, dim_name, dim_pk):
+        self.ctx.check(self.ctx.lib.laq_star_add_link(self.h, fact_fk.encode(), dim_name.encode(), dim_pk.encode()))
+
+    def prepare(self, q: query.QuerySpec) -> Plan:
+        return Plan(self, q)
+
+    def run_query(self, q: query.QuerySpec) -> np.ndarray:
+        holder = query.QueryDescHolder(q)
+        cap = 1 << 20
+        out = np.zeros(cap, np.float64)
+        rows, cols = C.c_int64(), C.c_int64()
+        rc = self.ctx.lib.laq_run_query(self.ctx.h, self.h, C.byref(holder.desc), out.ctypes.data_as(_abi.f64p),
+                                        cap, C.byref(rows), C.byref(cols))
+        self.ctx.check(rc)
+        return out[: rows.value * cols.value].reshape(rows.value, cols.value).copy()
+
+    def measure_selectivity(self, q: query.QuerySpec) -> float:
+        holder = query.QueryDescHolder(q)
+        out = C.c_double()
+        self.ctx.check(self.ctx.lib.laq_measure_selectivity(self.ctx.h, self.h, C.byref(holder.desc), C.byref(out)))
+        return out.value
+
+    def gen_queries(self, group: int, targets=()):
+        return query.gen_queries(self.measure_selectivity, group, targets)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.laq_star_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def upload_gen_star(g, ctx=None, row_range=None) -> DeviceStar:
+    """Upload a gen.GenStar (or oracle RefStar-like object with .tables/.kinds/.links())."""
+    links = g.links() if callable(getattr(g, "links", None)) else g.links
+    return DeviceStar.from_tables(g.tables, g.kinds, links, row_range=row_range, ctx=ctx)

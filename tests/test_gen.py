@@ -1,0 +1,63 @@
+"""CPU: the native host generator reproduces the reference generator bit for bit."""
+import random
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle.laq_oracle import fnv1a
+
+
+def _gen():
+    from paper_2306_08367_b200 import gen
+    try:
+        gen.lib()
+    except Exception:
+        pytest.skip("liblaq_gen.so not built")
+    return gen
+
+
+def _h(a):
+    return "%016x" % fnv1a(np.ascontiguousarray(a).tobytes())
+
+
+def test_generator_matches_reference_columns():
+    gen = _gen()
+    G = load_golden("ssb_s2_sf2.json")
+    for narrow in (False, True):
+        g = gen.gen_star(G["setting"], G["sf"], G["seed"], narrow=narrow)
+        assert set(g.tables) == set(G["tables"])
+        for t, cols in G["tables"].items():
+            for c, meta in cols.items():
+                a = g.tables[t][c]
+                assert len(a) == meta["rows"]
+                a64 = a.astype(np.int64) if a.dtype != np.float64 else a
+                assert _h(a64) == meta["fnv"], (t, c)
+
+
+def test_cfg1_inputs_match_reference_draws():
+    gen = _gen()
+    G = load_golden("cfg1_small.json")
+    fk, pk, feats, W = gen.cfg1_inputs(G["n_fact"], G["dim_rows"], G["k"], G["l"])
+    assert _h(fk) == G["fk_fnv"]
+    assert _h(feats) == G["feats_fnv"]
+    assert [float(v).hex() for v in W.ravel()] == G["W"]
+
+
+def test_fast_modulo_is_exact():
+    gen = _gen()
+    L = gen.lib()
+    rnd = random.Random(3)
+    for _ in range(20000):
+        x = rnd.getrandbits(64)
+        n = rnd.choice([rnd.getrandbits(rnd.randint(1, 64)) or 1, rnd.randint(1, 5000), 1 << rnd.randint(0, 63)])
+        assert L.laqgen_fastmod(x, n) == x % n
+
+
+def test_capacity_guard():
+    gen = _gen()
+    from paper_2306_08367_b200 import errors
+    with pytest.raises(errors.CapacityError):
+        gen.gen_star("Ssb", 100, 42, max_bytes=1 << 20)
+    with pytest.raises(errors.GenError):
+        gen.gen_star("S2", 0, 42)

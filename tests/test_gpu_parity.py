@@ -1,0 +1,228 @@
+"""GPU parity: every C-ABI operator vs the reference's golden vectors and the
+pinned oracle.  Bar: bit-exact for keys / indices / integer aggregates, and
+bit-exact for the fp64 fused-prediction paths too (same association order);
+groupby_sum_single uses device atomics, so its float sums are checked at the
+north_star tolerance (1e-5 relative) unless the inputs are exactly
+representable (then exact)."""
+import numpy as np
+import pytest
+
+from conftest import fa, ia, load_golden
+from oracle import laq_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+OPS = load_golden("ops.json")
+FUS = load_golden("fusion.json")
+
+
+@pytest.fixture(scope="module")
+def lib(gpu_ctx):
+    from paper_2306_08367_b200 import errors, fusion, ops
+    return ops, fusion, errors
+
+
+def test_key_domain(lib):
+    ops, _, errors = lib
+    d = ops.build_key_domain(np.array([1, 0, 4, 2, 3]), np.array([2, 3, 0, 4, 7]))
+    assert d.sorted_keys.tolist() == [0, 1, 2, 3, 4, 7]
+    assert d.position(7) == 5
+    with pytest.raises(errors.DomainError):
+        d.position(6)
+    with pytest.raises(errors.DomainError):
+        ops.build_key_domain(np.array([-1]), np.array([2, 4]))
+    for c in OPS["domains"]:
+        d = ops.build_key_domain(ia(c["r"]), ia(c["s"]))
+        assert d.sorted_keys.tolist() == c["out"]
+        assert ops.update_key_domain(d, ia(c["new"])).sorted_keys.tolist() == c["updated"]
+
+
+def test_key_domain_large_and_wide(lib):
+    ops, _, _ = lib
+    rng = np.random.default_rng(1)
+    for hi in (1000, 1 << 26, 1 << 45):  # bitmap path, big bitmap, radix-sort path
+        a = rng.integers(0, hi, 500_000)
+        b = rng.integers(0, hi, 30_000)
+        assert np.array_equal(ops.build_key_domain(a, b).sorted_keys, O.build_key_domain(a, b))
+
+
+def test_key_matrix(lib):
+    ops, _, errors = lib
+    g = OPS["key_matrix_example"]
+    d = ops.KeyDomain(ia(g["domain"]))
+    m = ops.key_matrix(ia(g["keys"]), d, "RowsByDomain")
+    assert m.row_ptr.tolist() == g["rbd"]["row_ptr"] and m.col_idx.tolist() == g["rbd"]["col_idx"]
+    m = ops.key_matrix(ia(g["keys"]), d, "DomainByRows")
+    assert m.row_ptr.tolist() == g["dbr"]["row_ptr"] and m.col_idx.tolist() == g["dbr"]["col_idx"]
+    v = OPS["key_matrix_valued"]
+    m = ops.key_matrix(ia(v["keys"]), ops.KeyDomain(ia(v["domain"])), "RowsByDomain", fa(v["values_in"]))
+    assert m.col_idx.tolist() == v["col_idx"] and np.array_equal(m.values, fa(v["values"]))
+    with pytest.raises(errors.DomainError):
+        ops.key_matrix(ia([9]), d, "RowsByDomain")
+    rng = np.random.default_rng(2)
+    keys = rng.integers(0, 5000, 200_000)
+    vals = rng.integers(-2, 3, 200_000).astype(np.float64)
+    dom = O.build_key_domain(keys, [])
+    rp, ci, vv = O.key_matrix(keys, dom, "DomainByRows", vals)
+    m = ops.key_matrix(keys, ops.KeyDomain(dom), "DomainByRows", vals)
+    assert np.array_equal(m.row_ptr, rp) and np.array_equal(m.col_idx, ci) and np.array_equal(m.values, vv)
+
+
+def test_mm_join(lib):
+    ops, _, errors = lib
+    for c in OPS["mm_join"]:
+        m = ops.mm_join(ia(c["r"]), ia(c["s"]))
+        assert m.row_idx.tolist() == c["out_r"] and m.col_idx.tolist() == c["out_s"]
+    rng = np.random.default_rng(3)
+    r = rng.integers(0, 3000, 100_000)
+    s = rng.integers(0, 3000, 20_000)
+    m = ops.mm_join(r, s)
+    a, b = O.mm_join(r, s)
+    assert np.array_equal(m.row_idx, a) and np.array_equal(m.col_idx, b)
+    # cached superset domain gives identical output (test_laqops.cpp:256-262)
+    dom = ops.update_key_domain(ops.build_key_domain(r, s), rng.integers(0, 6000, 500))
+    m2 = ops.mm_join(r, s, dom)
+    assert np.array_equal(m2.row_idx, a) and np.array_equal(m2.col_idx, b)
+    assert ops.mm_join(ia([1, 2]), ia([3, 4])).nnz() == 0
+    with pytest.raises(errors.DomainError):
+        ops.mm_join(ia([-3]), ia([1]))
+
+
+def test_star_join(lib):
+    ops, _, errors = lib
+    for c in OPS["star_join"]:
+        surv, rows = ops.multiway_star_join([ia(f) for f in c["fks"]], [ia(p) for p in c["pks"]])
+        assert surv.tolist() == c["survivors"]
+        assert [r.tolist() for r in rows] == c["dim_rows"]
+    with pytest.raises(errors.DuplicateKeyError):
+        ops.multiway_star_join([ia([0, 1])], [ia([0, 0])])
+    # trivial cases (test_laqops.cpp:303-322)
+    surv, rows = ops.multiway_star_join([ia([2, 0, 1, 2])], [ia([0, 1, 2])])
+    assert surv.tolist() == [0, 1, 2, 3]
+    surv, rows = ops.multiway_star_join([ia([2, 0, 1, 2])] * 2, [ia([0, 1, 2]), ia([])])
+    assert len(surv) == 0 and all(len(r) == 0 for r in rows)
+
+
+def test_star_join_large_direct_and_hash(lib):
+    ops, _, _ = lib
+    rng = np.random.default_rng(4)
+    n = 3_000_000
+    pks = [np.arange(800_000), rng.permutation(1 << 40)[:0] if False else rng.choice(1 << 40, 20_000, replace=False),
+           np.arange(2555) * 7 + 11]
+    fks = [rng.integers(0, 900_000, n), np.where(rng.random(n) < 0.8, pks[1][rng.integers(0, 20_000, n)], 5),
+           rng.integers(0, 2555 * 7 + 20, n)]
+    surv, rows = ops.multiway_star_join(fks, pks)
+    ws, wr = O.multiway_star_join(fks, pks)
+    assert np.array_equal(surv, ws)
+    for a, b in zip(rows, wr):
+        assert np.array_equal(a, b)
+
+
+def test_groupby(lib):
+    ops, _, errors = lib
+    e = OPS["groupby_single_example"]
+    g, s = ops.groupby_sum_single(ia(e["kr"]), fa(e["vr"]), ia(e["ks"]), ia(e["gs"]))
+    assert g.tolist() == [0, 1, 2] and s.tolist() == [1000.0, 10010.0, 100.0]
+    for c in OPS["groupby_single"]:  # quarter-integer values: exact in any order
+        g, s = ops.groupby_sum_single(ia(c["kr"]), fa(c["vr"]), ia(c["ks"]), ia(c["gs"]))
+        assert g.tolist() == c["groups"] and np.array_equal(s, fa(c["sums"]))
+    for c in OPS["groupby_multi"]:  # row-order segmented sums: bit-exact
+        k, s = ops.groupby_sum_multi([ia(x) for x in c["cols"]], fa(c["vals"]))
+        assert [x.tolist() for x in k] == c["keys"] and np.array_equal(s, fa(c["sums"]))
+    rng = np.random.default_rng(6)
+    kr = rng.integers(0, 500, 100_000)
+    vr = rng.normal(size=100_000)
+    ks = rng.integers(0, 500, 700)
+    gs = rng.integers(0, 30, 700)
+    g, s = ops.groupby_sum_single(kr, vr, ks, gs)
+    wg, ws = O.groupby_sum_single(kr, vr, ks, gs)
+    assert np.array_equal(g, wg)
+    np.testing.assert_allclose(s, ws, rtol=1e-5, atol=1e-9)  # north_star float tolerance
+
+
+def _star(c):
+    dims = [fa(d["data"], (d["rows"], d["cols"])) for d in c["dims"]]
+    L = fa(c["L"]["data"], (c["L"]["k"], c["L"]["l"]))
+    return dims, c["placements"], L, [ia(i) for i in c["idx"]]
+
+
+def test_fusion_bit_exact(lib):
+    ops, fusion, errors = lib
+    for c in FUS["stars"]:
+        dims, pls, L, idx = _star(c)
+        f = fusion.prefuse_linear(dims, pls, L)
+        for p, want in zip(f.partials, c["partials"]):
+            assert np.array_equal(p.ravel(), fa(want))
+        if len(idx[0]) == 0:
+            continue
+        assert np.array_equal(fusion.apply_fused_linear(idx, f).ravel(), fa(c["Y"]))
+        T = ops.materialize(idx, dims, pls, L.shape[0])
+        assert np.array_equal(T.ravel(), fa(c["T"]))
+        assert np.array_equal(fusion.predict_linear(T, L).ravel(), fa(c["Y_nonfused"]))
+    for c in FUS["matmul"]:
+        a = fa(c["a"], (c["m"], c["k"]))
+        b = fa(c["b"], (c["k"], c["n"]))
+        assert np.array_equal(fusion.dense_matmul(a, b).ravel(), fa(c["c"]))
+    d1 = [np.random.default_rng(0).random((4, 2))]
+    with pytest.raises(errors.MappingError):
+        fusion.prefuse_linear(d1 * 2, [[0, 1], [1, 2]], np.ones((3, 1)))
+    with pytest.raises(errors.ShapeError):
+        fusion.prefuse_linear(d1, [[0, 1]], np.ones((3, 1)))
+
+
+def test_fused_star_predict_cfg1_small(lib):
+    _, fusion, _ = lib
+    from paper_2306_08367_b200 import gen
+    G = load_golden("cfg1_small.json")
+    fk, pk, feats, W = gen.cfg1_inputs(G["n_fact"], G["dim_rows"], G["k"], G["l"])
+    f = fusion.prefuse_linear([feats], [np.arange(16)], W)
+    y, surv = fusion.fused_star_predict([fk], [pk], f.partials)
+    assert str(O.checksum_rows(y)) == G["checksum"]
+    assert [float(v).hex() for v in y[:16].ravel()] == G["Y_head"]
+    assert np.array_equal(surv, np.arange(G["n_fact"]))
+
+
+@pytest.mark.parametrize("l", [1, 3, 8, 40])
+def test_fused_star_predict_multi_dim(lib, l):
+    _, fusion, _ = lib
+    rng = np.random.default_rng(10 + l)
+    n = 1_234_567
+    rows = [2000, 517, 2555]
+    pks = [np.arange(r) + 3 for r in rows]
+    fks = [rng.integers(0, r + 10, n) for r in rows]
+    ks = [6, 5, 5]
+    dims = [rng.random((r, k)) for r, k in zip(rows, ks)]
+    pls = [np.arange(0, 6), np.arange(6, 11), np.arange(11, 16)]
+    L = rng.random((16, l)) * 2 - 1
+    f = fusion.prefuse_linear(dims, pls, L)
+    y, surv = fusion.fused_star_predict(fks, pks, f.partials)
+    ws, wr = O.multiway_star_join(fks, pks)
+    wy = O.apply_fused_linear(wr, O.prefuse_linear(dims, pls, L))
+    assert np.array_equal(surv, ws)
+    assert np.array_equal(y, wy)  # bit-exact: same association as fusion.cpp:73-76
+
+
+def test_predictor_graph_capturable(lib):
+    import torch
+    _, fusion, _ = lib
+    rng = np.random.default_rng(3)
+    pk = np.arange(10_000)
+    fk = rng.integers(0, 10_000, 1_000_000)
+    P = rng.random((10_000, 1))
+    pred = fusion.FusedStarPredictor([pk], [P])
+    fk_d = torch.from_numpy(fk.astype(np.int32)).cuda()
+    out = torch.empty((1_000_000, 1), dtype=torch.float64, device="cuda")
+    pred([fk_d], out=out, sync=False)  # warm-up (allocates look-back scratch)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        pred.ctx.bind_stream(s)
+        with torch.cuda.graph(g, stream=s):
+            pred([fk_d], out=out, sync=False)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    pred.ctx.bind_stream()
+    assert np.array_equal(out.cpu().numpy()[:, 0], P[fk, 0] + 0.0)
+    assert int(pred.nnz_dev.item()) == 1_000_000
