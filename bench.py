@@ -20,7 +20,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -60,55 +59,61 @@ def dist_init():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md recipe)."""
-
-    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle-reason sampling (NVML, the library nvidia-smi reads)
+    every 10 ms from before warm-up to the end of the timed region; the report
+    uses the samples taken inside the timed region (B200_PROFILING.md recipe)."""
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
-        self.proc = None
-        self.lines = []
+        self.samples = []  # (t, sm_mhz, reasons bitmask)
+        self.marks = []
+        self._stop = threading.Event()
+        self.ok = False
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
-                                          "-i", str(self.gpu), "-lms", "100"], stdout=subprocess.PIPE,
-                                         stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            import pynvml as N
+            N.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.gpu]) if vis and vis.split(",")[self.gpu].isdigit() else self.gpu
+            self.N, self.h = N, N.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self.ok = True
         except Exception:
-            self.proc = None
+            return
+        self.t = threading.Thread(target=self._loop, daemon=True)
+        self.t.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _loop(self):
+        N = self.N
+        while not self._stop.is_set():
+            try:
+                self.samples.append((time.perf_counter(), N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM),
+                                     N.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def mark(self):
+        self.marks.append(time.perf_counter())
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            p = [x.strip() for x in ln.split(",")]
-            if len(p) < 9:
-                continue
-            try:
-                sm.append(float(p[1]))
-                smax = float(p[2])
-            except ValueError:
-                continue
-            for n, v in zip(names, p[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        self._stop.set()
+        self.t.join(timeout=2)
+        N = self.N
+        t0, t1 = (self.marks[0], self.marks[-1]) if len(self.marks) >= 2 else (0, 1e30)
+        inside = [s for s in self.samples if t0 <= s[0] <= t1]
+        use = inside if inside else self.samples
+        names = {N.nvmlClocksEventReasonHwSlowdown: "hw_slowdown",
+                 N.nvmlClocksEventReasonHwThermalSlowdown: "hw_thermal_slowdown",
+                 N.nvmlClocksEventReasonSwThermalSlowdown: "sw_thermal_slowdown",
+                 N.nvmlClocksEventReasonSwPowerCap: "sw_power_cap"}
+        reasons = sorted({v for _, _, m in use for k, v in names.items() if m & k})
+        return {"sm_mhz": float(np.median([s[1] for s in use])) if use else None, "sm_max_mhz": float(self.max_mhz),
+                "reasons": reasons, "samples": len(use),
+                "window": "timed region" if inside else "warm-up + timed region (timed region < 10 ms)"}
 
 
 # ---------------------------------------------------------------------------
@@ -249,14 +254,15 @@ def main():
         a = acc_host.numpy()
         return [p.emit(a[offs[qi]: offs[qi + 1]]) for qi, p in enumerate(plans)]
 
+    clocks = Clocks(local)
+    clocks.start()
     for _ in range(args.warmup):
         results = step()
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = ctx.launches
-    clocks = Clocks(local)
-    clocks.start()
+    clocks.mark()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
@@ -264,6 +270,7 @@ def main():
         results = step(i)
     t_end.record(stream)
     torch.cuda.synchronize()
+    clocks.mark()
     clk = clocks.stop()
     launches = ctx.launches - launches0
     ms_total = t_start.elapsed_time(t_end)

@@ -49,7 +49,7 @@ def build_cuda(force=False, verbose=False):
     out = os.path.join(NATIVE, "liblaq_b200.so")
     if not (force or _stale(out, srcs + hdrs)):
         return out
-    objs = []
+    objs, jobs = [], []
     for s in srcs:
         o = os.path.join(NATIVE, os.path.basename(s)[:-3] + ".o")
         if force or _stale(o, [s] + hdrs):
@@ -58,8 +58,12 @@ def build_cuda(force=False, verbose=False):
                    "-c", s, "-o", o]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
-            _run(cmd)
+            jobs.append(cmd)
         objs.append(o)
+    if jobs:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=max(1, os.cpu_count() or 1)) as ex:
+            list(ex.map(_run, jobs))
     _run([NVCC, *ARCH, "-shared", *objs, "-o", out, "-lcudart"])
     return out
 

@@ -1,5 +1,5 @@
-// K4 ssb_scan_groupby: the query plan driver run_query_laq (cli.cpp:73-138)
-// as ONE fused pass over the fact table per query.
+// K4 ssb_scan_groupby host side: the query plan driver run_query_laq
+// (cli.cpp:73-138) as ONE fused pass over the fact table per query.
 //
 // Reference plan:  filter_table(fact), filter_table(dim_j)  ->  multiway_star_join
 // (one-hot key matrices x spmm per link)  ->  gather measure (spmm_dense)  ->
@@ -14,39 +14,45 @@
 //    columns' value ranges, first group column most significant, so ascending
 //    group id == ascending group tuple == the order groupby_sum_multi +
 //    sort_rows produce);
-//  * the scan kernel streams the touched int32 fact columns once (16-20 B/row),
-//    evaluates fact filters, probes each link (1 gather into an L2-resident
-//    code table, skipped for rows already dead), and accumulates per group id
-//    an exact int64 (count, sum) in shared memory; blocks merge with global
-//    atomics into the caller's accumulator (the NCCL all-reduce buffer when
-//    sharded across GPUs).
+//  * the scan (ssb_scan.cuh) streams the touched int32 fact columns once
+//    (16-20 B/row), evaluates fact filters, probes each link, and accumulates
+//    per group id an exact int64 (count, sum) into the caller's accumulator
+//    (the NCCL all-reduce buffer when the fact table is sharded across GPUs).
 // Integer sums are exact, so results equal the reference bit for bit.
 #include <algorithm>
 #include <climits>
 #include <cstring>
 #include <map>
 #include <memory>
+#include <numeric>
 #include <string>
 #include <vector>
 
-#include "probe.cuh"
+#include "ssb_launch.cuh"
 
 namespace laq {
 namespace {
 
-constexpr int kMaxLinks = 8;
-constexpr int kMaxFactFilters = 4;
-constexpr int kMaxFactGroups = 4;
+using scan::FactFilter;
+using scan::FactGroup;
+using scan::LinkProbe;
+using scan::ScanArgs;
+using scan::kMaxFactFilters;
+using scan::kMaxFactGroups;
+using scan::kMaxLinks;
+
 constexpr int kMaxDimFilters = 8;
 constexpr int kMaxDimGroups = 4;
-constexpr int kScanBlock = 256;
-constexpr int64_t kSmemBins = 6144;  // group ids accumulated in shared memory
+constexpr int64_t kSmemBinsPipe = 4096;  // group ids binned in shared memory (pipe kernel)
+constexpr int64_t kSmemBinsLdg = 6144;
+constexpr int64_t kSmemTabMaxSlots = 49152;
 
 struct DevCol {
   std::string name;
   int kind = LAQ_COL_INT;
   int32_t* d = nullptr;  // int32 device column (nullptr for float columns)
   int64_t mn = 0, mx = -1;
+  bool padded = false;   // allocation has >= 16 readable bytes past the end
 };
 
 struct DevTable {
@@ -114,32 +120,11 @@ struct CodeArgs {
   DimGroup g[kMaxDimGroups];
 };
 
-__device__ __forceinline__ bool pred_eval(int kind, int64_t v, int64_t lo, int64_t hi, const int64_t* set, int n) {
-  switch (kind) {  // predicate.hpp:84-93
-    case LAQ_PRED_LT: return v < lo;
-    case LAQ_PRED_LE: return v <= lo;
-    case LAQ_PRED_EQ: return v == lo;
-    case LAQ_PRED_GE: return v >= lo;
-    case LAQ_PRED_GT: return v > lo;
-    case LAQ_PRED_BETWEEN: return v >= lo && v <= hi;
-    default: {  // InSet: binary search over the sorted set
-      int a = 0, b = n;
-      while (a < b) {
-        const int m = (a + b) >> 1;
-        const int64_t s = set[m];
-        if (s == v) return true;
-        if (s < v) a = m + 1; else b = m;
-      }
-      return false;
-    }
-  }
-}
-
 __global__ void code_kernel(const CodeArgs a) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < a.rows; r += (int64_t)gridDim.x * blockDim.x) {
     bool pass = true;
     for (int i = 0; i < a.n_filters && pass; ++i)
-      pass = pred_eval(a.f[i].kind, a.f[i].col[r], a.f[i].lo, a.f[i].hi, a.f[i].set, a.f[i].set_len);
+      pass = scan::pred_eval(a.f[i].kind, a.f[i].col[r], a.f[i].lo, a.f[i].hi, a.f[i].set, a.f[i].set_len);
     int64_t code = -1;
     if (pass) {
       code = 0;
@@ -149,204 +134,27 @@ __global__ void code_kernel(const CodeArgs a) {
   }
 }
 
-// ---- the fused scan --------------------------------------------------------------
-
-struct LinkProbe {
-  int kind;
-  int64_t base, size;
-  const int64_t* keys;
-  const int32_t* code;  // per slot
-};
-
-struct FactFilter {
-  const int32_t* col;
-  int kind;
-  int64_t lo, hi;
-  const int64_t* set;
-  int set_len;
-};
-
-struct FactGroup {
-  const int32_t* col;
-  int64_t mn, stride;
-};
-
-struct ScanArgs {
-  int64_t n;
-  const int32_t* fk[kMaxLinks];
-  LinkProbe link[kMaxLinks];
-  FactFilter ff[kMaxFactFilters];
-  int n_fgroups;
-  FactGroup fg[kMaxFactGroups];
-  const int32_t* measure;  // nullptr: count only
-  int64_t n_groups;
-  unsigned long long* acc;  // [2*G]: count, sum
-};
-
-__device__ __forceinline__ int32_t link_code(const LinkProbe& p, int32_t key) {
-  if (p.kind == PROBE_DIRECT) {
-    const uint64_t s = static_cast<uint64_t>(static_cast<int64_t>(key) - p.base);
-    return s < static_cast<uint64_t>(p.size) ? __ldg(p.code + s) : -1;
-  }
-  const uint64_t mask = static_cast<uint64_t>(p.size) - 1;
-  uint64_t h = static_cast<uint64_t>(static_cast<int64_t>(key)) * 0x9E3779B97F4A7C15ull;
-  h ^= h >> 29;
-  for (uint64_t s = h & mask;; s = (s + 1) & mask) {
-    const int64_t k = __ldg(p.keys + s);
-    if (k == key) return __ldg(p.code + s);
-    if (k < 0) return -1;
-  }
+__global__ void count_pass_kernel(const int32_t* __restrict__ code, int64_t slots, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < slots; s += (int64_t)gridDim.x * blockDim.x)
+    c += code[s] >= 0 ? 1 : 0;
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
 
-__device__ __forceinline__ int4 ld4(const int32_t* p, int64_t row0, int64_t n, bool vec) {
-  if (vec && row0 + 4 <= n) return __ldcs(reinterpret_cast<const int4*>(p + row0));
-  int4 v;
-  v.x = row0 + 0 < n ? p[row0 + 0] : 0;
-  v.y = row0 + 1 < n ? p[row0 + 1] : 0;
-  v.z = row0 + 2 < n ? p[row0 + 2] : 0;
-  v.w = row0 + 3 < n ? p[row0 + 3] : 0;
-  return v;
-}
+// ---- kernel dispatch (instantiated per link count in ssb_scan_nl*.cu) -----
 
-__device__ __forceinline__ int comp(const int4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
-
-// mode: 0 = single group held in registers, 1 = shared-memory bins, 2 = global atomics
-template <int NL, int NF, int MODE>
-__global__ void __launch_bounds__(kScanBlock) scan_kernel(const ScanArgs a, const bool vec) {
-  extern __shared__ unsigned long long s_bins[];  // MODE 1: [G] counts then [G] sums
-  if constexpr (MODE == 1) {
-    for (int64_t g = threadIdx.x; g < 2 * a.n_groups; g += blockDim.x) s_bins[g] = 0;
-    __syncthreads();
-  }
-  unsigned long long r_cnt = 0, r_sum = 0;
-
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
-  for (int64_t row0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; row0 < a.n; row0 += stride) {
-    // Issue every streamed column load up front (memory-level parallelism).
-    int4 fk[NL > 0 ? NL : 1], fv[NF > 0 ? NF : 1], mv;
-#pragma unroll
-    for (int j = 0; j < NL; ++j) fk[j] = ld4(a.fk[j], row0, a.n, vec);
-#pragma unroll
-    for (int f = 0; f < NF; ++f) fv[f] = ld4(a.ff[f].col, row0, a.n, vec);
-    if (a.measure) mv = ld4(a.measure, row0, a.n, vec);
-
-    int64_t gid[4];
-    bool alive[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      alive[i] = row0 + i < a.n;
-      gid[i] = 0;
-    }
-#pragma unroll
-    for (int f = 0; f < NF; ++f)
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        alive[i] = alive[i] && pred_eval(a.ff[f].kind, comp(fv[f], i), a.ff[f].lo, a.ff[f].hi, a.ff[f].set,
-                                         a.ff[f].set_len);
-#pragma unroll
-    for (int j = 0; j < NL; ++j)
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (alive[i]) {
-          const int32_t c = link_code(a.link[j], comp(fk[j], i));
-          alive[i] = c >= 0;
-          gid[i] += c;
-        }
-    for (int g = 0; g < a.n_fgroups; ++g) {
-      const int4 v = ld4(a.fg[g].col, row0, a.n, vec);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) gid[i] += (static_cast<int64_t>(comp(v, i)) - a.fg[g].mn) * a.fg[g].stride;
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (!alive[i]) continue;
-      const unsigned long long val = a.measure ? static_cast<unsigned long long>(static_cast<long long>(comp(mv, i))) : 0ull;
-      if constexpr (MODE == 0) {
-        r_cnt += 1;
-        r_sum += val;
-      } else if constexpr (MODE == 1) {
-        atomicAdd(s_bins + gid[i], 1ull);
-        if (a.measure) atomicAdd(s_bins + a.n_groups + gid[i], val);
-      } else {
-        atomicAdd(a.acc + 2 * gid[i], 1ull);
-        if (a.measure) atomicAdd(a.acc + 2 * gid[i] + 1, val);
-      }
-    }
-  }
-
-  if constexpr (MODE == 0) {
-    for (int o = 16; o; o >>= 1) {
-      r_cnt += __shfl_xor_sync(0xffffffffu, r_cnt, o);
-      r_sum += __shfl_xor_sync(0xffffffffu, r_sum, o);
-    }
-    __shared__ unsigned long long w_cnt[kScanBlock / 32], w_sum[kScanBlock / 32];
-    if ((threadIdx.x & 31) == 0) {
-      w_cnt[threadIdx.x >> 5] = r_cnt;
-      w_sum[threadIdx.x >> 5] = r_sum;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned long long c = 0, s = 0;
-      for (int w = 0; w < kScanBlock / 32; ++w) {
-        c += w_cnt[w];
-        s += w_sum[w];
-      }
-      if (c) {
-        atomicAdd(a.acc, c);
-        atomicAdd(a.acc + 1, s);
-      }
-    }
-  } else if constexpr (MODE == 1) {
-    __syncthreads();
-    for (int64_t g = threadIdx.x; g < a.n_groups; g += blockDim.x) {
-      const unsigned long long c = s_bins[g];
-      if (c) {
-        atomicAdd(a.acc + 2 * g, c);
-        atomicAdd(a.acc + 2 * g + 1, s_bins[a.n_groups + g]);
-      }
-    }
-  }
-}
-
-template <int NL, int NF>
-void launch_scan_nf(laq_ctx* ctx, const ScanArgs& a, bool vec, int mode, int grid) {
-  const size_t smem = mode == 1 ? static_cast<size_t>(2 * a.n_groups) * sizeof(unsigned long long) : 0;
-  if (mode == 0) scan_kernel<NL, NF, 0><<<grid, kScanBlock, 0, ctx->stream>>>(a, vec);
-  else if (mode == 1) {
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-      LAQ_CUDA(cudaFuncSetAttribute(scan_kernel<NL, NF, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(2 * kSmemBins * sizeof(unsigned long long))));
-      attr_set = true;
-    }
-    scan_kernel<NL, NF, 1><<<grid, kScanBlock, smem, ctx->stream>>>(a, vec);
-  } else scan_kernel<NL, NF, 2><<<grid, kScanBlock, 0, ctx->stream>>>(a, vec);
-}
-
-template <int NL>
-void launch_scan_nl(laq_ctx* ctx, const ScanArgs& a, int nf, bool vec, int mode, int grid) {
-  switch (nf) {
-    case 0: launch_scan_nf<NL, 0>(ctx, a, vec, mode, grid); break;
-    case 1: launch_scan_nf<NL, 1>(ctx, a, vec, mode, grid); break;
-    case 2: launch_scan_nf<NL, 2>(ctx, a, vec, mode, grid); break;
-    case 3: launch_scan_nf<NL, 3>(ctx, a, vec, mode, grid); break;
-    case 4: launch_scan_nf<NL, 4>(ctx, a, vec, mode, grid); break;
-    default: fail(LAQ_ERR_UNSUPPORTED, "at most 4 fact filters per query");
-  }
-}
-
-void launch_scan(laq_ctx* ctx, const ScanArgs& a, int nl, int nf, bool vec, int mode, int grid) {
+void launch_scan(laq_ctx* ctx, const ScanArgs& a, int nl, int nf, int mode, bool pipe, bool vec, int grid,
+                 size_t smem) {
   switch (nl) {
-    case 0: launch_scan_nl<0>(ctx, a, nf, vec, mode, grid); break;
-    case 1: launch_scan_nl<1>(ctx, a, nf, vec, mode, grid); break;
-    case 2: launch_scan_nl<2>(ctx, a, nf, vec, mode, grid); break;
-    case 3: launch_scan_nl<3>(ctx, a, nf, vec, mode, grid); break;
-    case 4: launch_scan_nl<4>(ctx, a, nf, vec, mode, grid); break;
-    case 5: launch_scan_nl<5>(ctx, a, nf, vec, mode, grid); break;
-    case 6: launch_scan_nl<6>(ctx, a, nf, vec, mode, grid); break;
-    case 7: launch_scan_nl<7>(ctx, a, nf, vec, mode, grid); break;
-    case 8: launch_scan_nl<8>(ctx, a, nf, vec, mode, grid); break;
-    default: fail(LAQ_ERR_UNSUPPORTED, "at most 8 joins per query");
+    case 0: scan::launch_nl<0>(ctx, a, nf, mode, pipe, vec, grid, smem); break;
+    case 1: scan::launch_nl<1>(ctx, a, nf, mode, pipe, vec, grid, smem); break;
+    case 2: scan::launch_nl<2>(ctx, a, nf, mode, pipe, vec, grid, smem); break;
+    case 3: scan::launch_nl<3>(ctx, a, nf, mode, pipe, vec, grid, smem); break;
+    case 4: scan::launch_nl<4>(ctx, a, nf, mode, pipe, vec, grid, smem); break;
+    case 5: scan::launch_nl<5>(ctx, a, nf, mode, pipe, vec, grid, smem); break;
+    case 6: scan::launch_nl<6>(ctx, a, nf, mode, pipe, vec, grid, smem); break;
+    default: fail(LAQ_ERR_UNSUPPORTED, "at most 6 joins per query");
   }
   launched(ctx);
 }
@@ -413,25 +221,117 @@ struct laq_plan {
   int64_t fact_rows = 0;
   bool plain_sum = false;
   bool count_only = false;
-  // emission: group columns in group_by order
   struct GCol {
     int64_t mn, range, stride;
   };
-  std::vector<GCol> gcols;
-  // per link code tables
+  std::vector<GCol> gcols;  // emission: group columns in group_by order
   struct LinkCode {
     CodeArgs args;
     DevMem<int32_t> code;
     int64_t slots;
   };
-  std::vector<LinkCode> links;
-  DevMem<int64_t> sets;  // INSET values of every filter
-  ScanArgs scan{};
+  std::vector<LinkCode> links;  // in query join order
+  DevMem<int64_t> sets;         // INSET values of every filter
+  ScanArgs scan{};              // links in probe order
   int nl = 0, nf = 0;
   bool vec = true;
+  bool pipe = false;
   int mode = 0;
   int grid = 1;
+  size_t smem = 0;
+  int64_t bytes_per_row = 0;
 };
+
+namespace laq {
+namespace {
+
+void build_codes(laq_ctx* ctx, laq_plan* p) {
+  for (auto& lc : p->links) {
+    LAQ_CUDA(cudaMemsetAsync(lc.code.get(), 0xFF, lc.slots * sizeof(int32_t), ctx->stream));
+    if (lc.args.rows > 0) {
+      code_kernel<<<grid_for(lc.args.rows, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(lc.args);
+      launched(ctx);
+    }
+  }
+}
+
+// Decide the scan's probe order, shared-memory layout, grid and bins.
+void lay_out_scan(laq_ctx* ctx, laq_plan* p, const std::vector<const int32_t*>& fks,
+                  const std::vector<const Probe*>& probes, int64_t measure_min, int64_t measure_max, bool all_padded) {
+  ScanArgs& a = p->scan;
+  const int nl = static_cast<int>(p->links.size());
+  // Pass fraction of each link (dim rows surviving its filters), measured once.
+  std::vector<double> frac(nl, 1.0);
+  if (nl > 0) {
+    build_codes(ctx, p);
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(ctx->d_flags + 56);
+    for (int j = 0; j < nl; ++j) {
+      LAQ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), ctx->stream));
+      count_pass_kernel<<<grid_for(p->links[j].slots, 256, ctx->sm_count * 4), 256, 0, ctx->stream>>>(
+          p->links[j].code.get(), p->links[j].slots, cnt);
+      launched(ctx);
+      LAQ_CUDA(cudaMemcpyAsync(ctx->h_pinned + j, cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+      sync(ctx);
+    }
+    for (int j = 0; j < nl; ++j)
+      frac[j] = p->links[j].args.rows ? static_cast<double>(ctx->h_pinned[j]) / p->links[j].args.rows : 0.0;
+  }
+  std::vector<int> order(nl);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+    if (frac[x] != frac[y]) return frac[x] < frac[y];
+    return probes[x]->size < probes[y]->size;
+  });
+
+  // Shared-memory budget of the pipelined kernel.
+  int optin = 0;
+  LAQ_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+  const int64_t budget = static_cast<int64_t>(optin) - 2048;  // static smem + mbarriers
+  const int nc = p->nl + p->nf + (a.measure ? 1 : 0);
+  const int64_t stage_bytes = static_cast<int64_t>(nc) * scan::kTile * 4;
+  // 32-bit bins are exact when a tile's largest possible sum fits 32 bits; the
+  // kernel spills them to the 64-bit accumulator every flush_every tiles.
+  const int64_t vmax = a.measure ? std::max<int64_t>(measure_max, 1) : 1;
+  const bool narrow = a.measure == nullptr || (measure_min >= 0 && vmax < (int64_t{1} << 21));
+  const int64_t bin_bytes = p->mode == 1 ? (narrow ? 8 : 16) * p->G : 0;
+  int64_t tab_budget = budget - bin_bytes - 3 * stage_bytes;
+  int64_t tab_elems = 0;
+  for (int q = 0; q < nl; ++q) {
+    const int j = order[q];
+    const Probe& pr = *probes[j];
+    LinkProbe lp{pr.kind, pr.base, pr.size, pr.keys.get(), p->links[j].code.get(), -1};
+    const int64_t need = (pr.size + 7) & ~int64_t{7};
+    if (pr.kind == PROBE_DIRECT && pr.size <= kSmemTabMaxSlots && p->G <= 32767 && (tab_elems + need) * 2 <= tab_budget) {
+      lp.smem_off = static_cast<int>(tab_elems);
+      tab_elems += need;
+    }
+    a.fk[q] = fks[j];
+    a.link[q] = lp;
+  }
+  const int64_t rest = budget - bin_bytes - tab_elems * 2;
+  const int64_t stages = std::min<int64_t>(scan::kMaxStages, rest / std::max<int64_t>(stage_bytes, 1));
+  p->pipe = p->vec && all_padded && stages >= 2 && nc >= 1 && (p->mode != 1 || p->G <= kSmemBinsPipe);
+  if (p->pipe) {
+    a.stages = static_cast<int>(stages);
+    a.smem_tab_elems = static_cast<int>(tab_elems);
+    a.narrow_bins = narrow ? 1 : 0;
+    // u32 sums: between spills a CTA adds at most flush_every * kTile values <= vmax.
+    a.flush_every = std::max<int64_t>(1, (int64_t{1} << 32) / (int64_t{scan::kTile} * vmax) - 1);
+    p->smem = static_cast<size_t>(stages * stage_bytes + 8 * scan::kMaxStages + ((tab_elems * 2 + 15) & ~15) +
+                                  bin_bytes);
+    const int64_t tiles = (p->fact_rows + scan::kTile - 1) / scan::kTile;
+    p->grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctx->sm_count, tiles)));
+  } else {
+    for (int q = 0; q < nl; ++q) a.link[q].smem_off = -1;
+    p->smem = p->mode == 1 ? static_cast<size_t>(2 * p->G) * sizeof(unsigned long long) : 0;
+    const int per_sm = p->mode == 1 && p->G > 1024 ? 2 : 6;
+    p->grid = static_cast<int>(
+        std::max<int64_t>(1, std::min<int64_t>(ctx->sm_count * per_sm, (p->fact_rows + 1023) / 1024)));
+  }
+}
+
+}  // namespace
+}  // namespace laq
 
 extern "C" {
 
@@ -481,8 +381,11 @@ int laq_star_add_table(laq_star* s, const char* name, int32_t is_fact, int64_t r
         t.cols.push_back(col);
         continue;
       }
-      t.owned.emplace_back(static_cast<size_t>(std::max<int64_t>(rows, 1)));
+      // +4 elements: bulk copies of the last tile may read up to 12 bytes past the end.
+      t.owned.emplace_back(static_cast<size_t>(rows + 4));
       col.d = t.owned.back().get();
+      col.padded = true;
+      LAQ_CUDA(cudaMemsetAsync(col.d + rows, 0, 4 * sizeof(int32_t), ctx->stream));
       if (rows > 0) {
         if (int_width == 8) {
           unsigned long long init[2] = {~0ull, 0ull};
@@ -512,6 +415,7 @@ int laq_star_add_table(laq_star* s, const char* name, int32_t is_fact, int64_t r
       }
       t.cols.push_back(col);
     }
+    sync(ctx);
   });
 }
 
@@ -525,6 +429,7 @@ int laq_star_add_table_device(laq_star* s, const char* name, int32_t is_fact, in
       col.name = col_names[c];
       col.kind = col_kinds[c];
       col.d = const_cast<int32_t*>(d_cols[c]);
+      col.padded = rows % 4 == 0;  // whole 16-byte tail: no read past the end
       if (col.kind != LAQ_COL_FLOAT && rows > 0) minmax_i32(ctx, col.d, rows, &col.mn, &col.mx);
       if (col.kind == LAQ_COL_KEY && col.mn < 0)
         fail(LAQ_ERR_FORMAT, "table: negative key in column '" + col.name + "'");
@@ -555,7 +460,7 @@ int laq_query_prepare(laq_ctx* ctx, const laq_star* cs, const laq_query_desc* q,
     auto plan = std::make_unique<laq_plan>();
     plan->ctx = ctx;
     plan->fact_rows = fact.rows;
-    if (q->n_joins > kMaxLinks) fail(LAQ_ERR_UNSUPPORTED, "at most 8 joins per query");
+    if (q->n_joins > 6) fail(LAQ_ERR_UNSUPPORTED, "at most 6 joins per query");
 
     // Collect all INSET constants into one device array.
     std::vector<int64_t> sets;
@@ -599,13 +504,19 @@ int laq_query_prepare(laq_ctx* ctx, const laq_star* cs, const laq_query_desc* q,
     ScanArgs& a = plan->scan;
     a.n = fact.rows;
     a.n_groups = G;
-    bool aligned = true;
-    auto note_align = [&](const int32_t* p) { aligned = aligned && (reinterpret_cast<uintptr_t>(p) % 16 == 0); };
+    bool aligned = true, padded = true;
+    auto note = [&](const DevCol& c) {
+      aligned = aligned && (reinterpret_cast<uintptr_t>(c.d) % 16 == 0);
+      padded = padded && c.padded;
+    };
     // Measure (cli.cpp:100-101); NULL = count survivors only.
+    int64_t mmin = 0, mmax = 0;
     if (q->measure) {
       const DevCol& mcol = int_col(fact, q->measure);
       a.measure = mcol.d;
-      note_align(mcol.d);
+      mmin = mcol.mn;
+      mmax = mcol.mx;
+      note(mcol);
     } else {
       a.measure = nullptr;
       plan->count_only = true;
@@ -621,7 +532,7 @@ int laq_query_prepare(laq_ctx* ctx, const laq_star* cs, const laq_query_desc* q,
       check_pred_type(*c, f);
       if (nf >= kMaxFactFilters) fail(LAQ_ERR_UNSUPPORTED, "at most 4 fact filters per query");
       a.ff[nf++] = FactFilter{c->d, f.kind, f.lo, f.hi, dsets + set_off[i], static_cast<int>(f.set_len)};
-      note_align(c->d);
+      note(*c);
     }
     plan->nf = nf;
 
@@ -630,11 +541,12 @@ int laq_query_prepare(laq_ctx* ctx, const laq_star* cs, const laq_query_desc* q,
       if (q->group_by[g].target != -1) continue;
       if (a.n_fgroups >= kMaxFactGroups) fail(LAQ_ERR_UNSUPPORTED, "at most 4 fact group columns");
       a.fg[a.n_fgroups++] = FactGroup{gc[g]->d, plan->gcols[g].mn, plan->gcols[g].stride};
-      note_align(gc[g]->d);
     }
 
     // Links: probe (cached per dim/pk) + per-query code table.
     plan->links.resize(q->n_joins);
+    std::vector<const int32_t*> fks(q->n_joins);
+    std::vector<const Probe*> probes(q->n_joins);
     for (int j = 0; j < q->n_joins; ++j) {
       const laq_link_desc& l = q->joins[j];
       const DevCol& fk = int_col(fact, l.fact_fk);
@@ -662,31 +574,23 @@ int laq_query_prepare(laq_ctx* ctx, const laq_star* cs, const laq_query_desc* q,
         if (ca.n_groups >= kMaxDimGroups) fail(LAQ_ERR_UNSUPPORTED, "at most 4 group columns per dimension");
         ca.g[ca.n_groups++] = DimGroup{gc[g]->d, plan->gcols[g].mn, plan->gcols[g].stride};
       }
-      a.fk[j] = fk.d;
-      a.link[j] = LinkProbe{pr.kind, pr.base, pr.size, pr.keys.get(), lc.code.get()};
-      note_align(fk.d);
+      fks[j] = fk.d;
+      probes[j] = &pr;
+      note(fk);
     }
     plan->nl = q->n_joins;
     plan->vec = aligned;
-    plan->mode = G == 1 ? 0 : (G <= kSmemBins ? 1 : 2);
-    // Persistent grid: enough resident blocks to cover every SM several times.
-    const int per_sm = plan->mode == 1 && G > 1024 ? 2 : 6;
-    plan->grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctx->sm_count * per_sm, (fact.rows + 1023) / 1024)));
+    plan->mode = G == 1 ? 0 : (G <= kSmemBinsPipe ? 1 : (G <= kSmemBinsLdg ? 1 : 2));
+    plan->bytes_per_row = 4 * (plan->nl + plan->nf + a.n_fgroups + (a.measure ? 1 : 0));
+    lay_out_scan(ctx, plan.get(), fks, probes, mmin, mmax, padded);
+    if (!plan->pipe && plan->mode == 1 && G > kSmemBinsLdg) plan->mode = 2;
     *h_n_groups = G;
     *out = plan.release();
   });
 }
 
 int laq_plan_build_codes(laq_ctx* ctx, laq_plan* p) {
-  return guard(ctx, [&] {
-    for (auto& lc : p->links) {
-      LAQ_CUDA(cudaMemsetAsync(lc.code.get(), 0xFF, lc.slots * sizeof(int32_t), ctx->stream));
-      if (lc.args.rows > 0) {
-        code_kernel<<<grid_for(lc.args.rows, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(lc.args);
-        launched(ctx);
-      }
-    }
-  });
+  return guard(ctx, [&] { build_codes(ctx, p); });
 }
 
 int laq_plan_scan(laq_ctx* ctx, laq_plan* p, int64_t* d_acc, int32_t accumulate) {
@@ -695,7 +599,7 @@ int laq_plan_scan(laq_ctx* ctx, laq_plan* p, int64_t* d_acc, int32_t accumulate)
     if (p->fact_rows == 0) return;
     ScanArgs a = p->scan;
     a.acc = reinterpret_cast<unsigned long long*>(d_acc);
-    launch_scan(ctx, a, p->nl, p->nf, p->vec, p->mode, p->grid);
+    launch_scan(ctx, a, p->nl, p->nf, p->mode, p->pipe, p->vec, p->grid, p->smem);
   });
 }
 
@@ -704,10 +608,7 @@ int laq_plan_execute(laq_ctx* ctx, laq_plan* p, int64_t* d_acc, int32_t accumula
   return rc ? rc : laq_plan_scan(ctx, p, d_acc, accumulate);
 }
 
-int64_t laq_plan_bytes_per_row(const laq_plan* p) {
-  // fks + fact filter columns + fact group columns + measure, int32 each.
-  return 4 * (p->nl + p->nf + p->scan.n_fgroups + (p->scan.measure ? 1 : 0));
-}
+int64_t laq_plan_bytes_per_row(const laq_plan* p) { return p->bytes_per_row; }
 
 int laq_plan_emit(const laq_plan* p, const int64_t* acc, double* out, int64_t cap, int64_t* rows, int64_t* cols) {
   try {
@@ -775,7 +676,8 @@ int laq_measure_selectivity(laq_ctx* ctx, const laq_star* s, const laq_query_des
   int rc = laq_query_prepare(ctx, s, &c, &p, &G);
   if (rc) return rc;
   rc = guard(ctx, [&] {
-    const int rc2 = laq_plan_execute(ctx, p, ctx->d_flags + 32, 0);
+    // prepare already built the code tables (pass fractions): scan only.
+    const int rc2 = laq_plan_scan(ctx, p, ctx->d_flags + 32, 0);
     if (rc2) fail(rc2, ctx->err);
     LAQ_CUDA(cudaMemcpyAsync(ctx->h_pinned, ctx->d_flags + 32, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
     sync(ctx);

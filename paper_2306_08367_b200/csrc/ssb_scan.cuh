@@ -1,0 +1,472 @@
+// K4 scan kernels: the fused filter -> star probe -> group-id -> exact int64
+// (count, sum) aggregation over the fact table.  Included by ssb.cu only.
+//
+// scan_pipe_kernel (primary, sm_100a):
+//   * one persistent CTA per SM, 512 threads, static round-robin over
+//     2048-row tiles;
+//   * thread 0 streams every touched int32 fact column of a tile into shared
+//     memory with cp.async.bulk (the TMA bulk-copy engine) completing on a
+//     per-stage mbarrier, S stages ahead (S = 2..4 by smem budget), so the
+//     HBM stream never waits on the probes;
+//   * small per-link code tables (<= 48K slots, int16) are staged in shared
+//     memory once per CTA; larger ones (e.g. part at SF>=10) are gathered
+//     from L2 (int32, read-only path);
+//   * links are probed in ascending pass-fraction order (set on the host), so
+//     the L2 gathers of the big dimension only happen for rows that survived
+//     the cheap, selective smem-resident ones;
+//   * per-group (count, sum) bins live in shared memory as 32-bit counters
+//     updated with native ATOMS.ADD (64-bit shared atomics are CAS loops on
+//     this part) whenever the host proves a CTA's partial sums fit 32 bits;
+//     bins are merged into the global 64-bit accumulator once per CTA.
+// scan_ldg_kernel (fallback): plain vectorised loads, for column bases that are
+// not 16-byte aligned (e.g. arbitrary row-shard views).
+#pragma once
+
+#include "probe.cuh"
+
+namespace laq {
+namespace scan {
+
+constexpr int kMaxLinks = 8;
+constexpr int kMaxFactFilters = 4;
+constexpr int kMaxFactGroups = 4;
+constexpr int kMaxCols = kMaxLinks + kMaxFactFilters + 1;
+constexpr int kPipeThreads = 512;
+constexpr int kTile = 4 * kPipeThreads;  // 2048 rows
+constexpr int kMaxStages = 4;
+
+struct LinkProbe {
+  int kind;
+  int64_t base, size;
+  const int64_t* keys;
+  const int32_t* code;  // per slot, global
+  int smem_off;         // >= 0: int16 code table staged in smem at this element offset
+};
+
+struct FactFilter {
+  const int32_t* col;
+  int kind;
+  int64_t lo, hi;
+  const int64_t* set;
+  int set_len;
+};
+
+struct FactGroup {
+  const int32_t* col;
+  int64_t mn, stride;
+};
+
+struct ScanArgs {
+  int64_t n;
+  const int32_t* fk[kMaxLinks];
+  LinkProbe link[kMaxLinks];
+  FactFilter ff[kMaxFactFilters];
+  int n_fgroups;
+  FactGroup fg[kMaxFactGroups];
+  const int32_t* measure;  // nullptr: count only
+  int64_t n_groups;
+  unsigned long long* acc;  // [2*G]: count, sum
+  // pipe kernel layout
+  int stages;
+  int smem_tab_elems;  // int16 elements of staged code tables
+  int narrow_bins;     // 1: u32 (count, sum) bins, flushed every flush_every tiles
+  int64_t flush_every; // tiles per CTA after which u32 bins could overflow
+};
+
+__device__ __forceinline__ bool pred_eval(int kind, int64_t v, int64_t lo, int64_t hi, const int64_t* set, int n) {
+  switch (kind) {  // predicate.hpp:84-93
+    case LAQ_PRED_LT: return v < lo;
+    case LAQ_PRED_LE: return v <= lo;
+    case LAQ_PRED_EQ: return v == lo;
+    case LAQ_PRED_GE: return v >= lo;
+    case LAQ_PRED_GT: return v > lo;
+    case LAQ_PRED_BETWEEN: return v >= lo && v <= hi;
+    default: {  // InSet: binary search over the sorted set (predicate.hpp:90)
+      int a = 0, b = n;
+      while (a < b) {
+        const int m = (a + b) >> 1;
+        const int64_t s = set[m];
+        if (s == v) return true;
+        if (s < v) a = m + 1; else b = m;
+      }
+      return false;
+    }
+  }
+}
+
+__device__ __forceinline__ int32_t hash_code(const LinkProbe& p, int32_t key) {
+  const uint64_t mask = static_cast<uint64_t>(p.size) - 1;
+  uint64_t h = static_cast<uint64_t>(static_cast<int64_t>(key)) * 0x9E3779B97F4A7C15ull;
+  h ^= h >> 29;
+  for (uint64_t s = h & mask;; s = (s + 1) & mask) {
+    const int64_t k = __ldg(p.keys + s);
+    if (k == key) return __ldg(p.code + s);
+    if (k < 0) return -1;
+  }
+}
+
+__device__ __forceinline__ int comp(const int4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
+
+// Probe one link for 4 rows; loads are independent (issued together).
+__device__ __forceinline__ void probe4(const LinkProbe& p, const int4& k, const int16_t* s_tab, bool (&alive)[4],
+                                       int64_t (&gid)[4]) {
+  int32_t c[4];
+  if (p.kind == PROBE_HASH) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c[i] = alive[i] ? hash_code(p, comp(k, i)) : -1;
+  } else {
+    uint32_t s[4];
+    bool ok[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      s[i] = static_cast<uint32_t>(comp(k, i) - static_cast<int32_t>(p.base));
+      ok[i] = alive[i] && static_cast<int64_t>(comp(k, i)) - p.base >= 0 &&
+              static_cast<int64_t>(comp(k, i)) - p.base < p.size;
+    }
+    if (p.smem_off >= 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) c[i] = ok[i] ? static_cast<int32_t>(s_tab[p.smem_off + s[i]]) : -1;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) c[i] = ok[i] ? __ldg(p.code + s[i]) : -1;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    alive[i] = alive[i] && c[i] >= 0;
+    gid[i] += c[i];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// PTX helpers: mbarrier + bulk async copy (TMA engine, 1-D)
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "LAQ_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra LAQ_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// ---------------------------------------------------------------------------
+// the pipelined scan
+// ---------------------------------------------------------------------------
+
+template <int NL, int NF, int MODE>
+__global__ void __launch_bounds__(kPipeThreads, 1) scan_pipe_kernel(const ScanArgs a) {
+  constexpr int NCmax = NL + NF + 1;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int nc = NL + NF + (a.measure ? 1 : 0);
+  const int S = a.stages;
+  const int stage_bytes = nc * kTile * 4;
+  unsigned char* stage_base = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
+  int16_t* s_tab = reinterpret_cast<int16_t*>(full + kMaxStages);
+  unsigned char* bins_base = reinterpret_cast<unsigned char*>(s_tab) + ((a.smem_tab_elems * 2 + 15) & ~15);
+  uint32_t* b32 = reinterpret_cast<uint32_t*>(bins_base);              // [G] counts, [G] sums
+  unsigned long long* b64 = reinterpret_cast<unsigned long long*>(bins_base);
+
+  const int tid = threadIdx.x;
+  const int64_t n_tiles = (a.n + kTile - 1) / kTile;
+  const int64_t my_tiles = n_tiles > blockIdx.x ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+  const int32_t* cols[NCmax];
+#pragma unroll
+  for (int j = 0; j < NL; ++j) cols[j] = a.fk[j];
+#pragma unroll
+  for (int f = 0; f < NF; ++f) cols[NL + f] = a.ff[f].col;
+  cols[NL + NF] = a.measure;
+
+  uint64_t policy = 0;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(full + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    policy = evict_first_policy();
+  }
+  __syncthreads();
+
+  auto issue = [&](int64_t i) {  // thread 0: load my i-th tile into stage i % S
+    const int64_t tile = blockIdx.x + i * gridDim.x;
+    const int64_t row0 = tile * kTile;
+    const int64_t rows = min(static_cast<int64_t>(kTile), a.n - row0);
+    const uint32_t bytes = static_cast<uint32_t>((rows * 4 + 15) & ~15ll);
+    const int st = static_cast<int>(i % S);
+    uint64_t* bar = full + st;
+    mbar_arrive_expect_tx(bar, bytes * nc);
+#pragma unroll
+    for (int c = 0; c < NCmax; ++c)
+      if (c < nc) bulk_g2s(stage_base + st * stage_bytes + c * kTile * 4, cols[c] + row0, bytes, bar, policy);
+  };
+  if (tid == 0)
+    for (int64_t i = 0; i < S && i < my_tiles; ++i) issue(i);
+
+  // Stage code tables (int16) and zero the bins while the first tiles land.
+#pragma unroll
+  for (int j = 0; j < NL; ++j) {
+    const LinkProbe& p = a.link[j];
+    if (p.smem_off >= 0)
+      for (int64_t s = tid; s < p.size; s += kPipeThreads) s_tab[p.smem_off + s] = static_cast<int16_t>(__ldg(p.code + s));
+  }
+  if constexpr (MODE == 1) {
+    const int64_t words = a.narrow_bins ? 2 * a.n_groups : 4 * a.n_groups;
+    for (int64_t g = tid; g < words; g += kPipeThreads) b32[g] = 0;
+  }
+  __syncthreads();
+
+  unsigned long long r_cnt = 0, r_sum = 0;
+  for (int64_t i = 0; i < my_tiles; ++i) {
+    const int st = static_cast<int>(i % S);
+    mbar_wait(full + st, static_cast<uint32_t>((i / S) & 1));
+    const int64_t row0 = (blockIdx.x + i * gridDim.x) * kTile + tid * 4;
+    const unsigned char* sb = stage_base + st * stage_bytes + tid * 16;
+
+    int4 kv[NL > 0 ? NL : 1], fv[NF > 0 ? NF : 1], mv;
+#pragma unroll
+    for (int j = 0; j < NL; ++j) kv[j] = *reinterpret_cast<const int4*>(sb + j * kTile * 4);
+#pragma unroll
+    for (int f = 0; f < NF; ++f) fv[f] = *reinterpret_cast<const int4*>(sb + (NL + f) * kTile * 4);
+    if (a.measure) mv = *reinterpret_cast<const int4*>(sb + (NL + NF) * kTile * 4);
+
+    bool alive[4];
+    int64_t gid[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      alive[r] = row0 + r < a.n;
+      gid[r] = 0;
+    }
+#pragma unroll
+    for (int f = 0; f < NF; ++f)
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        alive[r] = alive[r] && pred_eval(a.ff[f].kind, comp(fv[f], r), a.ff[f].lo, a.ff[f].hi, a.ff[f].set,
+                                         a.ff[f].set_len);
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+      const bool any = alive[0] | alive[1] | alive[2] | alive[3];
+      if (any) probe4(a.link[j], kv[j], s_tab, alive, gid);
+    }
+    for (int g = 0; g < a.n_fgroups; ++g)
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (alive[r]) gid[r] += (static_cast<int64_t>(__ldg(a.fg[g].col + row0 + r)) - a.fg[g].mn) * a.fg[g].stride;
+
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      if (!alive[r]) continue;
+      const long long v = a.measure ? static_cast<long long>(comp(mv, r)) : 0ll;
+      if constexpr (MODE == 0) {
+        r_cnt += 1;
+        r_sum += static_cast<unsigned long long>(v);
+      } else if constexpr (MODE == 1) {
+        if (a.narrow_bins) {
+          atomicAdd(b32 + gid[r], 1u);
+          if (a.measure) atomicAdd(b32 + a.n_groups + gid[r], static_cast<uint32_t>(v));
+        } else {
+          atomicAdd(b64 + gid[r], 1ull);
+          if (a.measure) atomicAdd(b64 + a.n_groups + gid[r], static_cast<unsigned long long>(v));
+        }
+      } else {
+        atomicAdd(a.acc + 2 * gid[r], 1ull);
+        if (a.measure) atomicAdd(a.acc + 2 * gid[r] + 1, static_cast<unsigned long long>(v));
+      }
+    }
+    __syncthreads();  // every thread is done with stage st
+    if (tid == 0 && i + S < my_tiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(i + S);
+    }
+    if constexpr (MODE == 1) {
+      if (a.narrow_bins && (i + 1) % a.flush_every == 0 && i + 1 < my_tiles) {
+        // Spill the 32-bit partials before they can wrap.
+        for (int64_t g = tid; g < a.n_groups; g += kPipeThreads) {
+          const uint32_t c = b32[g];
+          if (c) {
+            atomicAdd(a.acc + 2 * g, static_cast<unsigned long long>(c));
+            atomicAdd(a.acc + 2 * g + 1, static_cast<unsigned long long>(b32[a.n_groups + g]));
+            b32[g] = 0;
+            b32[a.n_groups + g] = 0;
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+
+  if constexpr (MODE == 0) {
+    for (int o = 16; o; o >>= 1) {
+      r_cnt += __shfl_xor_sync(0xffffffffu, r_cnt, o);
+      r_sum += __shfl_xor_sync(0xffffffffu, r_sum, o);
+    }
+    __shared__ unsigned long long w_cnt[kPipeThreads / 32], w_sum[kPipeThreads / 32];
+    if ((tid & 31) == 0) {
+      w_cnt[tid >> 5] = r_cnt;
+      w_sum[tid >> 5] = r_sum;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long c = 0, s = 0;
+      for (int w = 0; w < kPipeThreads / 32; ++w) {
+        c += w_cnt[w];
+        s += w_sum[w];
+      }
+      if (c) {
+        atomicAdd(a.acc, c);
+        atomicAdd(a.acc + 1, s);
+      }
+    }
+  } else if constexpr (MODE == 1) {
+    __syncthreads();
+    for (int64_t g = tid; g < a.n_groups; g += kPipeThreads) {
+      if (a.narrow_bins) {
+        const uint32_t c = b32[g];
+        if (c) {
+          atomicAdd(a.acc + 2 * g, static_cast<unsigned long long>(c));
+          atomicAdd(a.acc + 2 * g + 1, static_cast<unsigned long long>(b32[a.n_groups + g]));
+        }
+      } else {
+        const unsigned long long c = b64[g];
+        if (c) {
+          atomicAdd(a.acc + 2 * g, c);
+          atomicAdd(a.acc + 2 * g + 1, b64[a.n_groups + g]);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fallback: vectorised-load scan (any alignment), shared 64-bit bins
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ int4 ld4(const int32_t* p, int64_t row0, int64_t n, bool vec) {
+  if (vec && row0 + 4 <= n) return __ldcs(reinterpret_cast<const int4*>(p + row0));
+  int4 v;
+  v.x = row0 + 0 < n ? p[row0 + 0] : 0;
+  v.y = row0 + 1 < n ? p[row0 + 1] : 0;
+  v.z = row0 + 2 < n ? p[row0 + 2] : 0;
+  v.w = row0 + 3 < n ? p[row0 + 3] : 0;
+  return v;
+}
+
+template <int NL, int NF, int MODE>
+__global__ void __launch_bounds__(256) scan_ldg_kernel(const ScanArgs a, const bool vec) {
+  extern __shared__ unsigned long long s_bins[];  // MODE 1: [G] counts then [G] sums
+  if constexpr (MODE == 1) {
+    for (int64_t g = threadIdx.x; g < 2 * a.n_groups; g += blockDim.x) s_bins[g] = 0;
+    __syncthreads();
+  }
+  unsigned long long r_cnt = 0, r_sum = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+  for (int64_t row0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; row0 < a.n; row0 += stride) {
+    int4 fk[NL > 0 ? NL : 1], fv[NF > 0 ? NF : 1], mv;
+#pragma unroll
+    for (int j = 0; j < NL; ++j) fk[j] = ld4(a.fk[j], row0, a.n, vec);
+#pragma unroll
+    for (int f = 0; f < NF; ++f) fv[f] = ld4(a.ff[f].col, row0, a.n, vec);
+    if (a.measure) mv = ld4(a.measure, row0, a.n, vec);
+    int64_t gid[4];
+    bool alive[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      alive[i] = row0 + i < a.n;
+      gid[i] = 0;
+    }
+#pragma unroll
+    for (int f = 0; f < NF; ++f)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        alive[i] = alive[i] && pred_eval(a.ff[f].kind, comp(fv[f], i), a.ff[f].lo, a.ff[f].hi, a.ff[f].set,
+                                         a.ff[f].set_len);
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+      LinkProbe p = a.link[j];
+      p.smem_off = -1;
+      probe4(p, fk[j], nullptr, alive, gid);
+    }
+    for (int g = 0; g < a.n_fgroups; ++g) {
+      const int4 v = ld4(a.fg[g].col, row0, a.n, vec);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) gid[i] += (static_cast<int64_t>(comp(v, i)) - a.fg[g].mn) * a.fg[g].stride;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (!alive[i]) continue;
+      const unsigned long long val = a.measure ? static_cast<unsigned long long>(static_cast<long long>(comp(mv, i))) : 0ull;
+      if constexpr (MODE == 0) {
+        r_cnt += 1;
+        r_sum += val;
+      } else if constexpr (MODE == 1) {
+        atomicAdd(s_bins + gid[i], 1ull);
+        if (a.measure) atomicAdd(s_bins + a.n_groups + gid[i], val);
+      } else {
+        atomicAdd(a.acc + 2 * gid[i], 1ull);
+        if (a.measure) atomicAdd(a.acc + 2 * gid[i] + 1, val);
+      }
+    }
+  }
+  if constexpr (MODE == 0) {
+    for (int o = 16; o; o >>= 1) {
+      r_cnt += __shfl_xor_sync(0xffffffffu, r_cnt, o);
+      r_sum += __shfl_xor_sync(0xffffffffu, r_sum, o);
+    }
+    __shared__ unsigned long long w_cnt[8], w_sum[8];
+    if ((threadIdx.x & 31) == 0) {
+      w_cnt[threadIdx.x >> 5] = r_cnt;
+      w_sum[threadIdx.x >> 5] = r_sum;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long c = 0, s = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        c += w_cnt[w];
+        s += w_sum[w];
+      }
+      if (c) {
+        atomicAdd(a.acc, c);
+        atomicAdd(a.acc + 1, s);
+      }
+    }
+  } else if constexpr (MODE == 1) {
+    __syncthreads();
+    for (int64_t g = threadIdx.x; g < a.n_groups; g += blockDim.x) {
+      const unsigned long long c = s_bins[g];
+      if (c) {
+        atomicAdd(a.acc + 2 * g, c);
+        atomicAdd(a.acc + 2 * g + 1, s_bins[a.n_groups + g]);
+      }
+    }
+  }
+}
+
+}  // namespace scan
+}  // namespace laq

@@ -1,0 +1,4 @@
+// K4 scan kernels for queries joining 3 dimension(s).
+#include "ssb_scan_inst.cuh"
+
+LAQ_SCAN_INSTANTIATE(3)
