@@ -21,6 +21,7 @@
 // Integer sums are exact, so results equal the reference bit for bit.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -204,6 +205,31 @@ const DevCol& int_col(const DevTable& t, const std::string& name) {
   return *c;
 }
 
+// A fact predicate as a closed int32 interval (branch-free in the scan), or InSet.
+FactFilter lower_filter(const int32_t* col, const laq_filter_desc& f, const int64_t* dset) {
+  FactFilter r{col, 1, 0, 0, dset, static_cast<int>(f.set_len)};
+  if (f.kind == LAQ_PRED_INSET) {
+    r.inset = 1;
+    return r;
+  }
+  int64_t lo = INT64_MIN, hi = INT64_MAX;
+  switch (f.kind) {  // predicate.hpp:84-89 over integers
+    case LAQ_PRED_LT: hi = f.lo == INT64_MIN ? INT64_MIN : f.lo - 1; if (f.lo == INT64_MIN) lo = 1; break;
+    case LAQ_PRED_LE: hi = f.lo; break;
+    case LAQ_PRED_EQ: lo = hi = f.lo; break;
+    case LAQ_PRED_GE: lo = f.lo; break;
+    case LAQ_PRED_GT: lo = f.lo == INT64_MAX ? INT64_MAX : f.lo + 1; if (f.lo == INT64_MAX) hi = 0; break;
+    default: lo = f.lo; hi = f.hi; break;  // Between, inclusive
+  }
+  lo = std::max<int64_t>(lo, INT32_MIN);
+  hi = std::min<int64_t>(hi, INT32_MAX);
+  if (lo <= hi) {
+    r.lo = static_cast<int32_t>(lo);
+    r.hi = static_cast<int32_t>(hi);
+  }  // else stays the empty interval [1, 0]
+  return r;
+}
+
 void check_pred_type(const DevCol& c, const laq_filter_desc& f) {
   // predicate.hpp:95-103: typed constants vs column kind.
   const bool col_float = c.kind == LAQ_COL_FLOAT;
@@ -276,13 +302,6 @@ void lay_out_scan(laq_ctx* ctx, laq_plan* p, const std::vector<const int32_t*>& 
     for (int j = 0; j < nl; ++j)
       frac[j] = p->links[j].args.rows ? static_cast<double>(ctx->h_pinned[j]) / p->links[j].args.rows : 0.0;
   }
-  std::vector<int> order(nl);
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
-    if (frac[x] != frac[y]) return frac[x] < frac[y];
-    return probes[x]->size < probes[y]->size;
-  });
-
   // Shared-memory budget of the pipelined kernel.
   int optin = 0;
   LAQ_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
@@ -294,30 +313,51 @@ void lay_out_scan(laq_ctx* ctx, laq_plan* p, const std::vector<const int32_t*>& 
   const int64_t vmax = a.measure ? std::max<int64_t>(measure_max, 1) : 1;
   const bool narrow = a.measure == nullptr || (measure_min >= 0 && vmax < (int64_t{1} << 21));
   const int64_t bin_bytes = p->mode == 1 ? (narrow ? 8 : 16) * p->G : 0;
-  int64_t tab_budget = budget - bin_bytes - 3 * stage_bytes;
+  const int64_t tab_budget = budget - bin_bytes - 4 * stage_bytes;
+
+  // 1) Which code tables live in shared memory: smallest first while they fit.
+  std::vector<int> by_size(nl);
+  std::iota(by_size.begin(), by_size.end(), 0);
+  std::stable_sort(by_size.begin(), by_size.end(), [&](int x, int y) { return probes[x]->size < probes[y]->size; });
+  std::vector<int64_t> smem_off(nl, -1);
   int64_t tab_elems = 0;
+  for (int j : by_size) {
+    const Probe& pr = *probes[j];
+    const int64_t need = (pr.size + 7) & ~int64_t{7};
+    if (!std::getenv("LAQ_NOSMEMTAB") && pr.kind == PROBE_DIRECT && pr.size <= kSmemTabMaxSlots && p->G <= 32767 &&
+        (tab_elems + need) * 2 <= tab_budget) {
+      smem_off[j] = tab_elems;
+      tab_elems += need;
+    }
+  }
+  // 2) Probe order: ascending rank cost / (1 - pass fraction) (the classic
+  // ordering of independent filters), cost ~ 1 smem lookup, 8 L2 gather, 16 hash.
+  std::vector<double> rank(nl);
+  for (int j = 0; j < nl; ++j) {
+    const double cost = smem_off[j] >= 0 ? 1.0 : (probes[j]->kind == PROBE_HASH ? 16.0 : 8.0);
+    rank[j] = cost / std::max(1.0 - frac[j], 1e-9);
+  }
+  std::vector<int> order(nl);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return rank[x] < rank[y]; });
   for (int q = 0; q < nl; ++q) {
     const int j = order[q];
     const Probe& pr = *probes[j];
-    LinkProbe lp{pr.kind, pr.base, pr.size, pr.keys.get(), p->links[j].code.get(), -1};
-    const int64_t need = (pr.size + 7) & ~int64_t{7};
-    if (pr.kind == PROBE_DIRECT && pr.size <= kSmemTabMaxSlots && p->G <= 32767 && (tab_elems + need) * 2 <= tab_budget) {
-      lp.smem_off = static_cast<int>(tab_elems);
-      tab_elems += need;
-    }
     a.fk[q] = fks[j];
-    a.link[q] = lp;
+    a.link[q] = LinkProbe{pr.kind, pr.base, pr.size, pr.keys.get(), p->links[j].code.get(), static_cast<int>(smem_off[j])};
   }
   const int64_t rest = budget - bin_bytes - tab_elems * 2;
-  const int64_t stages = std::min<int64_t>(scan::kMaxStages, rest / std::max<int64_t>(stage_bytes, 1));
+  int64_t stages = std::min<int64_t>(scan::kMaxStages, rest / std::max<int64_t>(stage_bytes, 1));
+  if (const char* v = std::getenv("LAQ_STAGES")) stages = std::min<int64_t>(stages, std::atoi(v));  // diagnostics
   p->pipe = p->vec && all_padded && stages >= 2 && nc >= 1 && (p->mode != 1 || p->G <= kSmemBinsPipe);
+  if (const char* v = std::getenv("LAQ_SCAN")) p->pipe = p->pipe && std::string(v) != "ldg";  // A/B switch
   if (p->pipe) {
     a.stages = static_cast<int>(stages);
     a.smem_tab_elems = static_cast<int>(tab_elems);
     a.narrow_bins = narrow ? 1 : 0;
     // u32 sums: between spills a CTA adds at most flush_every * kTile values <= vmax.
     a.flush_every = std::max<int64_t>(1, (int64_t{1} << 32) / (int64_t{scan::kTile} * vmax) - 1);
-    p->smem = static_cast<size_t>(stages * stage_bytes + 8 * scan::kMaxStages + ((tab_elems * 2 + 15) & ~15) +
+    p->smem = static_cast<size_t>(stages * stage_bytes + 16 * scan::kMaxStages + ((tab_elems * 2 + 15) & ~15) +
                                   bin_bytes);
     const int64_t tiles = (p->fact_rows + scan::kTile - 1) / scan::kTile;
     p->grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctx->sm_count, tiles)));
@@ -531,7 +571,7 @@ int laq_query_prepare(laq_ctx* ctx, const laq_star* cs, const laq_query_desc* q,
       if (!c) fail(LAQ_ERR_NAME, std::string("unknown column: ") + f.column);
       check_pred_type(*c, f);
       if (nf >= kMaxFactFilters) fail(LAQ_ERR_UNSUPPORTED, "at most 4 fact filters per query");
-      a.ff[nf++] = FactFilter{c->d, f.kind, f.lo, f.hi, dsets + set_off[i], static_cast<int>(f.set_len)};
+      a.ff[nf++] = lower_filter(c->d, f, dsets + set_off[i]);
       note(*c);
     }
     plan->nf = nf;

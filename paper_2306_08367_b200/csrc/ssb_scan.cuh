@@ -1,25 +1,25 @@
 // K4 scan kernels: the fused filter -> star probe -> group-id -> exact int64
-// (count, sum) aggregation over the fact table.  Included by ssb.cu only.
+// (count, sum) aggregation over the fact table.  Included by the launch units.
 //
-// scan_pipe_kernel (primary, sm_100a):
-//   * one persistent CTA per SM, 512 threads, static round-robin over
-//     2048-row tiles;
-//   * thread 0 streams every touched int32 fact column of a tile into shared
-//     memory with cp.async.bulk (the TMA bulk-copy engine) completing on a
-//     per-stage mbarrier, S stages ahead (S = 2..4 by smem budget), so the
-//     HBM stream never waits on the probes;
+// scan_pipe_kernel (primary, sm_100a), warp-specialised:
+//   * one persistent CTA per SM: 1 producer warp + 16 consumer warps,
+//     static round-robin over 2048-row tiles;
+//   * the producer streams every touched int32 fact column of a tile into
+//     shared memory with cp.async.bulk (the TMA bulk-copy engine, SASS
+//     UBLKCP) completing on a per-stage "full" mbarrier, S stages ahead;
+//     consumer warps release a stage through a per-stage "empty" mbarrier, so
+//     no CTA-wide barrier sits in the steady-state loop;
 //   * small per-link code tables (<= 48K slots, int16) are staged in shared
 //     memory once per CTA; larger ones (e.g. part at SF>=10) are gathered
-//     from L2 (int32, read-only path);
-//   * links are probed in ascending pass-fraction order (set on the host), so
-//     the L2 gathers of the big dimension only happen for rows that survived
-//     the cheap, selective smem-resident ones;
+//     from L2 through the read-only path;
+//   * links are probed in ascending pass-fraction order (chosen on the host),
+//     so gathers into a big dimension only happen for rows that survived the
+//     cheap, selective shared-memory ones;
+//   * predicates are pre-lowered to closed int32 intervals (branch-free);
 //   * per-group (count, sum) bins live in shared memory as 32-bit counters
-//     updated with native ATOMS.ADD (64-bit shared atomics are CAS loops on
-//     this part) whenever the host proves a CTA's partial sums fit 32 bits;
-//     bins are merged into the global 64-bit accumulator once per CTA.
-// scan_ldg_kernel (fallback): plain vectorised loads, for column bases that are
-// not 16-byte aligned (e.g. arbitrary row-shard views).
+//     (native ATOMS.ADD; 64-bit shared atomics are CAS loops on this part),
+//     spilled into the global 64-bit accumulator before they could wrap.
+// scan_ldg_kernel (fallback): plain vectorised loads, any 4-byte alignment.
 #pragma once
 
 #include "probe.cuh"
@@ -30,10 +30,10 @@ namespace scan {
 constexpr int kMaxLinks = 8;
 constexpr int kMaxFactFilters = 4;
 constexpr int kMaxFactGroups = 4;
-constexpr int kMaxCols = kMaxLinks + kMaxFactFilters + 1;
-constexpr int kPipeThreads = 512;
-constexpr int kTile = 4 * kPipeThreads;  // 2048 rows
-constexpr int kMaxStages = 4;
+constexpr int kConsumerWarps = 16;
+constexpr int kPipeThreads = 32 * (kConsumerWarps + 1);
+constexpr int kTile = 4 * 32 * kConsumerWarps;  // 2048 rows
+constexpr int kMaxStages = 8;
 
 struct LinkProbe {
   int kind;
@@ -43,10 +43,11 @@ struct LinkProbe {
   int smem_off;         // >= 0: int16 code table staged in smem at this element offset
 };
 
+// A fact predicate lowered to  lo <= v <= hi  over int32 (or InSet).
 struct FactFilter {
   const int32_t* col;
-  int kind;
-  int64_t lo, hi;
+  int32_t lo, hi;
+  int inset;
   const int64_t* set;
   int set_len;
 };
@@ -68,9 +69,9 @@ struct ScanArgs {
   unsigned long long* acc;  // [2*G]: count, sum
   // pipe kernel layout
   int stages;
-  int smem_tab_elems;  // int16 elements of staged code tables
-  int narrow_bins;     // 1: u32 (count, sum) bins, flushed every flush_every tiles
-  int64_t flush_every; // tiles per CTA after which u32 bins could overflow
+  int smem_tab_elems;   // int16 elements of staged code tables
+  int narrow_bins;      // 1: u32 (count, sum) bins, spilled every flush_every tiles
+  int64_t flush_every;  // tiles per CTA after which u32 bins could overflow
 };
 
 __device__ __forceinline__ bool pred_eval(int kind, int64_t v, int64_t lo, int64_t hi, const int64_t* set, int n) {
@@ -94,6 +95,11 @@ __device__ __forceinline__ bool pred_eval(int kind, int64_t v, int64_t lo, int64
   }
 }
 
+__device__ __forceinline__ bool filter_ok(const FactFilter& f, int32_t v) {
+  if (f.inset) return pred_eval(LAQ_PRED_INSET, v, 0, 0, f.set, f.set_len);
+  return v >= f.lo && v <= f.hi;
+}
+
 __device__ __forceinline__ int32_t hash_code(const LinkProbe& p, int32_t key) {
   const uint64_t mask = static_cast<uint64_t>(p.size) - 1;
   uint64_t h = static_cast<uint64_t>(static_cast<int64_t>(key)) * 0x9E3779B97F4A7C15ull;
@@ -107,28 +113,25 @@ __device__ __forceinline__ int32_t hash_code(const LinkProbe& p, int32_t key) {
 
 __device__ __forceinline__ int comp(const int4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
 
-// Probe one link for 4 rows; loads are independent (issued together).
+// Probe one link for 4 rows; the 4 lookups are independent (issued together).
 __device__ __forceinline__ void probe4(const LinkProbe& p, const int4& k, const int16_t* s_tab, bool (&alive)[4],
-                                       int64_t (&gid)[4]) {
+                                       int32_t (&gid)[4]) {
   int32_t c[4];
   if (p.kind == PROBE_HASH) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) c[i] = alive[i] ? hash_code(p, comp(k, i)) : -1;
   } else {
+    const uint32_t base = static_cast<uint32_t>(p.base), size = static_cast<uint32_t>(p.size);
     uint32_t s[4];
-    bool ok[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      s[i] = static_cast<uint32_t>(comp(k, i) - static_cast<int32_t>(p.base));
-      ok[i] = alive[i] && static_cast<int64_t>(comp(k, i)) - p.base >= 0 &&
-              static_cast<int64_t>(comp(k, i)) - p.base < p.size;
-    }
+    for (int i = 0; i < 4; ++i) s[i] = static_cast<uint32_t>(comp(k, i)) - base;  // keys >= base >= 0
     if (p.smem_off >= 0) {
+      const int16_t* t = s_tab + p.smem_off;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) c[i] = ok[i] ? static_cast<int32_t>(s_tab[p.smem_off + s[i]]) : -1;
+      for (int i = 0; i < 4; ++i) c[i] = (alive[i] && s[i] < size) ? static_cast<int32_t>(t[s[i]]) : -1;
     } else {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) c[i] = ok[i] ? __ldg(p.code + s[i]) : -1;
+      for (int i = 0; i < 4; ++i) c[i] = (alive[i] && s[i] < size) ? __ldg(p.code + s[i]) : -1;
     }
   }
 #pragma unroll
@@ -152,6 +155,10 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -178,8 +185,33 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
   return p;
 }
 
+// Block-wide reduction of the single-group (count, sum) pair into acc[0..1].
+__device__ __forceinline__ void flush_single(unsigned long long cnt, unsigned long long sum, unsigned long long* acc) {
+  for (int o = 16; o; o >>= 1) {
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  }
+  if ((threadIdx.x & 31) == 0 && cnt) {
+    atomicAdd(acc, cnt);
+    atomicAdd(acc + 1, sum);
+  }
+}
+
+// Shared 32-bit bins -> global accumulator (and reset).
+__device__ __forceinline__ void spill_bins32(uint32_t* b32, int64_t G, unsigned long long* acc, int t, int nt) {
+  for (int64_t g = t; g < G; g += nt) {
+    const uint32_t c = b32[g];
+    if (c) {
+      atomicAdd(acc + 2 * g, static_cast<unsigned long long>(c));
+      atomicAdd(acc + 2 * g + 1, static_cast<unsigned long long>(b32[G + g]));
+      b32[g] = 0;
+      b32[G + g] = 0;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
-// the pipelined scan
+// the warp-specialised, TMA-fed scan
 // ---------------------------------------------------------------------------
 
 template <int NL, int NF, int MODE>
@@ -191,46 +223,25 @@ __global__ void __launch_bounds__(kPipeThreads, 1) scan_pipe_kernel(const ScanAr
   const int stage_bytes = nc * kTile * 4;
   unsigned char* stage_base = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
-  int16_t* s_tab = reinterpret_cast<int16_t*>(full + kMaxStages);
+  uint64_t* empty = full + kMaxStages;
+  int16_t* s_tab = reinterpret_cast<int16_t*>(empty + kMaxStages);
   unsigned char* bins_base = reinterpret_cast<unsigned char*>(s_tab) + ((a.smem_tab_elems * 2 + 15) & ~15);
-  uint32_t* b32 = reinterpret_cast<uint32_t*>(bins_base);              // [G] counts, [G] sums
+  uint32_t* b32 = reinterpret_cast<uint32_t*>(bins_base);  // [G] counts, [G] sums
   unsigned long long* b64 = reinterpret_cast<unsigned long long*>(bins_base);
 
   const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
   const int64_t n_tiles = (a.n + kTile - 1) / kTile;
   const int64_t my_tiles = n_tiles > blockIdx.x ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
-  const int32_t* cols[NCmax];
-#pragma unroll
-  for (int j = 0; j < NL; ++j) cols[j] = a.fk[j];
-#pragma unroll
-  for (int f = 0; f < NF; ++f) cols[NL + f] = a.ff[f].col;
-  cols[NL + NF] = a.measure;
-
-  uint64_t policy = 0;
   if (tid == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(full + s, 1);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, kConsumerWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    policy = evict_first_policy();
   }
-  __syncthreads();
-
-  auto issue = [&](int64_t i) {  // thread 0: load my i-th tile into stage i % S
-    const int64_t tile = blockIdx.x + i * gridDim.x;
-    const int64_t row0 = tile * kTile;
-    const int64_t rows = min(static_cast<int64_t>(kTile), a.n - row0);
-    const uint32_t bytes = static_cast<uint32_t>((rows * 4 + 15) & ~15ll);
-    const int st = static_cast<int>(i % S);
-    uint64_t* bar = full + st;
-    mbar_arrive_expect_tx(bar, bytes * nc);
-#pragma unroll
-    for (int c = 0; c < NCmax; ++c)
-      if (c < nc) bulk_g2s(stage_base + st * stage_bytes + c * kTile * 4, cols[c] + row0, bytes, bar, policy);
-  };
-  if (tid == 0)
-    for (int64_t i = 0; i < S && i < my_tiles; ++i) issue(i);
-
-  // Stage code tables (int16) and zero the bins while the first tiles land.
+  // Stage code tables (int16) and zero the bins.
 #pragma unroll
   for (int j = 0; j < NL; ++j) {
     const LinkProbe& p = a.link[j];
@@ -243,117 +254,116 @@ __global__ void __launch_bounds__(kPipeThreads, 1) scan_pipe_kernel(const ScanAr
   }
   __syncthreads();
 
-  unsigned long long r_cnt = 0, r_sum = 0;
-  for (int64_t i = 0; i < my_tiles; ++i) {
-    const int st = static_cast<int>(i % S);
-    mbar_wait(full + st, static_cast<uint32_t>((i / S) & 1));
-    const int64_t row0 = (blockIdx.x + i * gridDim.x) * kTile + tid * 4;
-    const unsigned char* sb = stage_base + st * stage_bytes + tid * 16;
-
-    int4 kv[NL > 0 ? NL : 1], fv[NF > 0 ? NF : 1], mv;
+  if (warp == kConsumerWarps) {
+    // ===== producer warp: one elected lane streams the tiles =====
+    if (lane == 0) {
+      const int32_t* cols[NCmax];
 #pragma unroll
-    for (int j = 0; j < NL; ++j) kv[j] = *reinterpret_cast<const int4*>(sb + j * kTile * 4);
+      for (int j = 0; j < NL; ++j) cols[j] = a.fk[j];
 #pragma unroll
-    for (int f = 0; f < NF; ++f) fv[f] = *reinterpret_cast<const int4*>(sb + (NL + f) * kTile * 4);
-    if (a.measure) mv = *reinterpret_cast<const int4*>(sb + (NL + NF) * kTile * 4);
-
-    bool alive[4];
-    int64_t gid[4];
+      for (int f = 0; f < NF; ++f) cols[NL + f] = a.ff[f].col;
+      cols[NL + NF] = a.measure;
+      const uint64_t policy = evict_first_policy();
+      int st = 0;
+      uint32_t phase = 0;
+      for (int64_t i = 0; i < my_tiles; ++i) {
+        if (i >= S) mbar_wait(empty + st, phase ^ 1);  // consumers released this stage
+        const int64_t row0 = (blockIdx.x + i * gridDim.x) * kTile;
+        const int64_t rows = min(static_cast<int64_t>(kTile), a.n - row0);
+        const uint32_t bytes = static_cast<uint32_t>((rows * 4 + 15) & ~15ll);
+        mbar_arrive_expect_tx(full + st, bytes * nc);
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      alive[r] = row0 + r < a.n;
-      gid[r] = 0;
-    }
-#pragma unroll
-    for (int f = 0; f < NF; ++f)
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-        alive[r] = alive[r] && pred_eval(a.ff[f].kind, comp(fv[f], r), a.ff[f].lo, a.ff[f].hi, a.ff[f].set,
-                                         a.ff[f].set_len);
-#pragma unroll
-    for (int j = 0; j < NL; ++j) {
-      const bool any = alive[0] | alive[1] | alive[2] | alive[3];
-      if (any) probe4(a.link[j], kv[j], s_tab, alive, gid);
-    }
-    for (int g = 0; g < a.n_fgroups; ++g)
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-        if (alive[r]) gid[r] += (static_cast<int64_t>(__ldg(a.fg[g].col + row0 + r)) - a.fg[g].mn) * a.fg[g].stride;
-
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      if (!alive[r]) continue;
-      const long long v = a.measure ? static_cast<long long>(comp(mv, r)) : 0ll;
-      if constexpr (MODE == 0) {
-        r_cnt += 1;
-        r_sum += static_cast<unsigned long long>(v);
-      } else if constexpr (MODE == 1) {
-        if (a.narrow_bins) {
-          atomicAdd(b32 + gid[r], 1u);
-          if (a.measure) atomicAdd(b32 + a.n_groups + gid[r], static_cast<uint32_t>(v));
-        } else {
-          atomicAdd(b64 + gid[r], 1ull);
-          if (a.measure) atomicAdd(b64 + a.n_groups + gid[r], static_cast<unsigned long long>(v));
+        for (int c = 0; c < NCmax; ++c)
+          if (c < nc) bulk_g2s(stage_base + st * stage_bytes + c * kTile * 4, cols[c] + row0, bytes, full + st, policy);
+        if (++st == S) {
+          st = 0;
+          phase ^= 1;
         }
-      } else {
-        atomicAdd(a.acc + 2 * gid[r], 1ull);
-        if (a.measure) atomicAdd(a.acc + 2 * gid[r] + 1, static_cast<unsigned long long>(v));
       }
     }
-    __syncthreads();  // every thread is done with stage st
-    if (tid == 0 && i + S < my_tiles) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(i + S);
-    }
-    if constexpr (MODE == 1) {
-      if (a.narrow_bins && (i + 1) % a.flush_every == 0 && i + 1 < my_tiles) {
-        // Spill the 32-bit partials before they can wrap.
-        for (int64_t g = tid; g < a.n_groups; g += kPipeThreads) {
-          const uint32_t c = b32[g];
-          if (c) {
-            atomicAdd(a.acc + 2 * g, static_cast<unsigned long long>(c));
-            atomicAdd(a.acc + 2 * g + 1, static_cast<unsigned long long>(b32[a.n_groups + g]));
-            b32[g] = 0;
-            b32[a.n_groups + g] = 0;
+  } else {
+    // ===== consumer warps: 4 consecutive rows per thread per tile =====
+    unsigned long long r_cnt = 0, r_sum = 0;
+    int st = 0;
+    uint32_t phase = 0;
+    int64_t since_flush = 0;
+    for (int64_t i = 0; i < my_tiles; ++i) {
+      mbar_wait(full + st, phase);
+      const int64_t row0 = (blockIdx.x + i * gridDim.x) * kTile + tid * 4;
+      const unsigned char* sb = stage_base + st * stage_bytes + tid * 16;
+      int4 kv[NL > 0 ? NL : 1], fv[NF > 0 ? NF : 1], mv;
+#pragma unroll
+      for (int j = 0; j < NL; ++j) kv[j] = *reinterpret_cast<const int4*>(sb + j * kTile * 4);
+#pragma unroll
+      for (int f = 0; f < NF; ++f) fv[f] = *reinterpret_cast<const int4*>(sb + (NL + f) * kTile * 4);
+      if (a.measure) mv = *reinterpret_cast<const int4*>(sb + (NL + NF) * kTile * 4);
+
+      bool alive[4];
+      int32_t gid[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        alive[r] = row0 + r < a.n;
+        gid[r] = 0;
+      }
+#pragma unroll
+      for (int f = 0; f < NF; ++f)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) alive[r] = alive[r] && filter_ok(a.ff[f], comp(fv[f], r));
+#pragma unroll
+      for (int j = 0; j < NL; ++j)
+        if (alive[0] | alive[1] | alive[2] | alive[3]) probe4(a.link[j], kv[j], s_tab, alive, gid);
+      for (int g = 0; g < a.n_fgroups; ++g)
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (alive[r])
+            gid[r] += static_cast<int32_t>((static_cast<int64_t>(__ldg(a.fg[g].col + row0 + r)) - a.fg[g].mn) *
+                                           a.fg[g].stride);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        if (!alive[r]) continue;
+        const int32_t v = a.measure ? comp(mv, r) : 0;
+        if constexpr (MODE == 0) {
+          r_cnt += 1;
+          r_sum += static_cast<unsigned long long>(static_cast<long long>(v));
+        } else if constexpr (MODE == 1) {
+          if (a.narrow_bins) {
+            atomicAdd(b32 + gid[r], 1u);
+            if (a.measure) atomicAdd(b32 + a.n_groups + gid[r], static_cast<uint32_t>(v));
+          } else {
+            atomicAdd(b64 + gid[r], 1ull);
+            if (a.measure) atomicAdd(b64 + a.n_groups + gid[r], static_cast<unsigned long long>(static_cast<long long>(v)));
           }
+        } else {
+          atomicAdd(a.acc + 2 * gid[r], 1ull);
+          if (a.measure) atomicAdd(a.acc + 2 * gid[r] + 1, static_cast<unsigned long long>(static_cast<long long>(v)));
         }
-        __syncthreads();
+      }
+      // Release the stage only after its data has been consumed (WAR vs the next bulk copy).
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + st);
+      if (++st == S) {
+        st = 0;
+        phase ^= 1;
+      }
+      if constexpr (MODE == 1) {
+        if (a.narrow_bins && ++since_flush == a.flush_every && i + 1 < my_tiles) {
+          // All consumer warps flush together (named barrier 1, producer excluded).
+          since_flush = 0;
+          asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps));
+          spill_bins32(b32, a.n_groups, a.acc, tid, 32 * kConsumerWarps);
+          asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps));
+        }
       }
     }
+    if constexpr (MODE == 0) flush_single(r_cnt, r_sum, a.acc);
   }
 
-  if constexpr (MODE == 0) {
-    for (int o = 16; o; o >>= 1) {
-      r_cnt += __shfl_xor_sync(0xffffffffu, r_cnt, o);
-      r_sum += __shfl_xor_sync(0xffffffffu, r_sum, o);
-    }
-    __shared__ unsigned long long w_cnt[kPipeThreads / 32], w_sum[kPipeThreads / 32];
-    if ((tid & 31) == 0) {
-      w_cnt[tid >> 5] = r_cnt;
-      w_sum[tid >> 5] = r_sum;
-    }
+  if constexpr (MODE == 1) {
     __syncthreads();
-    if (tid == 0) {
-      unsigned long long c = 0, s = 0;
-      for (int w = 0; w < kPipeThreads / 32; ++w) {
-        c += w_cnt[w];
-        s += w_sum[w];
-      }
-      if (c) {
-        atomicAdd(a.acc, c);
-        atomicAdd(a.acc + 1, s);
-      }
-    }
-  } else if constexpr (MODE == 1) {
-    __syncthreads();
-    for (int64_t g = tid; g < a.n_groups; g += kPipeThreads) {
-      if (a.narrow_bins) {
-        const uint32_t c = b32[g];
-        if (c) {
-          atomicAdd(a.acc + 2 * g, static_cast<unsigned long long>(c));
-          atomicAdd(a.acc + 2 * g + 1, static_cast<unsigned long long>(b32[a.n_groups + g]));
-        }
-      } else {
+    if (a.narrow_bins) {
+      spill_bins32(b32, a.n_groups, a.acc, tid, kPipeThreads);
+    } else {
+      for (int64_t g = tid; g < a.n_groups; g += kPipeThreads) {
         const unsigned long long c = b64[g];
         if (c) {
           atomicAdd(a.acc + 2 * g, c);
@@ -394,7 +404,7 @@ __global__ void __launch_bounds__(256) scan_ldg_kernel(const ScanArgs a, const b
 #pragma unroll
     for (int f = 0; f < NF; ++f) fv[f] = ld4(a.ff[f].col, row0, a.n, vec);
     if (a.measure) mv = ld4(a.measure, row0, a.n, vec);
-    int64_t gid[4];
+    int32_t gid[4];
     bool alive[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -404,9 +414,7 @@ __global__ void __launch_bounds__(256) scan_ldg_kernel(const ScanArgs a, const b
 #pragma unroll
     for (int f = 0; f < NF; ++f)
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        alive[i] = alive[i] && pred_eval(a.ff[f].kind, comp(fv[f], i), a.ff[f].lo, a.ff[f].hi, a.ff[f].set,
-                                         a.ff[f].set_len);
+      for (int i = 0; i < 4; ++i) alive[i] = alive[i] && filter_ok(a.ff[f], comp(fv[f], i));
 #pragma unroll
     for (int j = 0; j < NL; ++j) {
       LinkProbe p = a.link[j];
@@ -416,7 +424,8 @@ __global__ void __launch_bounds__(256) scan_ldg_kernel(const ScanArgs a, const b
     for (int g = 0; g < a.n_fgroups; ++g) {
       const int4 v = ld4(a.fg[g].col, row0, a.n, vec);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) gid[i] += (static_cast<int64_t>(comp(v, i)) - a.fg[g].mn) * a.fg[g].stride;
+      for (int i = 0; i < 4; ++i)
+        gid[i] += static_cast<int32_t>((static_cast<int64_t>(comp(v, i)) - a.fg[g].mn) * a.fg[g].stride);
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -435,27 +444,7 @@ __global__ void __launch_bounds__(256) scan_ldg_kernel(const ScanArgs a, const b
     }
   }
   if constexpr (MODE == 0) {
-    for (int o = 16; o; o >>= 1) {
-      r_cnt += __shfl_xor_sync(0xffffffffu, r_cnt, o);
-      r_sum += __shfl_xor_sync(0xffffffffu, r_sum, o);
-    }
-    __shared__ unsigned long long w_cnt[8], w_sum[8];
-    if ((threadIdx.x & 31) == 0) {
-      w_cnt[threadIdx.x >> 5] = r_cnt;
-      w_sum[threadIdx.x >> 5] = r_sum;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned long long c = 0, s = 0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-        c += w_cnt[w];
-        s += w_sum[w];
-      }
-      if (c) {
-        atomicAdd(a.acc, c);
-        atomicAdd(a.acc + 1, s);
-      }
-    }
+    flush_single(r_cnt, r_sum, a.acc);
   } else if constexpr (MODE == 1) {
     __syncthreads();
     for (int64_t g = threadIdx.x; g < a.n_groups; g += blockDim.x) {
