@@ -134,7 +134,9 @@ struct StarArgs {
   int* err;      // bit 0: negative key among live rows
 };
 
-constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
+#define kFlagAgg (1ull << 62)
+#define kFlagInc (2ull << 62)
+#define kValMask ((1ull << 62) - 1)
 
 template <class K>
 __device__ __forceinline__ void load_keys(const K* __restrict__ p, int64_t row0, int64_t n, int64_t (&k)[kItems]) {
@@ -157,90 +159,125 @@ __device__ __forceinline__ void load_keys(const K* __restrict__ p, int64_t row0,
   }
 }
 
+// Decoupled look-back with a whole warp: 32 predecessors inspected per step
+// (the first tile with an inclusive prefix ends the walk).  Returns this
+// tile's exclusive prefix on every lane; publishes the inclusive prefix.
+__device__ __forceinline__ unsigned long long lookback_warp(unsigned long long* state, int64_t tile,
+                                                            unsigned long long total) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) atomicExch(state, kFlagInc | total);
+    return 0;
+  }
+  if (lane == 0) atomicExch(state + tile, kFlagAgg | total);
+  unsigned long long prefix = 0;
+  int64_t p = tile - 1;
+  while (true) {
+    const int64_t idx = p - lane;
+    unsigned long long s;
+    do {
+      s = idx >= 0 ? *reinterpret_cast<volatile unsigned long long*>(state + idx) : kFlagInc;
+    } while (!__all_sync(0xffffffffu, (s & ~kValMask) != 0));
+    const unsigned inc = __ballot_sync(0xffffffffu, (s & ~kValMask) == kFlagInc);
+    const int stop = inc ? __ffs(inc) - 1 : 31;  // lanes 0..stop contribute
+    unsigned long long v = lane <= stop ? (s & kValMask) : 0;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    prefix += v;
+    if (inc) break;
+    p -= 32;
+  }
+  if (lane == 0) atomicExch(state + tile, kFlagInc | (prefix + total));
+  return prefix;
+}
+
+// Persistent: CTAs pull tiles from an atomic counter (so every predecessor of
+// a claimed tile is already running), probe, rank survivors, look back, and
+// write.  The l == 1 prediction is staged in shared memory so the compacted
+// output leaves in coalesced 8-byte runs.
 template <class K, int NL, bool kPredict>
 __global__ void __launch_bounds__(kBlock) star_kernel(const StarArgs<K> a) {
   using Scan = cub::BlockScan<int, kBlock>;
   __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ int64_t s_tile;
   __shared__ unsigned long long s_prefix;
-
-  if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1);
-  __syncthreads();
-  const int64_t tile = s_tile;
-  const int64_t row0 = tile * kTile + static_cast<int64_t>(threadIdx.x) * kItems;
-
-  int32_t rows[NL][kItems];
-  bool alive[kItems];
-#pragma unroll
-  for (int i = 0; i < kItems; ++i) alive[i] = row0 + i < a.n;
+  __shared__ double s_y[kPredict ? kTile : 1];
+  const bool stage_y = kPredict && a.l == 1;
 
   int neg = 0;
-#pragma unroll
-  for (int j = 0; j < NL; ++j) {
-    int64_t keys[kItems];
-    load_keys<K>(a.fk[j], row0, a.n, keys);
-    const ProbeView pv = a.probe[j];
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-      int32_t r = -1;
-      if (alive[i]) {
-        if (keys[i] < 0) neg = 1;
-        r = pv.row(keys[i]);
-        alive[i] = r >= 0;
-      }
-      rows[j][i] = r;
-    }
-  }
-  if (neg) atomicOr(a.err, 1);
+  while (true) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    if (tile >= a.n_tiles) break;
+    const int64_t row0 = tile * kTile + static_cast<int64_t>(threadIdx.x) * kItems;
 
-  int count = 0;
+    int32_t rows[NL][kItems];
+    bool alive[kItems];
 #pragma unroll
-  for (int i = 0; i < kItems; ++i) count += alive[i] ? 1 : 0;
-  int excl, total;
-  Scan(scan_tmp).ExclusiveSum(count, excl, total);
-
-  if (threadIdx.x == 0) {
-    unsigned long long prefix = 0;
-    if (tile == 0) {
-      atomicExch(a.tile_state, kFlagInc | static_cast<unsigned long long>(total));
-    } else {
-      atomicExch(a.tile_state + tile, kFlagAgg | static_cast<unsigned long long>(total));
-      int64_t p = tile - 1;
-      while (true) {
-        const unsigned long long s = *reinterpret_cast<volatile unsigned long long*>(a.tile_state + p);
-        const unsigned long long f = s & ~kValMask;
-        if (f == 0) continue;  // predecessor not published yet
-        prefix += s & kValMask;
-        if (f == kFlagInc) break;
-        --p;
-      }
-      atomicExch(a.tile_state + tile, kFlagInc | (prefix + static_cast<unsigned long long>(total)));
-    }
-    if (tile == a.n_tiles - 1) *a.nnz = static_cast<int64_t>(prefix) + total;
-    s_prefix = prefix;
-  }
-  __syncthreads();
-  int64_t pos = static_cast<int64_t>(s_prefix) + excl;
-
-#pragma unroll
-  for (int i = 0; i < kItems; ++i) {
-    if (!alive[i]) continue;
-    if (a.survivors) a.survivors[pos] = row0 + i;
+    for (int i = 0; i < kItems; ++i) alive[i] = row0 + i < a.n;
 #pragma unroll
     for (int j = 0; j < NL; ++j) {
-      if (a.rows64[j]) a.rows64[j][pos] = rows[j][i];
-      if (a.rows32[j]) a.rows32[j][pos] = rows[j][i];
-    }
-    if constexpr (kPredict) {
-      for (int64_t c = 0; c < a.l; ++c) {
-        double acc = __dadd_rn(0.0, __ldg(a.partial[0] + static_cast<int64_t>(rows[0][i]) * a.l + c));  // 0 + 1*x (spmm_dense)
+      int64_t keys[kItems];
+      load_keys<K>(a.fk[j], row0, a.n, keys);
+      const ProbeView pv = a.probe[j];
 #pragma unroll
-        for (int j = 1; j < NL; ++j) acc = __dadd_rn(acc, __ldg(a.partial[j] + static_cast<int64_t>(rows[j][i]) * a.l + c));
-        __stcs(a.y + pos * a.l + c, acc);
+      for (int i = 0; i < kItems; ++i) {
+        int32_t r = -1;
+        if (alive[i]) {
+          neg |= keys[i] < 0 ? 1 : 0;
+          r = pv.row(keys[i]);
+          alive[i] = r >= 0;
+        }
+        rows[j][i] = r;
       }
     }
-    ++pos;
+
+    int count = 0;
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) count += alive[i] ? 1 : 0;
+    int excl, total;
+    Scan(scan_tmp).ExclusiveSum(count, excl, total);
+    if (threadIdx.x < 32) {
+      const unsigned long long prefix = lookback_warp(a.tile_state, tile, static_cast<unsigned long long>(total));
+      if (threadIdx.x == 0) {
+        s_prefix = prefix;
+        if (tile == a.n_tiles - 1) *a.nnz = static_cast<int64_t>(prefix) + total;
+      }
+    }
+    __syncthreads();
+    const int64_t prefix = static_cast<int64_t>(s_prefix);
+    int64_t pos = prefix + excl;
+    int local = excl;
+
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      if (!alive[i]) continue;
+      if (a.survivors) a.survivors[pos] = row0 + i;
+#pragma unroll
+      for (int j = 0; j < NL; ++j) {
+        if (a.rows64[j]) a.rows64[j][pos] = rows[j][i];
+        if (a.rows32[j]) a.rows32[j][pos] = rows[j][i];
+      }
+      if constexpr (kPredict) {
+        for (int64_t c = 0; c < a.l; ++c) {
+          double acc = __dadd_rn(0.0, __ldg(a.partial[0] + static_cast<int64_t>(rows[0][i]) * a.l + c));  // 0 + 1*x (spmm_dense)
+#pragma unroll
+          for (int j = 1; j < NL; ++j)
+            acc = __dadd_rn(acc, __ldg(a.partial[j] + static_cast<int64_t>(rows[j][i]) * a.l + c));
+          if (stage_y) s_y[local] = acc;
+          else __stcs(a.y + pos * a.l + c, acc);
+        }
+      }
+      ++pos;
+      ++local;
+    }
+    if (stage_y) {
+      __syncthreads();
+      for (int t = threadIdx.x; t < total; t += kBlock) __stcs(a.y + prefix + t, s_y[t]);
+    }
+    __syncthreads();  // s_tile / s_y / scan storage are reused by the next tile
   }
+  if (neg) atomicOr(a.err, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -339,7 +376,8 @@ void run_star(laq_ctx* ctx, StarArgs<K>& a, StarScratch& scratch, bool predict) 
   a.tile_counter = scratch.counter.get();
   LAQ_CUDA(cudaMemsetAsync(a.tile_state, 0, a.n_tiles * sizeof(unsigned long long), ctx->stream));
   LAQ_CUDA(cudaMemsetAsync(a.tile_counter, 0, sizeof(int), ctx->stream));
-  const unsigned g = static_cast<unsigned>(a.n_tiles);
+  // Persistent grid: a few resident CTAs per SM pull tiles dynamically.
+  const unsigned g = static_cast<unsigned>(std::min<int64_t>(a.n_tiles, int64_t{ctx->sm_count} * 6));
   cudaStream_t s = ctx->stream;
 #define LAQ_STAR_CASE(N)                                                   \
   case N:                                                                  \

@@ -349,7 +349,9 @@ void lay_out_scan(laq_ctx* ctx, laq_plan* p, const std::vector<const int32_t*>& 
   const int64_t rest = budget - bin_bytes - tab_elems * 2;
   int64_t stages = std::min<int64_t>(scan::kMaxStages, rest / std::max<int64_t>(stage_bytes, 1));
   if (const char* v = std::getenv("LAQ_STAGES")) stages = std::min<int64_t>(stages, std::atoi(v));  // diagnostics
-  p->pipe = p->vec && all_padded && stages >= 2 && nc >= 1 && (p->mode != 1 || p->G <= kSmemBinsPipe);
+  bool fact_inset = false;
+  for (int f = 0; f < p->nf; ++f) fact_inset = fact_inset || a.ff[f].inset;
+  p->pipe = p->vec && all_padded && !fact_inset && stages >= 2 && nc >= 1 && (p->mode != 1 || p->G <= kSmemBinsPipe);
   if (const char* v = std::getenv("LAQ_SCAN")) p->pipe = p->pipe && std::string(v) != "ldg";  // A/B switch
   if (p->pipe) {
     a.stages = static_cast<int>(stages);

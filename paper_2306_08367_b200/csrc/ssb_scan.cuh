@@ -298,17 +298,25 @@ __global__ void __launch_bounds__(kPipeThreads, 1) scan_pipe_kernel(const ScanAr
       for (int f = 0; f < NF; ++f) fv[f] = *reinterpret_cast<const int4*>(sb + (NL + f) * kTile * 4);
       if (a.measure) mv = *reinterpret_cast<const int4*>(sb + (NL + NF) * kTile * 4);
 
+      const int64_t left = a.n - row0;  // rows of this thread's 4 that exist
+      const int valid = left >= 4 ? 4 : (left > 0 ? static_cast<int>(left) : 0);
       bool alive[4];
       int32_t gid[4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        alive[r] = row0 + r < a.n;
+        alive[r] = r < valid;
         gid[r] = 0;
       }
+      // Fact filters are closed int32 intervals here (InSet plans use the fallback kernel).
 #pragma unroll
-      for (int f = 0; f < NF; ++f)
+      for (int f = 0; f < NF; ++f) {
+        const int32_t lo = a.ff[f].lo, hi = a.ff[f].hi;
 #pragma unroll
-        for (int r = 0; r < 4; ++r) alive[r] = alive[r] && filter_ok(a.ff[f], comp(fv[f], r));
+        for (int r = 0; r < 4; ++r) {
+          const int32_t v = comp(fv[f], r);
+          alive[r] = alive[r] & (v >= lo) & (v <= hi);
+        }
+      }
 #pragma unroll
       for (int j = 0; j < NL; ++j)
         if (alive[0] | alive[1] | alive[2] | alive[3]) probe4(a.link[j], kv[j], s_tab, alive, gid);
@@ -318,24 +326,35 @@ __global__ void __launch_bounds__(kPipeThreads, 1) scan_pipe_kernel(const ScanAr
           if (alive[r])
             gid[r] += static_cast<int32_t>((static_cast<int64_t>(__ldg(a.fg[g].col + row0 + r)) - a.fg[g].mn) *
                                            a.fg[g].stride);
+      if constexpr (MODE == 0) {
+        // Branch-free: 4-row partials in 32 bits, one 64-bit add per tile.
+        int32_t c4 = 0;
+        long long s4 = 0;
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        if (!alive[r]) continue;
-        const int32_t v = a.measure ? comp(mv, r) : 0;
-        if constexpr (MODE == 0) {
-          r_cnt += 1;
-          r_sum += static_cast<unsigned long long>(static_cast<long long>(v));
-        } else if constexpr (MODE == 1) {
-          if (a.narrow_bins) {
-            atomicAdd(b32 + gid[r], 1u);
-            if (a.measure) atomicAdd(b32 + a.n_groups + gid[r], static_cast<uint32_t>(v));
+        for (int r = 0; r < 4; ++r) {
+          c4 += alive[r] ? 1 : 0;
+          s4 += alive[r] ? (a.measure ? comp(mv, r) : 0) : 0;
+        }
+        r_cnt += static_cast<unsigned long long>(c4);
+        r_sum += static_cast<unsigned long long>(static_cast<long long>(s4));
+      } else {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if (!alive[r]) continue;
+          const int32_t v = a.measure ? comp(mv, r) : 0;
+          if constexpr (MODE == 1) {
+            if (a.narrow_bins) {
+              atomicAdd(b32 + gid[r], 1u);
+              if (a.measure) atomicAdd(b32 + a.n_groups + gid[r], static_cast<uint32_t>(v));
+            } else {
+              atomicAdd(b64 + gid[r], 1ull);
+              if (a.measure)
+                atomicAdd(b64 + a.n_groups + gid[r], static_cast<unsigned long long>(static_cast<long long>(v)));
+            }
           } else {
-            atomicAdd(b64 + gid[r], 1ull);
-            if (a.measure) atomicAdd(b64 + a.n_groups + gid[r], static_cast<unsigned long long>(static_cast<long long>(v)));
+            atomicAdd(a.acc + 2 * gid[r], 1ull);
+            if (a.measure) atomicAdd(a.acc + 2 * gid[r] + 1, static_cast<unsigned long long>(static_cast<long long>(v)));
           }
-        } else {
-          atomicAdd(a.acc + 2 * gid[r], 1ull);
-          if (a.measure) atomicAdd(a.acc + 2 * gid[r] + 1, static_cast<unsigned long long>(static_cast<long long>(v)));
         }
       }
       // Release the stage only after its data has been consumed (WAR vs the next bulk copy).
