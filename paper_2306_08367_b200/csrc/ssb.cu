@@ -145,16 +145,16 @@ __global__ void count_pass_kernel(const int32_t* __restrict__ code, int64_t slot
 
 // ---- kernel dispatch (instantiated per link count in ssb_scan_nl*.cu) -----
 
-void launch_scan(laq_ctx* ctx, const ScanArgs& a, int nl, int nf, int mode, bool pipe, bool vec, int grid,
+void launch_scan(laq_ctx* ctx, const ScanArgs& a, int nl, int nf, int mode, int variant, bool vec, int grid,
                  size_t smem) {
   switch (nl) {
-    case 0: scan::launch_nl<0>(ctx, a, nf, mode, pipe, vec, grid, smem); break;
-    case 1: scan::launch_nl<1>(ctx, a, nf, mode, pipe, vec, grid, smem); break;
-    case 2: scan::launch_nl<2>(ctx, a, nf, mode, pipe, vec, grid, smem); break;
-    case 3: scan::launch_nl<3>(ctx, a, nf, mode, pipe, vec, grid, smem); break;
-    case 4: scan::launch_nl<4>(ctx, a, nf, mode, pipe, vec, grid, smem); break;
-    case 5: scan::launch_nl<5>(ctx, a, nf, mode, pipe, vec, grid, smem); break;
-    case 6: scan::launch_nl<6>(ctx, a, nf, mode, pipe, vec, grid, smem); break;
+    case 0: scan::launch_nl<0>(ctx, a, nf, mode, variant, vec, grid, smem); break;
+    case 1: scan::launch_nl<1>(ctx, a, nf, mode, variant, vec, grid, smem); break;
+    case 2: scan::launch_nl<2>(ctx, a, nf, mode, variant, vec, grid, smem); break;
+    case 3: scan::launch_nl<3>(ctx, a, nf, mode, variant, vec, grid, smem); break;
+    case 4: scan::launch_nl<4>(ctx, a, nf, mode, variant, vec, grid, smem); break;
+    case 5: scan::launch_nl<5>(ctx, a, nf, mode, variant, vec, grid, smem); break;
+    case 6: scan::launch_nl<6>(ctx, a, nf, mode, variant, vec, grid, smem); break;
     default: fail(LAQ_ERR_UNSUPPORTED, "at most 6 joins per query");
   }
   launched(ctx);
@@ -262,6 +262,7 @@ struct laq_plan {
   int nl = 0, nf = 0;
   bool vec = true;
   bool pipe = false;
+  int variant = 0;  // 0 ldg fallback, 1 TMA pipe, 2 resident-table stream
   int mode = 0;
   int grid = 1;
   size_t smem = 0;
@@ -351,25 +352,37 @@ void lay_out_scan(laq_ctx* ctx, laq_plan* p, const std::vector<const int32_t*>& 
   if (const char* v = std::getenv("LAQ_STAGES")) stages = std::min<int64_t>(stages, std::atoi(v));  // diagnostics
   bool fact_inset = false;
   for (int f = 0; f < p->nf; ++f) fact_inset = fact_inset || a.ff[f].inset;
-  p->pipe = p->vec && all_padded && !fact_inset && stages >= 2 && nc >= 1 && (p->mode != 1 || p->G <= kSmemBinsPipe);
-  if (const char* v = std::getenv("LAQ_SCAN")) p->pipe = p->pipe && std::string(v) != "ldg";  // A/B switch
-  if (p->pipe) {
+  // Variant: the resident-table stream kernel by default (fastest measured on
+  // B200 for every SSB shape, profiles/), the TMA pipeline on request, the
+  // plain-load kernel for unaligned / InSet / very wide group-id plans.
+  const bool fast_ok = p->vec && all_padded && !fact_inset && nc >= 1 && (p->mode != 1 || p->G <= kSmemBinsPipe);
+  const char* want = std::getenv("LAQ_SCAN");
+  const std::string pick = want ? std::string(want) : std::string("stream");
+  a.smem_tab_elems = static_cast<int>(tab_elems);
+  a.narrow_bins = narrow ? 1 : 0;
+  const size_t tab_bytes = static_cast<size_t>((tab_elems * 2 + 15) & ~15);
+  if (fast_ok && pick == "pipe" && stages >= 2) {
+    p->variant = 1;
     a.stages = static_cast<int>(stages);
-    a.smem_tab_elems = static_cast<int>(tab_elems);
-    a.narrow_bins = narrow ? 1 : 0;
     // u32 sums: between spills a CTA adds at most flush_every * kTile values <= vmax.
     a.flush_every = std::max<int64_t>(1, (int64_t{1} << 32) / (int64_t{scan::kTile} * vmax) - 1);
-    p->smem = static_cast<size_t>(stages * stage_bytes + 16 * scan::kMaxStages + ((tab_elems * 2 + 15) & ~15) +
-                                  bin_bytes);
+    p->smem = static_cast<size_t>(stages * stage_bytes + 16 * scan::kMaxStages) + tab_bytes + static_cast<size_t>(bin_bytes);
     const int64_t tiles = (p->fact_rows + scan::kTile - 1) / scan::kTile;
     p->grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctx->sm_count, tiles)));
+  } else if (fast_ok && pick != "ldg" && static_cast<int64_t>(tab_bytes) + bin_bytes <= budget) {
+    p->variant = 2;
+    a.flush_every = std::max<int64_t>(1, (int64_t{1} << 32) / (int64_t{scan::kStreamThreads} * 4 * vmax) - 1);
+    p->smem = tab_bytes + static_cast<size_t>(bin_bytes);
+    p->grid = ctx->sm_count;  // x resident CTAs per SM (occupancy, at launch)
   } else {
+    p->variant = 0;
     for (int q = 0; q < nl; ++q) a.link[q].smem_off = -1;
     p->smem = p->mode == 1 ? static_cast<size_t>(2 * p->G) * sizeof(unsigned long long) : 0;
     const int per_sm = p->mode == 1 && p->G > 1024 ? 2 : 6;
     p->grid = static_cast<int>(
         std::max<int64_t>(1, std::min<int64_t>(ctx->sm_count * per_sm, (p->fact_rows + 1023) / 1024)));
   }
+  p->pipe = p->variant == 1;
 }
 
 }  // namespace
@@ -625,7 +638,7 @@ int laq_query_prepare(laq_ctx* ctx, const laq_star* cs, const laq_query_desc* q,
     plan->mode = G == 1 ? 0 : (G <= kSmemBinsPipe ? 1 : (G <= kSmemBinsLdg ? 1 : 2));
     plan->bytes_per_row = 4 * (plan->nl + plan->nf + a.n_fgroups + (a.measure ? 1 : 0));
     lay_out_scan(ctx, plan.get(), fks, probes, mmin, mmax, padded);
-    if (!plan->pipe && plan->mode == 1 && G > kSmemBinsLdg) plan->mode = 2;
+    if (plan->variant == 0 && plan->mode == 1 && G > kSmemBinsLdg) plan->mode = 2;
     *h_n_groups = G;
     *out = plan.release();
   });
@@ -641,7 +654,7 @@ int laq_plan_scan(laq_ctx* ctx, laq_plan* p, int64_t* d_acc, int32_t accumulate)
     if (p->fact_rows == 0) return;
     ScanArgs a = p->scan;
     a.acc = reinterpret_cast<unsigned long long*>(d_acc);
-    launch_scan(ctx, a, p->nl, p->nf, p->mode, p->pipe, p->vec, p->grid, p->smem);
+    launch_scan(ctx, a, p->nl, p->nf, p->mode, p->variant, p->vec, p->grid, p->smem);
   });
 }
 

@@ -9,10 +9,10 @@ namespace laq {
 namespace scan {
 
 template <int NL>
-void launch_nl(laq_ctx* ctx, const ScanArgs& a, int nf, int mode, bool pipe, bool vec, int grid, size_t smem);
+void launch_nl(laq_ctx* ctx, const ScanArgs& a, int nf, int mode, int variant, bool vec, int grid, size_t smem);
 
 #define LAQ_SCAN_EXTERN(N)                                                                                   \
-  extern template void launch_nl<N>(laq_ctx*, const ScanArgs&, int, int, bool, bool, int, size_t);
+  extern template void launch_nl<N>(laq_ctx*, const ScanArgs&, int, int, int, bool, int, size_t);
 LAQ_SCAN_EXTERN(0)
 LAQ_SCAN_EXTERN(1)
 LAQ_SCAN_EXTERN(2)

@@ -476,5 +476,149 @@ __global__ void __launch_bounds__(256) scan_ldg_kernel(const ScanArgs a, const b
   }
 }
 
+// ---------------------------------------------------------------------------
+// stream: resident-table streaming scan (vectorised loads, register double
+// buffering), shared-memory code tables + 32-bit bins like the pipe kernel,
+// but with many more warps per SM to hide the L2 gathers of big dimensions.
+// ---------------------------------------------------------------------------
+
+constexpr int kStreamThreads = 256;
+
+__device__ __forceinline__ int4 ld4_padded(const int32_t* p, int64_t row0, int64_t n) {
+  // Columns on this path are 16-byte aligned with >= 16 readable bytes past the end.
+  return row0 < n ? __ldcs(reinterpret_cast<const int4*>(p + row0)) : make_int4(0, 0, 0, 0);
+}
+
+template <int NL, int NF, int MODE>
+__global__ void __launch_bounds__(kStreamThreads) scan_stream_kernel(const ScanArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  int16_t* s_tab = reinterpret_cast<int16_t*>(smem);
+  uint32_t* b32 = reinterpret_cast<uint32_t*>(smem + ((a.smem_tab_elems * 2 + 15) & ~15));
+  unsigned long long* b64 = reinterpret_cast<unsigned long long*>(b32);
+  const int tid = threadIdx.x;
+
+#pragma unroll
+  for (int j = 0; j < NL; ++j) {
+    const LinkProbe& p = a.link[j];
+    if (p.smem_off >= 0)
+      for (int64_t s = tid; s < p.size; s += kStreamThreads) s_tab[p.smem_off + s] = static_cast<int16_t>(__ldg(p.code + s));
+  }
+  if constexpr (MODE == 1) {
+    const int64_t words = a.narrow_bins ? 2 * a.n_groups : 4 * a.n_groups;
+    for (int64_t g = tid; g < words; g += kStreamThreads) b32[g] = 0;
+  }
+  __syncthreads();
+
+  const int64_t step = static_cast<int64_t>(gridDim.x) * kStreamThreads * 4;
+  const int64_t iters = (a.n + step - 1) / step;  // uniform across the block (barriers below)
+  int64_t row0 = (static_cast<int64_t>(blockIdx.x) * kStreamThreads + tid) * 4;
+
+  int4 kv[NL > 0 ? NL : 1], fv[NF > 0 ? NF : 1], mv = make_int4(0, 0, 0, 0);
+#pragma unroll
+  for (int j = 0; j < NL; ++j) kv[j] = ld4_padded(a.fk[j], row0, a.n);
+#pragma unroll
+  for (int f = 0; f < NF; ++f) fv[f] = ld4_padded(a.ff[f].col, row0, a.n);
+  if (a.measure) mv = ld4_padded(a.measure, row0, a.n);
+
+  unsigned long long r_cnt = 0, r_sum = 0;
+  for (int64_t it = 0; it < iters; ++it) {
+    // Prefetch the next rows while this batch is probed (register double buffer).
+    const int64_t nrow0 = row0 + step;
+    int4 nkv[NL > 0 ? NL : 1], nfv[NF > 0 ? NF : 1], nmv = make_int4(0, 0, 0, 0);
+#pragma unroll
+    for (int j = 0; j < NL; ++j) nkv[j] = ld4_padded(a.fk[j], nrow0, a.n);
+#pragma unroll
+    for (int f = 0; f < NF; ++f) nfv[f] = ld4_padded(a.ff[f].col, nrow0, a.n);
+    if (a.measure) nmv = ld4_padded(a.measure, nrow0, a.n);
+
+    const int64_t left = a.n - row0;
+    const int valid = left >= 4 ? 4 : (left > 0 ? static_cast<int>(left) : 0);
+    bool alive[4];
+    int32_t gid[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      alive[r] = r < valid;
+      gid[r] = 0;
+    }
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      const int32_t lo = a.ff[f].lo, hi = a.ff[f].hi;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int32_t v = comp(fv[f], r);
+        alive[r] = alive[r] & (v >= lo) & (v <= hi);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+      if (alive[0] | alive[1] | alive[2] | alive[3]) probe4(a.link[j], kv[j], s_tab, alive, gid);
+    for (int g = 0; g < a.n_fgroups; ++g)
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (alive[r])
+          gid[r] += static_cast<int32_t>((static_cast<int64_t>(__ldg(a.fg[g].col + row0 + r)) - a.fg[g].mn) *
+                                         a.fg[g].stride);
+    if constexpr (MODE == 0) {
+      int32_t c4 = 0;
+      long long s4 = 0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        c4 += alive[r] ? 1 : 0;
+        s4 += alive[r] ? comp(mv, r) : 0;
+      }
+      r_cnt += static_cast<unsigned long long>(c4);
+      r_sum += static_cast<unsigned long long>(s4);
+    } else {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        if (!alive[r]) continue;
+        const int32_t v = comp(mv, r);
+        if constexpr (MODE == 1) {
+          if (a.narrow_bins) {
+            atomicAdd(b32 + gid[r], 1u);
+            if (a.measure) atomicAdd(b32 + a.n_groups + gid[r], static_cast<uint32_t>(v));
+          } else {
+            atomicAdd(b64 + gid[r], 1ull);
+            if (a.measure) atomicAdd(b64 + a.n_groups + gid[r], static_cast<unsigned long long>(static_cast<long long>(v)));
+          }
+        } else {
+          atomicAdd(a.acc + 2 * gid[r], 1ull);
+          if (a.measure) atomicAdd(a.acc + 2 * gid[r] + 1, static_cast<unsigned long long>(static_cast<long long>(v)));
+        }
+      }
+      if constexpr (MODE == 1) {
+        if (a.narrow_bins && (it + 1) % a.flush_every == 0 && it + 1 < iters) {
+          __syncthreads();
+          spill_bins32(b32, a.n_groups, a.acc, tid, kStreamThreads);
+          __syncthreads();
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NL; ++j) kv[j] = nkv[j];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) fv[f] = nfv[f];
+    mv = nmv;
+    row0 = nrow0;
+  }
+
+  if constexpr (MODE == 0) {
+    flush_single(r_cnt, r_sum, a.acc);
+  } else if constexpr (MODE == 1) {
+    __syncthreads();
+    if (a.narrow_bins) {
+      spill_bins32(b32, a.n_groups, a.acc, tid, kStreamThreads);
+    } else {
+      for (int64_t g = tid; g < a.n_groups; g += kStreamThreads) {
+        const unsigned long long c = b64[g];
+        if (c) {
+          atomicAdd(a.acc + 2 * g, c);
+          atomicAdd(a.acc + 2 * g + 1, b64[a.n_groups + g]);
+        }
+      }
+    }
+  }
+}
+
 }  // namespace scan
 }  // namespace laq

@@ -13,9 +13,8 @@ DIALS = {(1, 0): 222, (1, 1): 200, (1, 2): 133, (2, 0): 500, (2, 1): 199, (2, 2)
 g = gen.gen_star("Ssb", int(os.environ.get("LAQ_SF", "10")), 42, narrow=True)
 ds = star.upload_gen_star(g)
 res = {}
-for variant in ("pipe", "ldg"):
-    if variant == "ldg":
-        os.environ["LAQ_SCAN"] = "ldg"
+for variant in ("stream", "pipe", "ldg"):
+    os.environ["LAQ_SCAN"] = variant
     plans = [ds.prepare(Q.spec_with_dial(Q.group_defs(gr)[qi], gr, d)) for (gr, qi), d in DIALS.items()]
     out = []
     for p in plans:
@@ -36,7 +35,7 @@ for variant in ("pipe", "ldg"):
     res[variant] = out
     print(variant, out, flush=True)
 bad = 0
-for a, b in zip(res["pipe"], res["ldg"]):
+for a, b in list(zip(res["pipe"], res["ldg"])) + list(zip(res["stream"], res["ldg"])):
     if a[3:] != b[3:]:
         bad += 1
         print("MISMATCH", a, b)
