@@ -10,7 +10,9 @@
 #include <cub/block/block_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
+#include "predict_slot.cuh"
 #include "probe.cuh"
 
 namespace laq {
@@ -159,17 +161,19 @@ __device__ __forceinline__ void load_keys(const K* __restrict__ p, int64_t row0,
   }
 }
 
-// Decoupled look-back with a whole warp: 32 predecessors inspected per step
-// (the first tile with an inclusive prefix ends the walk).  Returns this
-// tile's exclusive prefix on every lane; publishes the inclusive prefix.
-__device__ __forceinline__ unsigned long long lookback_warp(unsigned long long* state, int64_t tile,
-                                                            unsigned long long total) {
+// Decoupled look-back, split so the aggregate is published as soon as the
+// tile's own count is known and the walk happens after independent work.
+__device__ __forceinline__ void publish_aggregate(unsigned long long* state, int64_t tile, unsigned long long total) {
+  atomicExch(state + tile, (tile == 0 ? kFlagInc : kFlagAgg) | total);
+}
+
+// Whole-warp walk: 32 predecessors inspected per step; the first one holding
+// an inclusive prefix ends it.  Returns the exclusive prefix on every lane
+// and publishes this tile's inclusive prefix.
+__device__ __forceinline__ unsigned long long resolve_prefix(unsigned long long* state, int64_t tile,
+                                                             unsigned long long total) {
   const int lane = threadIdx.x & 31;
-  if (tile == 0) {
-    if (lane == 0) atomicExch(state, kFlagInc | total);
-    return 0;
-  }
-  if (lane == 0) atomicExch(state + tile, kFlagAgg | total);
+  if (tile == 0) return 0;
   unsigned long long prefix = 0;
   int64_t p = tile - 1;
   while (true) {
@@ -191,9 +195,10 @@ __device__ __forceinline__ unsigned long long lookback_warp(unsigned long long* 
 }
 
 // Persistent: CTAs pull tiles from an atomic counter (so every predecessor of
-// a claimed tile is already running), probe, rank survivors, look back, and
-// write.  The l == 1 prediction is staged in shared memory so the compacted
-// output leaves in coalesced 8-byte runs.
+// a claimed tile is already running), probe, rank survivors locally, publish
+// the tile aggregate, compute the predictions into shared memory (l == 1)
+// while predecessors publish, resolve the prefix, then write the compacted
+// output in coalesced runs.
 template <class K, int NL, bool kPredict>
 __global__ void __launch_bounds__(kBlock) star_kernel(const StarArgs<K> a) {
   using Scan = cub::BlockScan<int, kBlock>;
@@ -237,8 +242,21 @@ __global__ void __launch_bounds__(kBlock) star_kernel(const StarArgs<K> a) {
     for (int i = 0; i < kItems; ++i) count += alive[i] ? 1 : 0;
     int excl, total;
     Scan(scan_tmp).ExclusiveSum(count, excl, total);
+    if (threadIdx.x == 0) publish_aggregate(a.tile_state, tile, static_cast<unsigned long long>(total));
+
+    if (stage_y) {  // predictions need only the local rank
+      int local = excl;
+#pragma unroll
+      for (int i = 0; i < kItems; ++i) {
+        if (!alive[i]) continue;
+        double acc = __dadd_rn(0.0, __ldg(a.partial[0] + rows[0][i]));  // 0 + 1*x (spmm_dense)
+#pragma unroll
+        for (int j = 1; j < NL; ++j) acc = __dadd_rn(acc, __ldg(a.partial[j] + rows[j][i]));
+        s_y[local++] = acc;
+      }
+    }
     if (threadIdx.x < 32) {
-      const unsigned long long prefix = lookback_warp(a.tile_state, tile, static_cast<unsigned long long>(total));
+      const unsigned long long prefix = resolve_prefix(a.tile_state, tile, static_cast<unsigned long long>(total));
       if (threadIdx.x == 0) {
         s_prefix = prefix;
         if (tile == a.n_tiles - 1) *a.nnz = static_cast<int64_t>(prefix) + total;
@@ -246,9 +264,10 @@ __global__ void __launch_bounds__(kBlock) star_kernel(const StarArgs<K> a) {
     }
     __syncthreads();
     const int64_t prefix = static_cast<int64_t>(s_prefix);
-    int64_t pos = prefix + excl;
-    int local = excl;
+    if (stage_y)
+      for (int t = threadIdx.x; t < total; t += kBlock) __stcs(a.y + prefix + t, s_y[t]);
 
+    int64_t pos = prefix + excl;
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
       if (!alive[i]) continue;
@@ -259,21 +278,17 @@ __global__ void __launch_bounds__(kBlock) star_kernel(const StarArgs<K> a) {
         if (a.rows32[j]) a.rows32[j][pos] = rows[j][i];
       }
       if constexpr (kPredict) {
-        for (int64_t c = 0; c < a.l; ++c) {
-          double acc = __dadd_rn(0.0, __ldg(a.partial[0] + static_cast<int64_t>(rows[0][i]) * a.l + c));  // 0 + 1*x (spmm_dense)
+        if (!stage_y) {
+          for (int64_t c = 0; c < a.l; ++c) {
+            double acc = __dadd_rn(0.0, __ldg(a.partial[0] + static_cast<int64_t>(rows[0][i]) * a.l + c));
 #pragma unroll
-          for (int j = 1; j < NL; ++j)
-            acc = __dadd_rn(acc, __ldg(a.partial[j] + static_cast<int64_t>(rows[j][i]) * a.l + c));
-          if (stage_y) s_y[local] = acc;
-          else __stcs(a.y + pos * a.l + c, acc);
+            for (int j = 1; j < NL; ++j)
+              acc = __dadd_rn(acc, __ldg(a.partial[j] + static_cast<int64_t>(rows[j][i]) * a.l + c));
+            __stcs(a.y + pos * a.l + c, acc);
+          }
         }
       }
       ++pos;
-      ++local;
-    }
-    if (stage_y) {
-      __syncthreads();
-      for (int t = threadIdx.x; t < total; t += kBlock) __stcs(a.y + prefix + t, s_y[t]);
     }
     __syncthreads();  // s_tile / s_y / scan storage are reused by the next tile
   }
@@ -402,7 +417,86 @@ struct laq_probe {
   Probe probes[kMaxLinks];
   StarScratch scratch;
   DevMem<int> err;
+  // slot-ordered partials + existence bitmaps (predict_slot.cuh), rebuilt per call
+  DevMem<double> pslot[kMaxLinks];
+  DevMem<uint32_t> bits[kMaxLinks];
+  int64_t pslot_l = 0;
+  StarScratch slot_scratch;
 };
+
+namespace laq {
+namespace {
+
+// Fused predict over slot-ordered partials; every probe must be DIRECT.
+void run_slot_predict(laq_ctx* ctx, laq_probe* p, const int32_t* const* d_fks, int64_t n, const double* const* d_P,
+                      int64_t l, double* d_out, int64_t* d_survivors, int64_t* d_nnz) {
+  slot::Args a{};
+  a.n = n;
+  a.l = l;
+  int64_t words_total = 0;
+  for (int j = 0; j < p->n_links; ++j) {
+    const Probe& pr = p->probes[j];
+    const int64_t size = pr.size;
+    const int64_t words = std::max<int64_t>(1, (size + 31) / 32);
+    if (p->pslot_l != l || p->pslot[j].n < static_cast<size_t>(std::max<int64_t>(size * l, 1))) {
+      p->pslot[j] = DevMem<double>(static_cast<size_t>(std::max<int64_t>(size * l, 1)));
+      p->bits[j] = DevMem<uint32_t>(static_cast<size_t>(words));
+    }
+    LAQ_CUDA(cudaMemsetAsync(p->bits[j].get(), 0, words * sizeof(uint32_t), ctx->stream));
+    if (pr.n_rows > 0) {
+      slot::scatter_slots_kernel<<<grid_for(pr.n_rows, 256, ctx->sm_count * 4), 256, 0, ctx->stream>>>(
+          pr.row_slot.get(), pr.n_rows, d_P[j], l, p->pslot[j].get(), p->bits[j].get());
+      launched(ctx);
+    }
+    a.fk[j] = d_fks[j];
+    a.base[j] = pr.base;
+    a.size[j] = size;
+    a.bits[j] = p->bits[j].get();
+    a.pslot[j] = p->pslot[j].get();
+    a.smem_off[j] = -1;
+    if (words_total + words <= slot::kSmemBitmapWords) {
+      a.smem_off[j] = static_cast<int>(words_total);
+      words_total += words;
+    }
+  }
+  p->pslot_l = l;
+  a.smem_words = static_cast<int>(words_total);
+  a.y = d_out;
+  a.survivors = d_survivors;
+  a.nnz = d_nnz;
+  a.n_tiles = (n + slot::kTile - 1) / slot::kTile;
+  if (a.n_tiles == 0) {
+    LAQ_CUDA(cudaMemsetAsync(d_nnz, 0, sizeof(int64_t), ctx->stream));
+    return;
+  }
+  p->slot_scratch.ensure(a.n_tiles);
+  a.tile_state = p->slot_scratch.tile_state.get();
+  a.tile_counter = p->slot_scratch.counter.get();
+  LAQ_CUDA(cudaMemsetAsync(a.tile_state, 0, a.n_tiles * sizeof(unsigned long long), ctx->stream));
+  LAQ_CUDA(cudaMemsetAsync(a.tile_counter, 0, sizeof(int), ctx->stream));
+  const size_t smem = static_cast<size_t>(words_total) * sizeof(uint32_t);
+  auto launch = [&](auto kern) {
+    int per_sm = 0;
+    LAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, slot::kThreads, smem));
+    const unsigned g = static_cast<unsigned>(std::min<int64_t>(a.n_tiles, int64_t{ctx->sm_count} * std::max(per_sm, 1)));
+    kern<<<g, slot::kThreads, smem, ctx->stream>>>(a);
+  };
+  switch (p->n_links) {
+    case 1: launch(slot::predict_slot_kernel<1>); break;
+    case 2: launch(slot::predict_slot_kernel<2>); break;
+    case 3: launch(slot::predict_slot_kernel<3>); break;
+    case 4: launch(slot::predict_slot_kernel<4>); break;
+    case 5: launch(slot::predict_slot_kernel<5>); break;
+    case 6: launch(slot::predict_slot_kernel<6>); break;
+    case 7: launch(slot::predict_slot_kernel<7>); break;
+    case 8: launch(slot::predict_slot_kernel<8>); break;
+    default: fail(LAQ_ERR_UNSUPPORTED, "fused predict supports 1..8 dimensions");
+  }
+  launched(ctx);
+}
+
+}  // namespace
+}  // namespace laq
 
 extern "C" {
 
@@ -469,6 +563,12 @@ int laq_probe_fused_predict(laq_ctx* ctx, const laq_probe* probe, const int32_t*
   return guard(ctx, [&] {
     if (l < 1 || l > 8) fail(LAQ_ERR_UNSUPPORTED, "fused single-pass predict handles l <= 8 (use star join + apply)");
     auto* p = const_cast<laq_probe*>(probe);
+    bool all_direct = !std::getenv("LAQ_PREDICT_GENERIC");
+    for (int j = 0; j < p->n_links; ++j) all_direct = all_direct && p->probes[j].kind == PROBE_DIRECT;
+    if (all_direct) {
+      run_slot_predict(ctx, p, d_fks, n_fact, d_partials, l, d_out, d_survivors, d_nnz);
+      return;
+    }
     StarArgs<int32_t> a{};
     a.n_links = p->n_links;
     a.n = n_fact;
