@@ -161,6 +161,11 @@ int laq_fused_star_predict(laq_ctx* ctx, int32_t n_links, const int32_t* const* 
 typedef struct laq_probe laq_probe;
 int laq_probe_build(laq_ctx* ctx, int32_t n_links, const int32_t* const* d_pks,
                     const int64_t* h_pk_rows, laq_probe** out);
+/* Optionally bind the partials once (re-laid out in key-slot order next to an
+ * existence bitmap); later calls may then pass d_partials = NULL.  Binding
+ * snapshots the values: rebind after the partials change (refresh_partial,
+ * fusion.cpp:161-179). */
+int laq_probe_bind_partials(laq_ctx* ctx, laq_probe* probe, const double* const* d_partials, int64_t l);
 /* ... then stream the fact keys; the survivor count is written to d_nnz (device). */
 int laq_probe_fused_predict(laq_ctx* ctx, const laq_probe* probe, const int32_t* const* d_fks,
                             int64_t n_fact, const double* const* d_partials, int64_t l,

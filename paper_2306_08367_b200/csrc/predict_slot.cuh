@@ -4,18 +4,21 @@
 // instead of  slot -> dim row -> P_j[row]  (two dependent gathers into two
 // tables) the partials are re-laid out once per call in slot order,
 // Pslot_j[slot] = P_j[row(slot)], next to a 1-bit-per-slot existence bitmap.
-// A fact row then costs, per dimension, one bitmap test (shared memory when
-// the bitmaps fit) and one 8-byte gather that is only issued for rows still
-// alive.  That halves the gather footprint (L1 hit rate) and the dependent
-// latency chain of the generic star kernel.
 //
-// Survivor compaction: single-pass decoupled look-back over 4096-row tiles,
-// the tile aggregate published before the predictions are computed, the
-// walk resolved after; predictions staged in shared memory and written in
-// coalesced runs (l == 1) or directly (l <= 8).
+// Measured on B200 (profiles/): random 8-byte gathers through L1 cost one
+// L1 wavefront per lane, which caps a global-gather formulation near
+// 1.5-1.8 TB/s.  So this kernel stages the existence bitmaps AND the
+// slot-ordered partials in shared memory whenever they fit (cfg1: 10K x 8 B =
+// 80 KB), where a warp's 32 random reads cost a few bank-conflict cycles
+// instead of 32 wavefronts.
+//
+// Layout is striped: thread t of a 512-thread CTA owns rows
+// tile_base + k*512 + t (k < 8), so key loads and compacted prediction stores
+// are both warp-coalesced without a staging buffer.  Survivor ranks come
+// from warp ballots + one 128-entry scan per tile; the tile's global offset
+// from a single-pass decoupled look-back (whole-warp window), with the tile
+// aggregate published before the predictions are gathered.
 #pragma once
-
-#include <cub/block/block_scan.cuh>
 
 #include "probe.cuh"
 
@@ -23,10 +26,11 @@ namespace laq {
 namespace slot {
 
 constexpr int kMaxLinks = 8;
-constexpr int kThreads = 256;
-constexpr int kItems = 16;
-constexpr int kTile = kThreads * kItems;  // 4096 rows
-constexpr int kSmemBitmapWords = 4 * 1024;  // 16 KB of staged existence bitmaps
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+constexpr int kStripes = 8;
+constexpr int kTile = kThreads * kStripes;  // 4096 rows
+constexpr int kSmemBudget = 200 * 1024;    // bitmaps + partials staged per CTA
 
 struct Args {
   int64_t n;
@@ -36,8 +40,10 @@ struct Args {
   int64_t size[kMaxLinks];
   const uint32_t* bits[kMaxLinks];  // existence bitmap per link
   const double* pslot[kMaxLinks];   // slot-ordered partials (size x l)
-  int smem_off[kMaxLinks];          // >= 0: bitmap staged in smem at this word offset
-  int smem_words;
+  int bits_off[kMaxLinks];          // >= 0: bitmap staged in smem at this word offset
+  int p_off[kMaxLinks];             // >= 0: partials staged in smem at this double offset (l == 1)
+  int smem_words;                   // staged bitmap words
+  int smem_doubles;                 // staged partial doubles (after the bitmaps, 8-byte aligned)
   double* y;
   int64_t* survivors;
   unsigned long long* tile_state;
@@ -73,114 +79,198 @@ __device__ __forceinline__ unsigned long long resolve(unsigned long long* state,
   return prefix;
 }
 
+// ---------------------------------------------------------------------------
+// Two-pass, warp-centric, barrier-free formulation.
+//
+// A chunk is 32 lanes x 32 rows = 1024 consecutive fact rows, owned by ONE
+// warp, striped so lane t handles rows chunk_base + k*32 + t (k < 32): key
+// loads and compacted stores are coalesced.  Pass 1 counts each chunk's
+// survivors (keys + existence bits: 4*J bytes/row); a device scan turns the
+// counts into output offsets; pass 2 re-probes, ranks survivors with warp
+// ballots and writes the predictions.  No CTA-wide barrier and no inter-CTA
+// dependency sits on the hot path, so occupancy - not a look-back chain -
+// hides the gather latency (the single-pass look-back measured 3x slower
+// here: one tile in flight per CTA).
+// ---------------------------------------------------------------------------
+
+constexpr int kChunkRows = 1024;
+constexpr int kChunkSteps = kChunkRows / 32;
+constexpr int kWarpThreads = 256;
+
+__device__ __forceinline__ void stage_bits(const Args& a, uint32_t* s_bits, int nl) {
+  for (int j = 0; j < nl; ++j)
+    if (a.bits_off[j] >= 0) {
+      const int64_t words = (a.size[j] + 31) / 32;
+      for (int64_t w = threadIdx.x; w < words; w += blockDim.x) s_bits[a.bits_off[j] + w] = __ldg(a.bits[j] + w);
+    }
+  __syncthreads();
+}
+
+// 4 consecutive rows per lane (one int4 of keys per link): existence + slots.
 template <int NL>
-__global__ void __launch_bounds__(kThreads) predict_slot_kernel(const Args a) {
-  using Scan = cub::BlockScan<int, kThreads>;
-  extern __shared__ __align__(16) uint32_t s_bits[];
-  __shared__ typename Scan::TempStorage scan_tmp;
-  __shared__ int64_t s_tile;
-  __shared__ unsigned long long s_prefix;
-  __shared__ double s_y[kTile];
-
-  for (int w = threadIdx.x; w < a.smem_words; w += kThreads) {
+__device__ __forceinline__ int probe4_rows(const Args& a, const uint32_t* s_bits, int64_t r0,
+                                           const int4 (&kv)[NL], uint32_t (&slot)[NL][4], bool (&ok)[4]) {
+  const int64_t left = a.n - r0;
+  const int valid = left >= 4 ? 4 : (left > 0 ? static_cast<int>(left) : 0);
 #pragma unroll
-    for (int j = 0; j < NL; ++j)
-      if (a.smem_off[j] >= 0 && w >= a.smem_off[j] && w < a.smem_off[j] + (a.size[j] + 31) / 32)
-        s_bits[w] = __ldg(a.bits[j] + (w - a.smem_off[j]));
+  for (int i = 0; i < 4; ++i) ok[i] = i < valid;
+#pragma unroll
+  for (int j = 0; j < NL; ++j) {
+    const int32_t key[4] = {kv[j].x, kv[j].y, kv[j].z, kv[j].w};
+    const uint32_t base = static_cast<uint32_t>(a.base[j]), size = static_cast<uint32_t>(a.size[j]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t s = static_cast<uint32_t>(key[i]) - base;
+      bool o = ok[i] && key[i] >= 0 && s < size;
+      if (o) {
+        const uint32_t word = a.bits_off[j] >= 0 ? s_bits[a.bits_off[j] + (s >> 5)] : __ldg(a.bits[j] + (s >> 5));
+        o = (word >> (s & 31)) & 1u;
+      }
+      ok[i] = o;
+      slot[j][i] = s;
+    }
   }
-  const bool stage_y = a.l == 1;
+  return (ok[0] ? 1 : 0) + (ok[1] ? 1 : 0) + (ok[2] ? 1 : 0) + (ok[3] ? 1 : 0);
+}
 
-  while (true) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1);
-    __syncthreads();
-    const int64_t tile = s_tile;
-    if (tile >= a.n_tiles) break;
-    const int64_t row0 = tile * kTile + static_cast<int64_t>(threadIdx.x) * kItems;
-    const int64_t left = a.n - row0;
-    const int valid = left >= kItems ? kItems : (left > 0 ? static_cast<int>(left) : 0);
+template <int NL>
+__device__ __forceinline__ void load_kv(const Args& a, int64_t r0, int4 (&kv)[NL]) {
+#pragma unroll
+  for (int j = 0; j < NL; ++j) {
+    if (r0 + 4 <= a.n) {
+      kv[j] = __ldcs(reinterpret_cast<const int4*>(a.fk[j] + r0));
+    } else {
+      kv[j].x = r0 < a.n ? a.fk[j][r0] : -1;
+      kv[j].y = r0 + 1 < a.n ? a.fk[j][r0 + 1] : -1;
+      kv[j].z = r0 + 2 < a.n ? a.fk[j][r0 + 2] : -1;
+      kv[j].w = r0 + 3 < a.n ? a.fk[j][r0 + 3] : -1;
+    }
+  }
+}
 
-    uint32_t slot[NL][kItems];
-    bool alive[kItems];
+// Chunk = 1024 rows = 8 segments of 128 rows; in a segment lane t owns rows
+// seg + 4t .. seg + 4t + 3 (one 16-byte key load per link).
+constexpr int kSegRows = 128;
+constexpr int kSegs = kChunkRows / kSegRows;
+
+template <int NL>
+__global__ void __launch_bounds__(kWarpThreads) count_chunks_kernel(const Args a, int64_t n_chunks, int* counts) {
+  extern __shared__ __align__(16) uint32_t s_bits[];
+  stage_bits(a, s_bits, NL);
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (kWarpThreads / 32);
+  for (int64_t c = (static_cast<int64_t>(blockIdx.x) * kWarpThreads + threadIdx.x) >> 5; c < n_chunks; c += warps) {
+    int4 kv[kSegs][NL];
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) alive[i] = i < valid;
+    for (int g = 0; g < kSegs; ++g) load_kv<NL>(a, c * kChunkRows + g * kSegRows + 4 * lane, kv[g]);  // all loads first
+    int cnt = 0;
 #pragma unroll
-    for (int j = 0; j < NL; ++j) {
-      int32_t k[kItems];
-      if (valid == kItems) {
+    for (int g = 0; g < kSegs; ++g) {
+      uint32_t slot[NL][4];
+      bool ok[4];
+      cnt += probe4_rows<NL>(a, s_bits, c * kChunkRows + g * kSegRows + 4 * lane, kv[g], slot, ok);
+    }
+    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) counts[c] = cnt;
+  }
+}
+
+template <int NL>
+__global__ void __launch_bounds__(kWarpThreads) write_chunks_kernel(const Args a, int64_t n_chunks,
+                                                                    const int64_t* offsets) {
+  // Dynamic smem: [bitmaps][partials (l == 1, when staged)]; static: per-warp
+  // transpose buffers for two segments.
+  extern __shared__ __align__(16) uint32_t s_bits[];
+  double* s_p = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(s_bits) + ((a.smem_words * 4 + 15) & ~15));
+  __shared__ double s_y[kWarpThreads / 32][2 * kSegRows];
+  stage_bits(a, s_bits, NL);
 #pragma unroll
-        for (int q = 0; q < kItems / 4; ++q) {
-          const int4 v = __ldcs(reinterpret_cast<const int4*>(a.fk[j] + row0) + q);
-          k[4 * q] = v.x; k[4 * q + 1] = v.y; k[4 * q + 2] = v.z; k[4 * q + 3] = v.w;
+  for (int j = 0; j < NL; ++j)
+    if (a.p_off[j] >= 0)
+      for (int64_t s = threadIdx.x; s < a.size[j]; s += kWarpThreads) s_p[a.p_off[j] + s] = __ldg(a.pslot[j] + s);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (kWarpThreads / 32);
+  auto pval = [&](int j, uint32_t s) -> double {
+    return a.p_off[j] >= 0 ? s_p[a.p_off[j] + s] : __ldg(a.pslot[j] + s);
+  };
+  for (int64_t c = (static_cast<int64_t>(blockIdx.x) * kWarpThreads + threadIdx.x) >> 5; c < n_chunks; c += warps) {
+    int64_t pos = offsets[c];
+#pragma unroll 1
+    for (int g = 0; g < kSegs; g += 2) {  // two segments per step: 8 gathers in flight per lane
+      const int64_t r0 = c * kChunkRows + g * kSegRows + 4 * lane;
+      int4 kv0[NL], kv1[NL];
+      load_kv<NL>(a, r0, kv0);
+      load_kv<NL>(a, r0 + kSegRows, kv1);
+      uint32_t slot0[NL][4], slot1[NL][4];
+      bool ok0[4], ok1[4];
+      const int c0 = probe4_rows<NL>(a, s_bits, r0, kv0, slot0, ok0);
+      const int c1 = probe4_rows<NL>(a, s_bits, r0 + kSegRows, kv1, slot1, ok1);
+      int e0 = c0, e1 = c1;  // warp inclusive scans (row order = lane order within a segment)
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v0 = __shfl_up_sync(0xffffffffu, e0, o);
+        const int v1 = __shfl_up_sync(0xffffffffu, e1, o);
+        if (lane >= o) {
+          e0 += v0;
+          e1 += v1;
         }
-      } else {
-#pragma unroll
-        for (int i = 0; i < kItems; ++i) k[i] = i < valid ? a.fk[j][row0 + i] : 0;
       }
-      const uint32_t base = static_cast<uint32_t>(a.base[j]), size = static_cast<uint32_t>(a.size[j]);
-      const int off = a.smem_off[j];
+      const int t0 = __shfl_sync(0xffffffffu, e0, 31), t1 = __shfl_sync(0xffffffffu, e1, 31);
+      e0 -= c0;
+      e1 -= c1;
+      if (a.l == 1 && !a.survivors) {
+        double y0[4], y1[4];
 #pragma unroll
-      for (int i = 0; i < kItems; ++i) {
-        const uint32_t s = static_cast<uint32_t>(k[i]) - base;
-        bool ok = alive[i] && k[i] >= 0 && s < size;
-        if (ok) {
-          const uint32_t word = off >= 0 ? s_bits[off + (s >> 5)] : __ldg(a.bits[j] + (s >> 5));
-          ok = (word >> (s & 31)) & 1u;
+        for (int i = 0; i < 4; ++i) {  // issue every gather before any use
+          y0[i] = ok0[i] ? pval(0, slot0[0][i]) : 0.0;
+          y1[i] = ok1[i] ? pval(0, slot1[0][i]) : 0.0;
         }
-        alive[i] = ok;
-        slot[j][i] = s;
-      }
-    }
-
-    int count = 0;
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) count += alive[i] ? 1 : 0;
-    int excl, total;
-    Scan(scan_tmp).ExclusiveSum(count, excl, total);
-    if (threadIdx.x == 0)
-      atomicExch(a.tile_state + tile, (tile == 0 ? LAQ_SLOT_INC : LAQ_SLOT_AGG) | static_cast<unsigned long long>(total));
-
-    if (stage_y) {
-      int local = excl;
+        for (int i = 0; i < 4; ++i) {
+          y0[i] = __dadd_rn(0.0, y0[i]);  // 0 + 1*x (spmm_dense)
+          y1[i] = __dadd_rn(0.0, y1[i]);
 #pragma unroll
-      for (int i = 0; i < kItems; ++i) {
-        if (!alive[i]) continue;
-        double acc = __dadd_rn(0.0, __ldg(a.pslot[0] + slot[0][i]));  // 0 + 1*x (spmm_dense)
-#pragma unroll
-        for (int j = 1; j < NL; ++j) acc = __dadd_rn(acc, __ldg(a.pslot[j] + slot[j][i]));  // fusion.cpp:73-76
-        s_y[local++] = acc;
-      }
-    }
-    if (threadIdx.x < 32) {
-      const unsigned long long prefix = resolve(a.tile_state, tile, static_cast<unsigned long long>(total));
-      if (threadIdx.x == 0) {
-        s_prefix = prefix;
-        if (tile == a.n_tiles - 1) *a.nnz = static_cast<int64_t>(prefix) + total;
-      }
-    }
-    __syncthreads();
-    const int64_t prefix = static_cast<int64_t>(s_prefix);
-    if (stage_y) {
-      for (int t = threadIdx.x; t < total; t += kThreads) __stcs(a.y + prefix + t, s_y[t]);
-    }
-    if (!stage_y || a.survivors) {
-      int64_t pos = prefix + excl;
-#pragma unroll
-      for (int i = 0; i < kItems; ++i) {
-        if (!alive[i]) continue;
-        if (a.survivors) a.survivors[pos] = row0 + i;
-        if (!stage_y) {
-          for (int64_t c = 0; c < a.l; ++c) {
-            double acc = __dadd_rn(0.0, __ldg(a.pslot[0] + static_cast<int64_t>(slot[0][i]) * a.l + c));
-#pragma unroll
-            for (int j = 1; j < NL; ++j)
-              acc = __dadd_rn(acc, __ldg(a.pslot[j] + static_cast<int64_t>(slot[j][i]) * a.l + c));
-            __stcs(a.y + pos * a.l + c, acc);
+          for (int j = 1; j < NL; ++j) {  // ((P_0 + P_1) + ...): fusion.cpp:73-76
+            y0[i] = __dadd_rn(y0[i], ok0[i] ? pval(j, slot0[j][i]) : 0.0);
+            y1[i] = __dadd_rn(y1[i], ok1[i] ? pval(j, slot1[j][i]) : 0.0);
           }
         }
-        ++pos;
+        int at0 = e0, at1 = t0 + e1;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (ok0[i]) s_y[wib][at0++] = y0[i];
+          if (ok1[i]) s_y[wib][at1++] = y1[i];
+        }
+        __syncwarp();
+        for (int m = lane; m < t0 + t1; m += 32) __stcs(a.y + pos + m, s_y[wib][m]);
+        __syncwarp();
+      } else {
+        int64_t at = pos + e0;
+        for (int seg = 0; seg < 2; ++seg) {
+          if (seg == 1) at = pos + t0 + e1;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const bool ok = seg == 0 ? ok0[i] : ok1[i];
+            if (!ok) continue;
+            if (a.survivors) a.survivors[at] = r0 + seg * kSegRows + i;
+            for (int64_t col = 0; col < a.l; ++col) {
+              const uint32_t s0 = seg == 0 ? slot0[0][i] : slot1[0][i];
+              double acc = __dadd_rn(0.0, __ldg(a.pslot[0] + static_cast<int64_t>(s0) * a.l + col));
+#pragma unroll
+              for (int j = 1; j < NL; ++j) {
+                const uint32_t sj = seg == 0 ? slot0[j][i] : slot1[j][i];
+                acc = __dadd_rn(acc, __ldg(a.pslot[j] + static_cast<int64_t>(sj) * a.l + col));
+              }
+              __stcs(a.y + at * a.l + col, acc);
+            }
+            ++at;
+          }
+        }
       }
+      pos += t0 + t1;
     }
-    __syncthreads();
+    if (c == n_chunks - 1 && lane == 0) *a.nnz = pos;
   }
 }
 

@@ -8,6 +8,7 @@
 // HBM traffic per fact row: 4*J bytes of int32 keys in, 8*l bytes of fp64
 // predictions out (partials P_j are L2/L1 resident: r_j*l*8 bytes each).
 #include <cub/block/block_scan.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <cstdlib>
@@ -421,19 +422,20 @@ struct laq_probe {
   DevMem<double> pslot[kMaxLinks];
   DevMem<uint32_t> bits[kMaxLinks];
   int64_t pslot_l = 0;
-  StarScratch slot_scratch;
+  bool bound = false;
+  // two-pass chunk counts / offsets + scan temp storage
+  DevMem<int> chunk_counts;
+  DevMem<int64_t> chunk_offsets;
+  DevMem<char> scan_tmp;
+  size_t scan_tmp_bytes = 0;
+  int64_t chunk_cap = 0;
 };
 
 namespace laq {
 namespace {
 
-// Fused predict over slot-ordered partials; every probe must be DIRECT.
-void run_slot_predict(laq_ctx* ctx, laq_probe* p, const int32_t* const* d_fks, int64_t n, const double* const* d_P,
-                      int64_t l, double* d_out, int64_t* d_survivors, int64_t* d_nnz) {
-  slot::Args a{};
-  a.n = n;
-  a.l = l;
-  int64_t words_total = 0;
+// Slot-ordered partials + existence bitmaps for every link (predict_slot.cuh).
+void bind_slots(laq_ctx* ctx, laq_probe* p, const double* const* d_P, int64_t l) {
   for (int j = 0; j < p->n_links; ++j) {
     const Probe& pr = p->probes[j];
     const int64_t size = pr.size;
@@ -448,48 +450,95 @@ void run_slot_predict(laq_ctx* ctx, laq_probe* p, const int32_t* const* d_fks, i
           pr.row_slot.get(), pr.n_rows, d_P[j], l, p->pslot[j].get(), p->bits[j].get());
       launched(ctx);
     }
+  }
+  p->pslot_l = l;
+  p->bound = true;
+}
+
+// Fused predict over slot-ordered partials; every probe must be DIRECT.
+// d_P == nullptr uses the partials bound by laq_probe_bind_partials.
+void run_slot_predict(laq_ctx* ctx, laq_probe* p, const int32_t* const* d_fks, int64_t n, const double* const* d_P,
+                      int64_t l, double* d_out, int64_t* d_survivors, int64_t* d_nnz) {
+  slot::Args a{};
+  a.n = n;
+  a.l = l;
+  int64_t words_total = 0;
+  if (d_P) bind_slots(ctx, p, d_P, l);
+  else if (!p->bound || p->pslot_l != l) fail(LAQ_ERR_SHAPE, "fused predict: no partials bound for this output width");
+  for (int j = 0; j < p->n_links; ++j) {
+    const Probe& pr = p->probes[j];
     a.fk[j] = d_fks[j];
     a.base[j] = pr.base;
-    a.size[j] = size;
+    a.size[j] = pr.size;
     a.bits[j] = p->bits[j].get();
     a.pslot[j] = p->pslot[j].get();
-    a.smem_off[j] = -1;
-    if (words_total + words <= slot::kSmemBitmapWords) {
-      a.smem_off[j] = static_cast<int>(words_total);
+    a.bits_off[j] = -1;
+    a.p_off[j] = -1;
+  }
+  // Shared-memory staging of the existence bitmaps that fit (partials are
+  // gathered through L1: high occupancy matters more than staging them).
+  for (int j = 0; j < p->n_links; ++j) {
+    const int64_t words = std::max<int64_t>(1, (a.size[j] + 31) / 32);
+    if ((words_total + words) * 4 <= 32 * 1024) {
+      a.bits_off[j] = static_cast<int>(words_total);
       words_total += words;
     }
   }
-  p->pslot_l = l;
   a.smem_words = static_cast<int>(words_total);
+  // l == 1: stage the slot-ordered partials too when they fit in 96 KB
+  // (shared-memory gathers instead of one L1 wavefront per lane).
+  int64_t doubles = 0;
+  if (l == 1)
+    for (int j = 0; j < p->n_links; ++j)
+      if ((doubles + a.size[j]) * 8 <= 96 * 1024) {
+        a.p_off[j] = static_cast<int>(doubles);
+        doubles += a.size[j];
+      }
+  a.smem_doubles = static_cast<int>(doubles);
   a.y = d_out;
   a.survivors = d_survivors;
   a.nnz = d_nnz;
-  a.n_tiles = (n + slot::kTile - 1) / slot::kTile;
-  if (a.n_tiles == 0) {
+  const int64_t n_chunks = (n + slot::kChunkRows - 1) / slot::kChunkRows;
+  if (n_chunks == 0) {
     LAQ_CUDA(cudaMemsetAsync(d_nnz, 0, sizeof(int64_t), ctx->stream));
     return;
   }
-  p->slot_scratch.ensure(a.n_tiles);
-  a.tile_state = p->slot_scratch.tile_state.get();
-  a.tile_counter = p->slot_scratch.counter.get();
-  LAQ_CUDA(cudaMemsetAsync(a.tile_state, 0, a.n_tiles * sizeof(unsigned long long), ctx->stream));
-  LAQ_CUDA(cudaMemsetAsync(a.tile_counter, 0, sizeof(int), ctx->stream));
-  const size_t smem = static_cast<size_t>(words_total) * sizeof(uint32_t);
-  auto launch = [&](auto kern) {
+  if (p->chunk_cap < n_chunks) {
+    p->chunk_counts = DevMem<int>(n_chunks);
+    p->chunk_offsets = DevMem<int64_t>(n_chunks);
+    size_t bytes = 0;
+    LAQ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, p->chunk_counts.get(), p->chunk_offsets.get(), n_chunks,
+                                           ctx->stream));
+    p->scan_tmp = DevMem<char>(std::max<size_t>(bytes, 1));
+    p->scan_tmp_bytes = bytes;
+    p->chunk_cap = n_chunks;
+  }
+  const size_t smem = static_cast<size_t>(words_total) * 4;
+  const size_t smem_w = static_cast<size_t>((words_total * 4 + 15) & ~int64_t{15}) + static_cast<size_t>(doubles) * 8;
+  auto launch = [&](auto count_k, auto write_k) {
+    LAQ_CUDA(cudaFuncSetAttribute(write_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_w)));
+    const int64_t want = (n_chunks + slot::kWarpThreads / 32 - 1) / (slot::kWarpThreads / 32);
     int per_sm = 0;
-    LAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, slot::kThreads, smem));
-    const unsigned g = static_cast<unsigned>(std::min<int64_t>(a.n_tiles, int64_t{ctx->sm_count} * std::max(per_sm, 1)));
-    kern<<<g, slot::kThreads, smem, ctx->stream>>>(a);
+    LAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, count_k, slot::kWarpThreads, smem));
+    const unsigned g1 = static_cast<unsigned>(std::min<int64_t>(want, int64_t{ctx->sm_count} * std::max(per_sm, 1)));
+    LAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, write_k, slot::kWarpThreads, smem_w));
+    const unsigned g2 = static_cast<unsigned>(std::min<int64_t>(want, int64_t{ctx->sm_count} * std::max(per_sm, 1)));
+    count_k<<<g1, slot::kWarpThreads, smem, ctx->stream>>>(a, n_chunks, p->chunk_counts.get());
+    size_t bytes = p->scan_tmp_bytes;
+    LAQ_CUDA(cub::DeviceScan::ExclusiveSum(p->scan_tmp.get(), bytes, p->chunk_counts.get(), p->chunk_offsets.get(),
+                                           n_chunks, ctx->stream));
+    write_k<<<g2, slot::kWarpThreads, smem_w, ctx->stream>>>(a, n_chunks, p->chunk_offsets.get());
+    ctx->launches += 2;
   };
   switch (p->n_links) {
-    case 1: launch(slot::predict_slot_kernel<1>); break;
-    case 2: launch(slot::predict_slot_kernel<2>); break;
-    case 3: launch(slot::predict_slot_kernel<3>); break;
-    case 4: launch(slot::predict_slot_kernel<4>); break;
-    case 5: launch(slot::predict_slot_kernel<5>); break;
-    case 6: launch(slot::predict_slot_kernel<6>); break;
-    case 7: launch(slot::predict_slot_kernel<7>); break;
-    case 8: launch(slot::predict_slot_kernel<8>); break;
+    case 1: launch(slot::count_chunks_kernel<1>, slot::write_chunks_kernel<1>); break;
+    case 2: launch(slot::count_chunks_kernel<2>, slot::write_chunks_kernel<2>); break;
+    case 3: launch(slot::count_chunks_kernel<3>, slot::write_chunks_kernel<3>); break;
+    case 4: launch(slot::count_chunks_kernel<4>, slot::write_chunks_kernel<4>); break;
+    case 5: launch(slot::count_chunks_kernel<5>, slot::write_chunks_kernel<5>); break;
+    case 6: launch(slot::count_chunks_kernel<6>, slot::write_chunks_kernel<6>); break;
+    case 7: launch(slot::count_chunks_kernel<7>, slot::write_chunks_kernel<7>); break;
+    case 8: launch(slot::count_chunks_kernel<8>, slot::write_chunks_kernel<8>); break;
     default: fail(LAQ_ERR_UNSUPPORTED, "fused predict supports 1..8 dimensions");
   }
   launched(ctx);
@@ -557,6 +606,15 @@ int laq_probe_destroy(laq_probe* p) {
   return LAQ_OK;
 }
 
+int laq_probe_bind_partials(laq_ctx* ctx, laq_probe* p, const double* const* d_partials, int64_t l) {
+  return guard(ctx, [&] {
+    if (l < 1) fail(LAQ_ERR_SHAPE, "bind_partials: output width must be positive");
+    for (int j = 0; j < p->n_links; ++j)
+      if (p->probes[j].kind != PROBE_DIRECT) fail(LAQ_ERR_UNSUPPORTED, "bind_partials: hashed dimension keys");
+    bind_slots(ctx, p, d_partials, l);
+  });
+}
+
 int laq_probe_fused_predict(laq_ctx* ctx, const laq_probe* probe, const int32_t* const* d_fks, int64_t n_fact,
                             const double* const* d_partials, int64_t l, double* d_out, int64_t* d_survivors,
                             int64_t* d_nnz) {
@@ -569,6 +627,7 @@ int laq_probe_fused_predict(laq_ctx* ctx, const laq_probe* probe, const int32_t*
       run_slot_predict(ctx, p, d_fks, n_fact, d_partials, l, d_out, d_survivors, d_nnz);
       return;
     }
+    if (!d_partials) fail(LAQ_ERR_SHAPE, "fused predict: partials required for hashed dimension keys");
     StarArgs<int32_t> a{};
     a.n_links = p->n_links;
     a.n = n_fact;

@@ -115,6 +115,9 @@ class FusedStarPredictor:
         self.ctx.check(self.ctx.lib.laq_probe_build(self.ctx.h, len(self.pks), ptrs(self.pks), prow, C.byref(h)))
         self.h = h
         self.nnz_dev = torch.zeros(1, dtype=torch.int64, device="cuda")
+        # Bind the partials once (slot-ordered layout); per call only the fact keys stream.
+        rc = self.ctx.lib.laq_probe_bind_partials(self.ctx.h, self.h, ptrs(self.partials), self.l)
+        self.bound = rc == 0
 
     def __call__(self, fact_fks, out=None, survivors=None, sync=True):
         fks = [dev(f, torch.int32) for f in fact_fks]
@@ -123,7 +126,7 @@ class FusedStarPredictor:
             out = torch.empty((n, self.l), dtype=f64, device="cuda")
         self.ctx.bind_stream()
         self.ctx.check(self.ctx.lib.laq_probe_fused_predict(
-            self.ctx.h, self.h, ptrs(fks), n, ptrs(self.partials), self.l, out.data_ptr(),
+            self.ctx.h, self.h, ptrs(fks), n, None if self.bound else ptrs(self.partials), self.l, out.data_ptr(),
             survivors.data_ptr() if survivors is not None else None, self.nnz_dev.data_ptr()))
         if not sync:
             return out, None
