@@ -286,6 +286,7 @@ def main():
     scan_ms = np.array([[ev[i][q][0].elapsed_time(ev[i][q][1]) for q in range(len(plans))] for i in range(args.steps)])
     bytes_per_launch = np.array([p.bytes_per_row * n_rows for p in plans], dtype=np.float64)
     achieved = float(bytes_per_launch.sum() / (scan_ms.mean(axis=0).sum() / 1e3) / 1e9)
+    traffic = ncu_traffic()
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(peaks_path):
         peaks = json.load(open(peaks_path))
@@ -360,7 +361,7 @@ def main():
                        "result_rows": [int(r.shape[0]) for r in results],
                        "per_query_scan_ms": [round(float(x), 4) for x in scan_ms.mean(axis=0)]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": traffic,
                          "kernel": "scan_kernel (K4 ssb_scan_groupby)",
                          "algorithmic_bytes_per_launch": [int(b) for b in bytes_per_launch],
                          "peak_source": peak_src},
@@ -376,6 +377,25 @@ def main():
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def ncu_traffic():
+    """DRAM bytes (read + write) per scan launch from the committed ncu --set full
+    capture of the same six queries (profiles/<round>/scan_full_metrics.json)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "scan_full_metrics.json")))
+    if not files:
+        return None
+    rows = json.load(open(files[-1]))
+    unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tot = []
+    for r in rows:
+        b = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            v, u = r[k].split()
+            b += float(v) * unit[u]
+        tot.append(b)
+    return {"bytes_per_launch_mean": sum(tot) / len(tot), "source": os.path.relpath(files[-1], ROOT)}
 
 
 def _fact_cols(q):

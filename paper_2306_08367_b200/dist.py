@@ -1,0 +1,41 @@
+"""Multi-GPU plumbing for the row-sharded fact table.
+
+Fact rows are independent: rank r owns the contiguous row range
+shard_range(n, r, world); dimensions are replicated.  Query accumulators
+(int64 [G][count, sum]) are summed across ranks with one all-reduce; fused
+predictions stay row-sharded and their global order is the rank order.
+torch.distributed is the transport (NCCL on GPUs, gloo in the CPU tests).
+"""
+from __future__ import annotations
+
+import torch
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """[begin, end) of rank's contiguous share of n rows (sizes differ by at most 1)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    return n * rank // world, n * (rank + 1) // world
+
+
+def allreduce_acc(acc: torch.Tensor, group=None) -> torch.Tensor:
+    """Sum the per-rank query accumulators in place (exact: int64)."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
+    return acc
+
+
+def gather_offsets(local_count: int, group=None, device=None) -> tuple[int, int]:
+    """Exclusive prefix of per-rank survivor counts -> (global offset, global total):
+    where rank r's fused predictions go in the global, rank-ordered output."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return 0, local_count
+    world = dist.get_world_size(group)
+    t = torch.tensor([local_count], dtype=torch.int64, device=device)
+    out = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(out, t, group=group)
+    counts = [int(x.item()) for x in out]
+    r = dist.get_rank(group)
+    return sum(counts[:r]), sum(counts)
