@@ -286,7 +286,7 @@ def main():
     scan_ms = np.array([[ev[i][q][0].elapsed_time(ev[i][q][1]) for q in range(len(plans))] for i in range(args.steps)])
     bytes_per_launch = np.array([p.bytes_per_row * n_rows for p in plans], dtype=np.float64)
     achieved = float(bytes_per_launch.sum() / (scan_ms.mean(axis=0).sum() / 1e3) / 1e9)
-    traffic = ncu_traffic()
+    traffic, traffic_src = ncu_traffic() or (None, None)
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(peaks_path):
         peaks = json.load(open(peaks_path))
@@ -361,7 +361,7 @@ def main():
                        "result_rows": [int(r.shape[0]) for r in results],
                        "per_query_scan_ms": [round(float(x), 4) for x in scan_ms.mean(axis=0)]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "kernel": "scan_kernel (K4 ssb_scan_groupby)",
                          "algorithmic_bytes_per_launch": [int(b) for b in bytes_per_launch],
                          "peak_source": peak_src},
@@ -395,7 +395,7 @@ def ncu_traffic():
             v, u = r[k].split()
             b += float(v) * unit[u]
         tot.append(b)
-    return {"bytes_per_launch_mean": sum(tot) / len(tot), "source": os.path.relpath(files[-1], ROOT)}
+    return sum(tot) / len(tot), os.path.relpath(files[-1], ROOT)
 
 
 def _fact_cols(q):

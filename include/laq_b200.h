@@ -121,6 +121,18 @@ int laq_star_join(laq_ctx* ctx, int32_t n_links, const int64_t* const* d_fks, in
 int laq_dense_matmul(laq_ctx* ctx, const double* d_a, int64_t m, int64_t k, const double* d_b,
                      int64_t n, double* d_c);
 
+/* spmm_dense (matrix.cpp:125-139) for a general CSR (rows x b_rows) times a
+ * dense b_rows x n: each output is the row's entries in CSR order, each product
+ * separately rounded (bit-identical).  Used for non-one-hot row/column maps. */
+int laq_spmm_dense(laq_ctx* ctx, const int64_t* d_row_ptr, const int64_t* d_col_idx, const double* d_values,
+                   int64_t rows, const double* d_b, int64_t b_rows, int64_t n, double* d_out);
+
+/* materialize's column placement (laqops.cpp:364-371): for each ColumnMap entry
+ * (src col, tgt col, v): d_dst[r, tgt] += v * d_src[r, src] (d_dst is rows x k). */
+int laq_place_columns(laq_ctx* ctx, const double* d_src, int64_t rows, int64_t src_cols,
+                      const int64_t* h_src_col, const int64_t* h_tgt_col, const double* h_val,
+                      int64_t nnz, int64_t k, double* d_dst);
+
 /* prefuse_linear (fusion.cpp:50-62) + linear_partial (fusion.cpp:31-36):
  * P_j = B_j * (M_j * L) where M_j is the placement of dim j's k_j columns into
  * the global width k (h_placements[j][c] = global column of local column c).

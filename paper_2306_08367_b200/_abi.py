@@ -59,6 +59,8 @@ _SIGS = {
     "laq_mm_join": (C.c_int, [vp, vp, i64, vp, i64, vp, vp, i64, i64p]),
     "laq_star_join": (C.c_int, [vp, i32, vp, i64, vp, i64p, vp, vp, i64p]),
     "laq_dense_matmul": (C.c_int, [vp, vp, i64, i64, vp, i64, vp]),
+    "laq_spmm_dense": (C.c_int, [vp, vp, vp, vp, i64, vp, i64, i64, vp]),
+    "laq_place_columns": (C.c_int, [vp, vp, i64, i64, i64p, i64p, f64p, i64, i64, vp]),
     "laq_prefuse_linear": (C.c_int, [vp, i32, vp, i64p, i64p, vp, vp, i64, i64, vp]),
     "laq_apply_fused_linear": (C.c_int, [vp, i32, vp, i64, vp, i64p, i64, vp]),
     "laq_materialize": (C.c_int, [vp, i32, vp, i64, vp, i64p, i64p, vp, i64, vp]),

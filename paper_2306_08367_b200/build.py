@@ -74,10 +74,18 @@ def build_oracle():
         _run(["make", "-s", "-j8", "-C", os.path.join(ROOT, "oracle")])
 
 
+def build_integration():
+    """The reference's operator API + its own test binaries over the C-ABI
+    (integration/Makefile; needs the reference headers, so only here)."""
+    if os.path.isdir("/root/reference/proj/src"):
+        _run(["make", "-s", "-j8", "-C", os.path.join(ROOT, "integration")])
+
+
 def build_all(force=False):
     build_gen(force)
     build_cuda(force)
     build_oracle()
+    build_integration()
 
 
 if __name__ == "__main__":

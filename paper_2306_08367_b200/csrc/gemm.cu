@@ -95,6 +95,31 @@ __global__ void gather_rows(const double* __restrict__ L, int64_t l, const int32
   }
 }
 
+// spmm_dense (matrix.cpp:125-139) for a general CSR: out(i, j) = sum over the
+// row's entries, in CSR order, of v * B(col, j) (separately rounded).
+__global__ void csr_spmm_dense_kernel(const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ col_idx,
+                                      const double* __restrict__ vals, int64_t rows, const double* __restrict__ B,
+                                      int64_t n, double* __restrict__ out) {
+  const int64_t total = rows * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e - i * n;
+    double acc = 0.0;
+    for (int64_t t = row_ptr[i]; t < row_ptr[i + 1]; ++t) acc = __dadd_rn(acc, __dmul_rn(vals[t], B[col_idx[t] * n + j]));
+    out[e] = acc;
+  }
+}
+
+// materialize's column placement (laqops.cpp:364-371): dst(r, tgt) += v * src(r, src_col).
+__global__ void place_columns_kernel(const double* __restrict__ src, int64_t rows, int64_t src_cols,
+                                     const int64_t* __restrict__ sc, const int64_t* __restrict__ tc,
+                                     const double* __restrict__ v, int64_t nnz, int64_t k, double* __restrict__ dst) {
+  const int64_t total = rows * nnz;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / nnz, q = e - r * nnz;
+    dst[r * k + tc[q]] = __dadd_rn(dst[r * k + tc[q]], __dmul_rn(v[q], src[r * src_cols + sc[q]]));
+  }
+}
+
 }  // namespace
 
 void dgemm_seq(laq_ctx* ctx, const double* A, int64_t m, int64_t k, const double* B, int64_t n, double* C) {
@@ -123,6 +148,33 @@ int laq_dense_matmul(laq_ctx* ctx, const double* a, int64_t m, int64_t k, const 
   return guard(ctx, [&] {
     if (m < 0 || k < 0 || n < 0) fail(LAQ_ERR_SHAPE, "dense_matmul: negative dimension");
     dgemm_seq(ctx, a, m, k, b, n, c);
+  });
+}
+
+int laq_spmm_dense(laq_ctx* ctx, const int64_t* d_row_ptr, const int64_t* d_col_idx, const double* d_values,
+                   int64_t rows, const double* d_b, int64_t b_rows, int64_t n, double* d_out) {
+  return guard(ctx, [&] {
+    (void)b_rows;
+    if (rows == 0 || n == 0) return;
+    csr_spmm_dense_kernel<<<grid_for(rows * n, 256, ctx->sm_count * 16), 256, 0, ctx->stream>>>(
+        d_row_ptr, d_col_idx, d_values, rows, d_b, n, d_out);
+    launched(ctx);
+  });
+}
+
+int laq_place_columns(laq_ctx* ctx, const double* d_src, int64_t rows, int64_t src_cols, const int64_t* h_src_col,
+                      const int64_t* h_tgt_col, const double* h_val, int64_t nnz, int64_t k, double* d_dst) {
+  return guard(ctx, [&] {
+    if (rows == 0 || nnz == 0) return;
+    DevBuf<int64_t> sc(ctx, nnz), tc(ctx, nnz);
+    DevBuf<double> v(ctx, nnz);
+    LAQ_CUDA(cudaMemcpyAsync(sc.get(), h_src_col, nnz * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+    LAQ_CUDA(cudaMemcpyAsync(tc.get(), h_tgt_col, nnz * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+    LAQ_CUDA(cudaMemcpyAsync(v.get(), h_val, nnz * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    place_columns_kernel<<<grid_for(rows * nnz, 256, ctx->sm_count * 16), 256, 0, ctx->stream>>>(
+        d_src, rows, src_cols, sc.get(), tc.get(), v.get(), nnz, k, d_dst);
+    launched(ctx);
+    sync(ctx);  // host triplets must outlive the copies
   });
 }
 
