@@ -184,6 +184,36 @@ int laq_probe_fused_predict(laq_ctx* ctx, const laq_probe* probe, const int32_t*
                             double* d_out, int64_t* d_survivors, int64_t* d_nnz);
 int laq_probe_destroy(laq_probe* probe);
 
+/* Star join over prebuilt probe tables, compacted to int32 row maps
+ * (multiway_star_join, laqops.cpp:233-319, for the tensor-core operators):
+ * d_rows[j][m] = row of dim j matched by the m-th surviving fact row (ascending);
+ * survivor count to d_nnz (device).  No host synchronisation. */
+int laq_probe_join_rows(laq_ctx* ctx, const laq_probe* probe, const int32_t* const* d_fks, int64_t n_fact,
+                        int32_t* const* d_rows, int64_t* d_survivors, int64_t* d_nnz);
+
+/* ---- tensor-core FFN over a star join (BASELINE configs[2]) -------------
+ * Y = ReLU(T W1) W2 with T = materialize(I_j, B_j, placements) (laqops.cpp:338-374)
+ * and the products of predict_linear / dense_matmul (mlops.cpp:248-250,
+ * matrix.cpp:158-174); the reference has no FFN, cfg3 composes these.  T is
+ * gathered tile by tile into shared memory, never written.  fp64 inputs are
+ * stored as a bf16x3 split; tcgen05 MMAs accumulate fp32 in TMEM (SURVEY.md
+ * Appendix B: condition-aware 1e-5).  Output fp32 [rows x l].
+ * Limits: 1..4 dims, sum of 8-padded dim widths <= 128, h multiple of 32 in
+ * [32,256], l in [1,8] (LAQ_ERR_UNSUPPORTED otherwise); placements as in
+ * laq_prefuse_linear (LAQ_ERR_MAPPING / LAQ_ERR_SHAPE). */
+typedef struct laq_ffn laq_ffn;
+int laq_ffn_create(laq_ctx* ctx, int32_t n_dims, const double* const* d_dims, const int64_t* h_dim_rows,
+                   const int64_t* h_dim_cols, const int64_t* const* h_placements, int64_t k, const double* d_W1,
+                   int64_t h, const double* d_W2, int64_t l, laq_ffn** out);
+/* Over explicit join row maps (one row of every dim per target row). Async. */
+int laq_ffn_predict_rows(laq_ctx* ctx, const laq_ffn* f, const int32_t* const* d_rows, int64_t rows, float* d_out);
+/* Join + FFN: probes the fact keys inside the kernel; if any fact row misses a
+ * dimension, compacts with laq_probe_join_rows and reruns on the survivors.
+ * Y[m] for the m-th surviving fact row (ascending).  Synchronises (*h_nnz). */
+int laq_ffn_predict_star(laq_ctx* ctx, const laq_ffn* f, const laq_probe* probe, const int32_t* const* d_fks,
+                         int64_t n_fact, float* d_out, int64_t* d_survivors, int64_t* h_nnz);
+int laq_ffn_destroy(laq_ffn* f);
+
 /* ---- aggregate-MM (laqops.hpp:112-166) --------------------------------- */
 
 /* groupby_sum_single (laqops.cpp:376-413): join R and S on key, sum R's values

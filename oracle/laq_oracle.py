@@ -193,6 +193,26 @@ def predict_linear(T, W):
     return dense_matmul(T, W)
 
 
+def ffn_predict(idx, dims, placements, k, W1, W2, exact_order=False):
+    """cfg3: the reference has no FFN; it is the composition
+    Y = predict_linear(ReLU(predict_linear(materialize(...), W1)), W2) of pinned
+    functions (laqops.cpp:338-374, mlops.cpp:248-250) with an elementwise ReLU.
+    Returns (Y, bound) where bound[m, c] is the condition-aware error scale
+        sum_n |W2[n,c]| * sum_k |T[m,k] W1[k,n]|  +  sum_n |ReLU(H[m,n]) W2[n,c]|
+    used for the 1e-5 tolerance.  exact_order=True uses
+    dense_matmul's sequential-k order (small cases); otherwise BLAS (the
+    association difference, ~1e-16 relative, is far below the tolerance)."""
+    T = materialize(idx, dims, placements, k)
+    W1 = np.asarray(W1, np.float64)
+    W2 = np.asarray(W2, np.float64)
+    mm = dense_matmul if exact_order else (lambda a, b: a @ b)
+    H = mm(T, W1)
+    R = np.maximum(H, 0.0)
+    Y = mm(R, W2)
+    bound = (np.abs(T) @ np.abs(W1)) @ np.abs(W2) + R @ np.abs(W2)
+    return Y, bound
+
+
 # ---------------------------------------------------------------------------
 # aggregation (laqops.cpp:376-478)
 # ---------------------------------------------------------------------------

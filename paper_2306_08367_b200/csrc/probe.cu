@@ -432,6 +432,12 @@ struct laq_probe {
 };
 
 namespace laq {
+int probe_links(const laq_probe* p) { return p->n_links; }
+ProbeView probe_view(const laq_probe* p, int j) { return p->probes[j].view(); }
+}  // namespace laq
+
+
+namespace laq {
 namespace {
 
 // Slot-ordered partials + existence bitmaps for every link (predict_slot.cuh).
@@ -598,6 +604,25 @@ int laq_probe_build(laq_ctx* ctx, int32_t n_links, const int32_t* const* d_pks, 
       throw;
     }
     *out = p;
+  });
+}
+
+int laq_probe_join_rows(laq_ctx* ctx, const laq_probe* probe, const int32_t* const* d_fks, int64_t n_fact,
+                        int32_t* const* d_rows, int64_t* d_survivors, int64_t* d_nnz) {
+  return guard(ctx, [&] {
+    auto* p = const_cast<laq_probe*>(probe);
+    StarArgs<int32_t> a{};
+    a.n_links = p->n_links;
+    a.n = n_fact;
+    for (int j = 0; j < p->n_links; ++j) {
+      a.fk[j] = d_fks[j];
+      a.probe[j] = p->probes[j].view();
+      a.rows32[j] = d_rows[j];
+    }
+    a.survivors = d_survivors;
+    a.nnz = d_nnz;
+    a.err = p->err.get();
+    run_star(ctx, a, p->scratch, false);
   });
 }
 

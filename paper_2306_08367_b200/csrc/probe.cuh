@@ -62,6 +62,10 @@ struct Probe {
 // Build a probe over n primary keys (int64 or int32 device array).
 // Throws DomainError on a negative key and DuplicateKeyError (with `what`) on
 // a duplicate (laqops.cpp:252-254).
+// Views into a laq_probe (defined in probe.cu) for other kernels (ffn.cu).
+int probe_links(const laq_probe* p);
+ProbeView probe_view(const laq_probe* p, int j);
+
 void build_probe(laq_ctx* ctx, const int64_t* d_pk64, const int32_t* d_pk32, int64_t n, Probe& out,
                  const std::string& what);
 
