@@ -14,18 +14,34 @@
 // with fp32 accumulation in TMEM, then ReLU and layer 2 in fp32 on the CUDA cores.
 // Accuracy is judged condition-aware at 1e-5 (tests/test_gpu_ffn.py).
 //
-// Kernel structure (persistent, one CTA per SM, 288 threads):
-//   warps 0-3  epilogue: tcgen05.ld the 128 x h accumulator (thread = row),
-//              ReLU, dot with W2 (shared memory), coalesced fp32 stores;
-//   warps 4-7  gather producers: resolve dim rows (row maps, or fact keys through
-//              the probe tables) two tiles ahead, then 16-byte cp.async of the
-//              hi/lo feature chunks into the K-major SW128 stage, cp.async.wait +
-//              proxy fence + mbarrier arrive;
-//   warp 8     TMEM owner + MMA issuer (one elected lane): 3 x K/16 tcgen05.mma
-//              per tile into one of two TMEM accumulators, tcgen05.commit frees
-//              the stage and hands the accumulator to the epilogue.
-// W1 (hi/lo, K-major) stays resident in shared memory for the whole kernel.
+// HBM layout: every dimension's features are cut into blocks of 32 columns; block b
+// is a bf16 table [rows_j x 64] whose row is (hi[32] | lo[32]) -- exactly one
+// 128-byte line, the unit one TMA gather moves.  W1 uses the same block layout
+// (W1^T rows = hidden units), so inside a 128-byte swizzled smem row the hi
+// operand sits at byte 0 and the lo operand at byte 64.
+//
+// Kernel structure (persistent, one CTA per SM, 416 threads):
+//   warps 0-7   epilogue: warp w reads TMEM lanes 32(w%4).. (thread = tile row) and
+//               every other 32-column chunk of the 128 x h accumulator (tcgen05.ld),
+//               ReLU, dot with W2 (broadcast shared loads, 4 independent FMA
+//               chains); the two column halves meet through shared memory and a
+//               named barrier; coalesced fp32 stores;
+//   warps 8-11  gather producers: each lane resolves one row (row maps, or fact
+//               keys through the probe tables, two tiles ahead); then every warp
+//               instruction moves 4 feature lines (4 rows x 128 B) with 16-byte
+//               cp.async into the SW128 stage; cp.async.mbarrier.arrive.noinc
+//               signals the stage when the thread's copies land (no blocking);
+//   warp 12     TMEM owner + MMA issuer (one lane): 3 x K/16 tcgen05.mma per tile
+//               into one of two TMEM accumulators; tcgen05.commit frees the stage
+//               and hands the accumulator to the epilogue.
+// Measured alternative (not used): TMA tile::gather4 (4 rows per instruction)
+// was issue-bound at ~1.5 TB/s on B200 because the per-lane row indices force
+// the uniform-datapath TMA instruction into a serialised per-lane loop.
+// W1 (hi/lo) stays resident in shared memory for the whole kernel.
 #include <algorithm>
+#include <cstdlib>
+#include <string>
+#include <utility>
 #include <vector>
 
 #include "probe.cuh"
@@ -35,69 +51,73 @@ namespace laq {
 namespace ffn {
 
 constexpr int kRows = 128;  // tile rows = UMMA M = TMEM lanes
-constexpr int kEpiWarps = 4, kProdWarps = 4;
-constexpr int kThreads = (kEpiWarps + kProdWarps + 1) * 32;
+constexpr int kEpiWarps = 8;
+constexpr int kProdWarps = 4, kProdWarp0 = 8, kMmaWarp = 12;
+constexpr int kThreads = 13 * 32;
 constexpr int kMaxDims = 4;
+constexpr int kMaxBlocks = 8;  // 32-feature blocks (K <= 256)
 constexpr int kMaxL = 8;
-constexpr int kProdThreads = kProdWarps * 32;
+constexpr uint32_t kBlockBytes = kRows * 128u;  // one feature block of a stage
 
 struct Args {
+  const __nv_bfloat16* block[kMaxBlocks];  // block b: [rows x 64] bf16 = (hi32 | lo32)
+  int n_blocks;
+  int block_dim[kMaxBlocks];    // dimension owning block b
+  int block_steps[kMaxBlocks];  // 16-feature MMA steps in block b (1 or 2)
   int n_dims;
-  int64_t n;  // rows processed (fact rows in probe mode, join rows otherwise)
+  int64_t n;                     // rows processed (fact rows in probe mode, join rows otherwise)
   const int32_t* idx[kMaxDims];  // row maps, or fact keys (probe mode)
   ProbeView probe[kMaxDims];
   int probe_mode;
-  const __nv_bfloat16* hi[kMaxDims];  // [rows_j x 8*chunks_j] row-major
-  const __nv_bfloat16* lo[kMaxDims];
-  int chunks[kMaxDims];  // 16-byte chunks per dim row
-  int chunk0[kMaxDims];  // first global chunk of dim j in the T row
-  int C;                 // chunks per T row (K_pad / 8)
-  int KB;                // 64-wide K blocks
-  int ksteps;            // K_pad / 16
-  int N;                 // hidden width (UMMA N)
+  int N;                    // hidden width (UMMA N)
   int l;
-  const __nv_bfloat16* w1hi;  // [N x K_pad] (W1^T, K-major)
-  const __nv_bfloat16* w1lo;
-  const float* w2;  // [N x l]
-  float* y;         // [n x l]
+  const __nv_bfloat16* w1;  // [n_blocks][N][64] (hi32 | lo32)
+  const float* w2;          // [N x LP] (l padded to a power of two with zeros)
+  float* y;                 // [n x l]
   int stages;
   int64_t n_tiles;
   unsigned long long* miss;  // probe mode: rows missing some dimension
+  int diag;  // A/B diagnostics: 1 no gathers, 2 no MMAs, 3 no gathers + no epilogue, 4 no gathers + TMEM loads only
 };
 
 struct Smem {  // offsets into the 1024-aligned dynamic buffer
   uint32_t b, a, w2, bars, stage_bytes;
 };
 
-__host__ __device__ inline Smem layout(int KB, int N, int l, int S) {
+__host__ __device__ inline Smem layout(int nb, int N, int lp, int S) {
   Smem m;
   m.b = 0;
-  m.a = static_cast<uint32_t>(KB) * 2u * N * 128u;
-  m.stage_bytes = static_cast<uint32_t>(KB) * 2u * kRows * 128u;
+  m.a = static_cast<uint32_t>(nb) * N * 128u;
+  m.stage_bytes = static_cast<uint32_t>(nb) * kBlockBytes;
   m.w2 = m.a + S * m.stage_bytes;
-  m.bars = (m.w2 + N * l * 4u + 15u) & ~15u;
+  m.bars = (m.w2 + N * lp * 4u + 15u) & ~15u;
   return m;
 }
-__host__ __device__ inline uint32_t smem_bytes(int KB, int N, int l, int S) {
+__host__ __device__ inline uint32_t smem_bytes(int nb, int N, int lp, int S) {
   // barriers: full[S], empty[S], acc_full[2], acc_empty[2] + tmem slot; +1 KB alignment slack
-  return layout(KB, N, l, S).bars + (2 * S + 4) * 8 + 16 + 1024;
+  return layout(nb, N, lp, S).bars + (2 * S + 4) * 8 + 16 + 1024;
 }
 
-// Resolve dim rows of this producer thread's row for one tile (row maps or probe).
-__device__ __forceinline__ void load_keys(const Args& a, int64_t tile, int lane_row, int32_t (&k)[kMaxDims]) {
-  int64_t r = tile * kRows + lane_row;
-  if (r >= a.n) r = a.n - 1;
+// Key (or row-map entry) of row `r` of `tile` for every dim, clamped to n-1.
+__device__ __forceinline__ void load_keys(const Args& a, int64_t tile, int r, int32_t (&k)[kMaxDims]) {
+  int64_t g = tile * kRows + r;
+  if (g >= a.n) g = a.n - 1;
 #pragma unroll
   for (int j = 0; j < kMaxDims; ++j)
-    if (j < a.n_dims) k[j] = __ldg(a.idx[j] + r);
+    if (j < a.n_dims) k[j] = __ldg(a.idx[j] + g);
+}
+__device__ __forceinline__ void resolve(const Args& a, const int32_t (&k)[kMaxDims], int32_t (&r)[kMaxDims]) {
+#pragma unroll
+  for (int j = 0; j < kMaxDims; ++j)
+    if (j < a.n_dims) r[j] = a.probe_mode ? a.probe[j].row(k[j]) : k[j];
 }
 
-template <int kLag>
-__global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const Args a) {
+template <int LP>
+__global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant__ Args a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int S = a.stages, KB = a.KB, N = a.N, l = a.l;
-  const Smem L = layout(KB, N, l, S);
+  const int S = a.stages, NB = a.n_blocks, N = a.N, l = a.l;
+  const Smem L = layout(NB, N, LP, S);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
   uint64_t* empty = full + S;
   uint64_t* acc_full = empty + S;
@@ -108,21 +128,17 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const Args a) {
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // ---- one-time setup: W1 (hi, lo) -> SW128 K-major blocks; W2 -> smem --------
-  {
-    const int C = a.C;
-    const int total = N * C * 2;
-    for (int e = threadIdx.x; e < total; e += kThreads) {
-      const int n = e / (2 * C), rem = e - n * 2 * C, p = rem >= C, c = rem - p * C;
-      const uint4 v = *reinterpret_cast<const uint4*>((p ? a.w1lo : a.w1hi) + static_cast<int64_t>(n) * C * 8 + c * 8);
-      *reinterpret_cast<uint4*>(smem + L.b + ((c >> 3) * 2 + p) * N * 128u + tc::sw128_off(n, c & 7)) = v;
-    }
-    for (int e = threadIdx.x; e < N * l; e += kThreads) s_w2[e] = a.w2[e];
+  // ---- one-time setup: W1 blocks -> SW128 K-major rows; W2 -> smem ----------------
+  for (int e = threadIdx.x; e < NB * N * 8; e += kThreads) {
+    const int c = e & 7, row = e >> 3;  // row = b * N + n
+    const uint4 v = *reinterpret_cast<const uint4*>(a.w1 + static_cast<int64_t>(row) * 64 + c * 8);
+    *reinterpret_cast<uint4*>(smem + L.b + tc::sw128_off(row, c)) = v;  // N is a multiple of 8
   }
-  if (warp == 8) {
+  for (int e = threadIdx.x; e < N * LP; e += kThreads) s_w2[e] = a.w2[e];
+  if (warp == kMmaWarp) {
     if (lane == 0) {
       for (int s = 0; s < S; ++s) {
-        tc::mbar_init(&full[s], kProdThreads);
+        tc::mbar_init(&full[s], kProdWarps * 32);
         tc::mbar_init(&empty[s], 1);
       }
       for (int b = 0; b < 2; ++b) {
@@ -140,26 +156,21 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const Args a) {
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp >= kEpiWarps && warp < kEpiWarps + kProdWarps) {
-    // ================= gather producers =================
-    const int pw = warp - kEpiWarps;  // rows 32*pw .. 32*pw+31 of every tile
-    const int C = a.C, items = 32 * 2 * C;
+  if (warp >= kProdWarp0 && warp < kProdWarp0 + kProdWarps) {
+    // ================= cp.async gather producers =================
+    const int pw = warp - kProdWarp0;  // tile rows 32*pw .. 32*pw+31
     __shared__ int32_t s_rows[kProdWarps][kMaxDims][32];
     int32_t k1[kMaxDims] = {}, k2[kMaxDims] = {}, r1[kMaxDims] = {};
     int64_t tile = blockIdx.x;
     const int64_t step = gridDim.x;
     unsigned long long misses = 0;
-    // prologue: keys for tiles 0 and 1, rows for tile 0
+    // prologue: keys of the first two tiles, rows of the first
     if (tile < a.n_tiles) load_keys(a, tile, 32 * pw + lane, k1);
     if (tile + step < a.n_tiles) load_keys(a, tile + step, 32 * pw + lane, k2);
-#pragma unroll
-    for (int j = 0; j < kMaxDims; ++j)
-      if (j < a.n_dims) r1[j] = a.probe_mode ? a.probe[j].row(k1[j]) : k1[j];
-    int it = 0;
-    for (; tile < a.n_tiles; tile += step, ++it) {
+    resolve(a, k1, r1);
+    const int sub = lane >> 3, chunk = lane & 7;  // 4 rows x 8 16-byte chunks per instruction
+    for (int it = 0; tile < a.n_tiles; tile += step, ++it) {
       const int s = it % S;
-      const uint32_t ph = (it / S) & 1;
-      // rows of this tile (resolved last iteration) -> shared
       const bool live = tile * kRows + 32 * pw + lane < a.n;
 #pragma unroll
       for (int j = 0; j < kMaxDims; ++j)
@@ -171,43 +182,34 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const Args a) {
           }
           s_rows[pw][j][lane] = r;
         }
-      // look ahead: rows of tile+1 (keys loaded last iteration), keys of tile+2
-#pragma unroll
-      for (int j = 0; j < kMaxDims; ++j)
-        if (j < a.n_dims) r1[j] = a.probe_mode ? a.probe[j].row(k2[j]) : k2[j];
+      // look ahead: rows of the next tile (keys loaded an iteration ago), keys two ahead
+      resolve(a, k2, r1);
       if (tile + 2 * step < a.n_tiles) load_keys(a, tile + 2 * step, 32 * pw + lane, k2);
       __syncwarp();
 
-      tc::mbar_wait(&empty[s], ph ^ 1);
-      const uint32_t abase = sbase + L.a + s * L.stage_bytes;
-      for (int e = lane; e < items; e += 32) {
-        const int rl = e / (2 * C), rem = e - rl * 2 * C, p = rem >= C, c = rem - p * C;
-        int j = 0;
+      tc::mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+      if (a.diag != 1 && a.diag < 3) {
+        const uint32_t abase = sbase + L.a + s * L.stage_bytes;
+        for (int b = 0; b < NB; ++b) {
+          const __nv_bfloat16* base = a.block[b] + chunk * 8;
+          const int j = a.block_dim[b];
+          const uint32_t dbase = abase + b * kBlockBytes;
 #pragma unroll
-        for (int q = 1; q < kMaxDims; ++q)
-          if (q < a.n_dims && c >= a.chunk0[q]) j = q;
-        const int cj = c - a.chunk0[j];
-        const int64_t drow = s_rows[pw][j][rl];
-        const __nv_bfloat16* src = (p ? a.lo[j] : a.hi[j]) + drow * (a.chunks[j] * 8) + cj * 8;
-        const int r = 32 * pw + rl;
-        tc::cp_async16(abase + ((c >> 3) * 2 + p) * (kRows * 128u) + tc::sw128_off(r, c & 7), src);
+          for (int q = 0; q < 8; ++q) {
+            const int rl = 4 * q + sub, r = 32 * pw + rl;
+            const int64_t drow = s_rows[pw][j][rl];
+            tc::cp_async16(dbase + tc::sw128_off(r, chunk), base + drow * 64);
+          }
+        }
       }
-      tc::cp_async_commit();
-      if (it >= kLag) {
-        tc::cp_async_wait<kLag>();
-        tc::fence_proxy_async();
-        tc::mbar_arrive(&full[(it - kLag) % S]);
-      }
+      tc::cp_async_arrive_noinc(&full[s]);
       __syncwarp();  // s_rows reuse
     }
-    tc::cp_async_wait<0>();
-    tc::fence_proxy_async();
-    for (int t = std::max(0, it - kLag); t < it; ++t) tc::mbar_arrive(&full[t % S]);
     if (a.probe_mode) {
       for (int o = 16; o; o >>= 1) misses += __shfl_xor_sync(0xffffffffu, misses, o);
       if (lane == 0 && misses) atomicAdd(a.miss, misses);
     }
-  } else if (warp == kEpiWarps + kProdWarps) {
+  } else if (warp == kMmaWarp) {
     // ================= MMA issuer =================
     if (lane == 0) {
       const uint32_t idesc = tc::idesc_bf16_f32(kRows, N);
@@ -216,21 +218,21 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const Args a) {
         const int s = it % S, ab = it & 1;
         tc::mbar_wait(&acc_empty[ab], ((it >> 1) & 1) ^ 1);
         tc::mbar_wait(&full[s], (it / S) & 1);
+        tc::fence_proxy_async();  // cp.async (generic proxy) writes -> tensor core reads
         tc::tc_fence_after();
         const uint32_t d = tmem + ab * N;
         const uint32_t abase = sbase + L.a + s * L.stage_bytes;
         uint32_t acc = 0;
 #pragma unroll
-        for (int pr = 0; pr < 3; ++pr) {  // hi.hi, hi.lo, lo.hi
-          const int pa = pr == 2, pb = pr == 1;
-          for (int ks = 0; ks < a.ksteps; ++ks) {
-            const int kb = ks >> 2;
-            const uint32_t koff = (ks & 3) * 32u;
-            const uint64_t ad = tc::sdesc_sw128(abase + (kb * 2 + pa) * (kRows * 128u) + koff);
-            const uint64_t bd = tc::sdesc_sw128(sbase + L.b + (kb * 2 + pb) * (N * 128u) + koff);
-            tc::mma_bf16(d, ad, bd, idesc, acc);
-            acc = 1;
-          }
+        for (int pr = 0; pr < (a.diag == 2 ? 0 : 3); ++pr) {  // hi.hi, hi.lo, lo.hi
+          const uint32_t pa = pr == 2 ? 64u : 0u, pb = pr == 1 ? 64u : 0u;
+          for (int b = 0; b < NB; ++b)
+            for (int st = 0; st < a.block_steps[b]; ++st) {
+              const uint64_t ad = tc::sdesc_sw128(abase + b * kBlockBytes + pa + st * 32u);
+              const uint64_t bd = tc::sdesc_sw128(sbase + L.b + b * (N * 128u) + pb + st * 32u);
+              tc::mma_bf16(d, ad, bd, idesc, acc);
+              acc = 1;
+            }
         }
         tc::mma_commit(&empty[s]);
         tc::mma_commit(&acc_full[ab]);
@@ -238,78 +240,114 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const Args a) {
     }
     __syncwarp();
   } else {
-    // ================= epilogue (warps 0-3) =================
+    // ================= epilogue (warps 0-7) =================
+    __shared__ float s_red[2][4][32][kMaxL];
+    const int q = warp & 3, hh = warp >> 2;  // TMEM lane group, column half
+    const uint32_t w2a = tc::smem_u32(s_w2);
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x, ++it) {
       const int ab = it & 1;
       tc::mbar_wait(&acc_full[ab], (it >> 1) & 1);
       tc::tc_fence_after();
-      float y[kMaxL];
+      float y[4][LP];  // 4 independent accumulation chains
 #pragma unroll
-      for (int c = 0; c < kMaxL; ++c) y[c] = 0.f;
-      const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * warp) << 16) + ab * N;
-      for (int c0 = 0; c0 < N; c0 += 32) {
-        uint32_t v[32];
-        tc::tmem_ld32(t0 + c0, v);
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int c = 0; c < LP; ++c) y[u][c] = 0.f;
+      const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * q) << 16) + ab * N;
+      // this warp's chunks: c0 = 32*hh, 32*hh + 64, ... (two per TMEM wait)
+      for (int c0 = 32 * hh; c0 < (a.diag >= 3 ? (a.diag == 3 ? 0 : N) : N); c0 += 128) {
+        uint32_t v[64];
+        const bool two = c0 + 64 < N;
+        tc::tmem_ld32(t0 + c0, *reinterpret_cast<uint32_t(*)[32]>(v));
+        if (two) tc::tmem_ld32(t0 + c0 + 64, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
         tc::tmem_ld_wait();
+        if (a.diag == 4) {
+          y[0][0] += __uint_as_float(v[0] ^ v[17] ^ v[33] ^ v[63]);
+          continue;
+        }
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float h = fmaxf(__uint_as_float(v[i]), 0.f);
-          const float* w = s_w2 + (c0 + i) * l;
+        for (int i0 = 0; i0 < 64; i0 += 4) {
+          if (i0 < 32 || two) {
+            const int col = c0 + (i0 < 32 ? i0 : i0 + 32);
+            float w[4 * LP];  // W2 rows col .. col+3 (broadcast 16-byte shared loads)
 #pragma unroll
-          for (int c = 0; c < kMaxL; ++c)
-            if (c < l) y[c] = fmaf(h, w[c], y[c]);
+            for (int qq = 0; qq < LP; ++qq) {
+              const float4 t = tc::lds128(w2a + (col * LP + 4 * qq) * 4u);
+              w[4 * qq] = t.x; w[4 * qq + 1] = t.y; w[4 * qq + 2] = t.z; w[4 * qq + 3] = t.w;
+            }
+#pragma unroll
+            for (int ii = 0; ii < 4; ++ii) {
+              const float h = fmaxf(__uint_as_float(v[i0 + ii]), 0.f);
+#pragma unroll
+              for (int c = 0; c < LP; ++c) y[ii][c] = fmaf(h, w[ii * LP + c], y[ii][c]);
+            }
+          }
         }
       }
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&acc_empty[ab]);
-      const int64_t row = tile * kRows + 32 * warp + lane;
-      if (row < a.n) {
+      float yy[LP];
 #pragma unroll
-        for (int c = 0; c < kMaxL; ++c)
-          if (c < l) __stcs(a.y + row * l + c, y[c]);
+      for (int c = 0; c < LP; ++c) yy[c] = (y[0][c] + y[1][c]) + (y[2][c] + y[3][c]);
+      if (hh == 1) {
+#pragma unroll
+        for (int c = 0; c < LP; ++c) s_red[ab][q][lane][c] = yy[c];
+      }
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");  // the two warps of lane group q
+      if (hh == 0) {
+        const int64_t row = tile * kRows + 32 * q + lane;
+        if (row < a.n) {
+#pragma unroll
+          for (int c = 0; c < LP; ++c)
+            if (c < l) __stcs(a.y + row * l + c, yy[c] + s_red[ab][q][lane][c]);
+        }
       }
     }
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 8) {
+  if (warp == kMmaWarp) {
     tc::tc_fence_after();
     tc::tmem_dealloc<512>(tmem);
   }
 }
 
 // ---- layout preparation --------------------------------------------------------
-// dim table B_j (rows x cols fp64) -> hi/lo bf16 [rows x kpad], zero padded.
-__global__ void split_table_kernel(const double* __restrict__ B, int64_t rows, int64_t cols, int64_t kpad,
-                                   __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo) {
-  const int64_t total = rows * kpad;
+// Feature block: columns [f0, f0 + 32) of B_j (rows x cols fp64) -> bf16
+// [rows x 64] = (hi[32] | lo[32]), zero padded past `cols`.
+__global__ void split_block_kernel(const double* __restrict__ B, int64_t rows, int64_t cols, int64_t f0,
+                                   __nv_bfloat16* __restrict__ out) {
+  const int64_t total = rows * 32;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e / kpad, c = e - r * kpad;
+    const int64_t r = e >> 5, c = e & 31;
     __nv_bfloat16 h = __float2bfloat16(0.f), q = __float2bfloat16(0.f);
-    if (c < cols) tc::split_bf16(B[r * cols + c], h, q);
-    hi[e] = h;
-    lo[e] = q;
+    if (f0 + c < cols) tc::split_bf16(B[r * cols + f0 + c], h, q);
+    out[r * 64 + c] = h;
+    out[r * 64 + 32 + c] = q;
   }
 }
-// W1 (k x n fp64, row-major) -> W1^T hi/lo [n x kpad]; T column q holds global
-// feature perm[q] (-1 = padding).
+// W1 (k x n fp64, row-major) -> [n_blocks][n][64]: block b, hidden unit col,
+// (hi | lo) of W1[perm[32 b + c]][col] (perm -1 = padding).
 __global__ void split_w1_kernel(const double* __restrict__ W, int64_t n, const int64_t* __restrict__ perm,
-                                int64_t kpad, __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo) {
-  const int64_t total = n * kpad;
+                                int64_t n_blocks, __nv_bfloat16* __restrict__ out) {
+  const int64_t total = n_blocks * n * 32;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t col = e / kpad, q = e - col * kpad;
+    const int64_t c = e & 31, bc = e >> 5, b = bc / n, col = bc - b * n;
     __nv_bfloat16 h = __float2bfloat16(0.f), o = __float2bfloat16(0.f);
-    const int64_t g = perm[q];
+    const int64_t g = perm[b * 32 + c];
     if (g >= 0) tc::split_bf16(W[g * n + col], h, o);
-    hi[e] = h;
-    lo[e] = o;
+    out[bc * 64 + c] = h;
+    out[bc * 64 + 32 + c] = o;
   }
 }
-__global__ void to_f32_kernel(const double* __restrict__ x, int64_t n, float* __restrict__ y) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
-    y[e] = static_cast<float>(x[e]);
+// W2 (h x l fp64) -> fp32 [h x lp], zero columns l..lp-1.
+__global__ void w2_pad_kernel(const double* __restrict__ x, int64_t h, int64_t l, int64_t lp, float* __restrict__ y) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < h * lp; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / lp, c = e - r * lp;
+    y[e] = c < l ? static_cast<float>(x[r * l + c]) : 0.f;
+  }
 }
 __global__ void iota_kernel(int64_t* __restrict__ out, int64_t n) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
@@ -323,12 +361,12 @@ using namespace laq;
 
 struct laq_ffn {
   int n_dims = 0;
-  int64_t dim_rows[ffn::kMaxDims] = {};
-  int chunks[ffn::kMaxDims] = {}, chunk0[ffn::kMaxDims] = {};
-  int C = 0, KB = 0, ksteps = 0, N = 0, l = 0, stages = 0;
+  int n_blocks = 0;
+  int block_dim[ffn::kMaxBlocks] = {}, block_steps[ffn::kMaxBlocks] = {};
+  int N = 0, l = 0, lp = 1, stages = 0;
   int64_t k = 0;
-  DevMem<__nv_bfloat16> hi[ffn::kMaxDims], lo[ffn::kMaxDims];
-  DevMem<__nv_bfloat16> w1hi, w1lo;
+  DevMem<__nv_bfloat16> blocks[ffn::kMaxBlocks];  // [rows_j x 64] (hi32 | lo32)
+  DevMem<__nv_bfloat16> w1;  // [n_blocks][N][64]
   DevMem<float> w2;
   DevMem<unsigned long long> miss;
 };
@@ -338,39 +376,42 @@ namespace {
 
 ffn::Args make_args(const laq_ffn* f, int64_t n, float* y) {
   ffn::Args a{};
+  a.n_blocks = f->n_blocks;
+  for (int b = 0; b < f->n_blocks; ++b) {
+    a.block[b] = f->blocks[b].get();
+    a.block_dim[b] = f->block_dim[b];
+    a.block_steps[b] = f->block_steps[b];
+  }
   a.n_dims = f->n_dims;
   a.n = n;
-  for (int j = 0; j < f->n_dims; ++j) {
-    a.hi[j] = f->hi[j].get();
-    a.lo[j] = f->lo[j].get();
-    a.chunks[j] = f->chunks[j];
-    a.chunk0[j] = f->chunk0[j];
-  }
-  a.C = f->C;
-  a.KB = f->KB;
-  a.ksteps = f->ksteps;
   a.N = f->N;
   a.l = f->l;
-  a.w1hi = f->w1hi.get();
-  a.w1lo = f->w1lo.get();
+  a.w1 = f->w1.get();
   a.w2 = f->w2.get();
   a.y = y;
   a.stages = f->stages;
   a.n_tiles = (n + ffn::kRows - 1) / ffn::kRows;
   a.miss = f->miss.get();
+  const char* d = std::getenv("LAQ_FFN_DIAG");
+  a.diag = d ? std::atoi(d) : 0;
   return a;
+}
+
+template <int LP>
+void launch_lp(laq_ctx* ctx, const ffn::Args& a, unsigned grid, uint32_t bytes) {
+  LAQ_CUDA(cudaFuncSetAttribute(ffn::ffn_kernel<LP>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  ffn::ffn_kernel<LP><<<grid, ffn::kThreads, bytes, ctx->stream>>>(a);
 }
 
 void launch_ffn(laq_ctx* ctx, const laq_ffn* f, const ffn::Args& a) {
   if (a.n_tiles == 0) return;
-  const uint32_t bytes = ffn::smem_bytes(f->KB, f->N, f->l, f->stages);
+  const uint32_t bytes = ffn::smem_bytes(f->n_blocks, f->N, f->lp, f->stages);
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>(a.n_tiles, ctx->sm_count));
-  if (f->stages >= 4) {
-    LAQ_CUDA(cudaFuncSetAttribute(ffn::ffn_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    ffn::ffn_kernel<2><<<grid, ffn::kThreads, bytes, ctx->stream>>>(a);
-  } else {
-    LAQ_CUDA(cudaFuncSetAttribute(ffn::ffn_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    ffn::ffn_kernel<1><<<grid, ffn::kThreads, bytes, ctx->stream>>>(a);
+  switch (f->lp) {
+    case 1: launch_lp<1>(ctx, a, grid, bytes); break;
+    case 2: launch_lp<2>(ctx, a, grid, bytes); break;
+    case 4: launch_lp<4>(ctx, a, grid, bytes); break;
+    default: launch_lp<8>(ctx, a, grid, bytes); break;
   }
   launched(ctx);
 }
@@ -404,49 +445,50 @@ int laq_ffn_create(laq_ctx* ctx, int32_t n_dims, const double* const* d_dims, co
       f->k = k;
       f->N = static_cast<int>(h);
       f->l = static_cast<int>(l);
-      // T row = concatenation of the dims' (8-padded) feature chunks
+      while (f->lp < f->l) f->lp *= 2;
+      // 32-feature blocks per dimension; W1 rows permuted to the block order
       std::vector<int64_t> perm;
-      for (int j = 0; j < n_dims; ++j) {
-        const int64_t kp = (h_dim_cols[j] + 7) / 8 * 8;
-        f->chunk0[j] = static_cast<int>(perm.size() / 8);
-        f->chunks[j] = static_cast<int>(kp / 8);
-        for (int64_t c = 0; c < kp; ++c) perm.push_back(c < h_dim_cols[j] ? h_placements[j][c] : -1);
-      }
-      while (perm.size() % 16) perm.push_back(-1);
-      const int64_t kpad = static_cast<int64_t>(perm.size());
-      if (kpad > 128) fail(LAQ_ERR_UNSUPPORTED, "ffn: gathered width > 128 features (use materialize + gemm)");
-      f->C = static_cast<int>(kpad / 8);
-      f->KB = (f->C + 7) / 8;
-      f->ksteps = static_cast<int>(kpad / 16);
+      std::vector<std::pair<int, int64_t>> src;  // (dim, first feature)
+      for (int j = 0; j < n_dims; ++j)
+        for (int64_t f0 = 0; f0 < h_dim_cols[j]; f0 += 32) {
+          if (f->n_blocks == ffn::kMaxBlocks)
+            fail(LAQ_ERR_UNSUPPORTED, "ffn: more than 8 32-feature blocks (use materialize + gemm)");
+          const int64_t w = std::min<int64_t>(32, h_dim_cols[j] - f0);
+          f->block_dim[f->n_blocks] = j;
+          f->block_steps[f->n_blocks] = w > 16 ? 2 : 1;
+          ++f->n_blocks;
+          src.emplace_back(j, f0);
+          for (int64_t c = 0; c < 32; ++c) perm.push_back(c < w ? h_placements[j][f0 + c] : -1);
+        }
       int S = 0;
       for (int s = 6; s >= 2; --s)
-        if (ffn::smem_bytes(f->KB, f->N, f->l, s) <= 224 * 1024) { S = s; break; }
+        if (ffn::smem_bytes(f->n_blocks, f->N, f->lp, s) <= 212 * 1024) { S = s; break; }
       if (S == 0) fail(LAQ_ERR_UNSUPPORTED, "ffn: W1 tile does not fit shared memory");
       f->stages = S;
       const int g = ctx->sm_count * 8;
-      for (int j = 0; j < n_dims; ++j) {
-        const int64_t r = h_dim_rows[j], kp = f->chunks[j] * 8;
-        f->dim_rows[j] = r;
-        f->hi[j] = DevMem<__nv_bfloat16>(static_cast<size_t>(std::max<int64_t>(r * kp, 1)));
-        f->lo[j] = DevMem<__nv_bfloat16>(static_cast<size_t>(std::max<int64_t>(r * kp, 1)));
+      for (int b = 0; b < f->n_blocks; ++b) {
+        const int j = src[b].first;
+        const int64_t r = h_dim_rows[j];
+        f->blocks[b] = DevMem<__nv_bfloat16>(static_cast<size_t>(std::max<int64_t>(r, 1) * 64));
         if (r > 0) {
-          ffn::split_table_kernel<<<g, 256, 0, ctx->stream>>>(d_dims[j], r, h_dim_cols[j], kp, f->hi[j].get(),
-                                                              f->lo[j].get());
+          ffn::split_block_kernel<<<g, 256, 0, ctx->stream>>>(d_dims[j], r, h_dim_cols[j], src[b].second,
+                                                              f->blocks[b].get());
           launched(ctx);
+        } else {
+          LAQ_CUDA(cudaMemsetAsync(f->blocks[b].get(), 0, 128, ctx->stream));
         }
       }
       DevBuf<int64_t> dperm(ctx, perm.size());
       LAQ_CUDA(cudaMemcpyAsync(dperm.get(), perm.data(), perm.size() * sizeof(int64_t), cudaMemcpyHostToDevice,
                                ctx->stream));
-      f->w1hi = DevMem<__nv_bfloat16>(static_cast<size_t>(h * kpad));
-      f->w1lo = DevMem<__nv_bfloat16>(static_cast<size_t>(h * kpad));
-      ffn::split_w1_kernel<<<g, 256, 0, ctx->stream>>>(d_W1, h, dperm.get(), kpad, f->w1hi.get(), f->w1lo.get());
+      f->w1 = DevMem<__nv_bfloat16>(static_cast<size_t>(f->n_blocks * h * 64));
+      ffn::split_w1_kernel<<<g, 256, 0, ctx->stream>>>(d_W1, h, dperm.get(), f->n_blocks, f->w1.get());
       launched(ctx);
-      f->w2 = DevMem<float>(static_cast<size_t>(h * l));
-      ffn::to_f32_kernel<<<g, 256, 0, ctx->stream>>>(d_W2, h * l, f->w2.get());
+      f->w2 = DevMem<float>(static_cast<size_t>(h * f->lp));
+      ffn::w2_pad_kernel<<<g, 256, 0, ctx->stream>>>(d_W2, h, l, f->lp, f->w2.get());
       launched(ctx);
       f->miss = DevMem<unsigned long long>(1);
-      sync(ctx);  // dperm is freed with the stream; host vector outlives the copy
+      sync(ctx);  // the host perm vector must outlive its async copy
     } catch (...) {
       delete f;
       throw;

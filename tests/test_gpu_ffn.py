@@ -36,7 +36,7 @@ def mods(gpu_ctx):
     ((16,), 32, 1, 1_000),         # smallest hidden width
     ((5, 11, 3), 64, 3, 3_001),    # ragged dim widths (8-padding), l > 1, partial tile
     ((40, 24), 128, 8, 777),       # two K blocks (K = 64 + 16 padded)
-    ((64, 48, 16), 96, 2, 2_500),  # K = 128, N = 96
+    ((64, 32, 16), 96, 2, 2_500),  # K = 112 in 4 blocks, N = 96
 ])
 def test_ffn_rows_matches_oracle(mods, widths, h, l, n):
     ffn, _ = mods
@@ -101,6 +101,10 @@ def test_ffn_empty_and_errors(mods):
         ffn.StarFFN(dims, [np.arange(8)], rng.random((9, 32)), rng.random((32, 1)))
     with pytest.raises(errors.UnsupportedError):
         ffn.StarFFN(dims, [np.arange(8)], rng.random((8, 48)), rng.random((48, 1)))  # h not multiple of 32
+    with pytest.raises(errors.UnsupportedError):  # W1 + two stages exceed shared memory
+        big = [rng.random((10, 64)), rng.random((10, 64)), rng.random((10, 64))]
+        ffn.StarFFN(big, [np.arange(64), np.arange(64, 128), np.arange(128, 192)], rng.random((192, 256)),
+                    rng.random((256, 1)))
 
 
 def test_ffn_cfg3_ssb_sample(mods):
