@@ -346,7 +346,9 @@ def main():
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(g, queries, args.cpu_sample_rows)
-        secondary = None if args.no_secondary or world > 1 else fused_predict_bench(ctx, args)
+        secondary = None
+        if not args.no_secondary and world == 1:
+            secondary = {"cfg1": fused_predict_bench(ctx, args), "cfg3": ffn_bench(ctx, args, g)}
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -403,6 +405,73 @@ def _fact_cols(q):
     cols |= {f.column for f in q.filters if f.target == -1}
     cols |= {g.column for g in q.group_by if g.target == -1}
     return cols
+
+
+def ffn_bench(ctx, args, g):
+    """configs[2]: SSB lineorder x customer x part + 2-layer FFN (h=256, l=1), the
+    planner's non-fused plan (cost ratio < 1) on the tensor cores (csrc/ffn.cu).
+    Timed through StarFFN (probe tables + join + FFN, one launch per call)."""
+    import torch
+    from oracle import laq_oracle as O
+    from paper_2306_08367_b200 import ffn, fusion
+    fks, pks, dims, pl, W1, W2 = ffn.cfg3_inputs(g)
+    n = len(fks[0])
+    plan = fusion.plan_linear(n, 64, 256, [len(p) for p in pks])
+    m = ffn.StarFFN(dims, pl, W1, W2, dim_pks=pks)
+    fd = [torch.from_numpy(np.ascontiguousarray(f)).cuda() for f in fks]
+    y = torch.empty((n, 1), dtype=torch.float32, device="cuda")
+    before = ctx.launches
+    for _ in range(3):
+        m(fd, out=y)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 5
+    e0.record()
+    for _ in range(reps):
+        m(fd, out=y)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    flop = 2 * 64 * 256 + 2 * 256
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:  # noqa: BLE001
+        pass
+    peak = float(peaks.get("bf16_tflops", 2250.0))
+    tensor_tf = 3 * n * 2 * 64 * 256 / (ms / 1e3) / 1e12
+    # parity on a slice (condition-aware 1e-5, SURVEY Appendix B)
+    cut = 100_000
+    ws, wrows = O.multiway_star_join([f[:cut] for f in fks], pks)
+    ref_y, bound = O.ffn_predict(wrows, dims, pl, 64, W1, W2)
+    got = y[:cut].double().cpu().numpy()
+    ok = bool(np.all(np.abs(got - ref_y) <= 1e-5 * bound))
+    out = {"workload": f"cfg3: SSB SF={args.sf} lineorder x customer x part ({n} rows), 64 features, "
+                       "FFN 64-256(ReLU)-1, plan=" + plan,
+           "ms": ms, "rows_per_s": n / (ms / 1e3), "launches_per_call": (ctx.launches - before) // (3 + reps),
+           "alg_tflops": n * flop / (ms / 1e3) / 1e12,
+           "roofline": {"bound": "tensor", "achieved": tensor_tf, "peak": peak, "unit": "TFLOP/s",
+                        "frac": tensor_tf / peak,
+                        "note": "tensor-pipe rate of the bf16x3 split (3 MMAs per product); algorithmic "
+                                "flops count each product once (alg_tflops)",
+                        "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" if peaks else "nominal"},
+           "gather_bytes_per_row": 256, "gather_gbs": 256 * n / (ms / 1e3) / 1e9,
+           "parity_slice_rows": cut, "parity_ok_cond_1e-5": ok}
+    try:
+        from oracle import ref
+        if ref.available():
+            sample = 20_000
+            idx = [r[:sample] for r in wrows]
+            t0 = time.perf_counter()
+            _, H = ref.materialize_predict(dims, pl, 64, idx, W1)
+            ref.dense_matmul(np.maximum(H, 0.0), W2)
+            dt = time.perf_counter() - t0
+            out["reference_cpu_1thread"] = {"sample_rows": sample, "s": dt, "rows_per_s": sample / dt,
+                                            "path": "materialize + predict_linear(W1) + ReLU + dense_matmul(W2)"}
+    except Exception as e:  # noqa: BLE001
+        out["reference_cpu_error"] = str(e)
+    m.close()
+    return out
 
 
 def fused_predict_bench(ctx, args):
