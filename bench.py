@@ -29,9 +29,24 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-QUERIES = [(1, 0), (1, 1), (1, 2), (2, 0), (2, 1), (2, 2)]  # Q1.1-Q1.3, Q2.1-Q2.3
+# --workload q1q2 (default, BASELINE configs[1]): Q1.1-Q1.3, Q2.1-Q2.3 at SF=10.
+# --workload q3q4 (BASELINE configs[3]): Q3.1-Q3.3, Q4.1-Q4.3 (multi-way joins incl.
+# the second date link), default SF=100, row-sharded over the GPUs.
+WORKLOADS = {"q1q2": ([(1, 0), (1, 1), (1, 2), (2, 0), (2, 1), (2, 2)], 10),
+             "q3q4": ([(3, 0), (3, 1), (3, 2), (4, 0), (4, 1), (4, 2)], 100)}
+QUERIES = WORKLOADS["q1q2"][0]
+QNAMES = ["Q1.1", "Q1.2", "Q1.3", "Q2.1", "Q2.2", "Q2.3"]
 METRIC = "SSB SF=10 Q1.1-Q2.3 fact-rows/sec (join-MM + group-by aggregation)"
 UNIT = "fact-rows/s"
+
+
+def set_workload(args):
+    global QUERIES, QNAMES, METRIC
+    QUERIES, default_sf = WORKLOADS[args.workload]
+    if args.sf is None:
+        args.sf = default_sf
+    QNAMES = [f"Q{g}.{i + 1}" for g, i in QUERIES]
+    METRIC = f"SSB SF={args.sf} {QNAMES[0]}-{QNAMES[-1]} fact-rows/sec (join-MM + group-by aggregation)"
 
 
 def parse():
@@ -40,11 +55,14 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="laq", choices=["laq", "reference"])
-    ap.add_argument("--sf", type=int, default=10)
+    ap.add_argument("--sf", type=int, default=None)
+    ap.add_argument("--workload", default="q1q2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--cpu-sample-rows", type=int, default=3_000_000)
-    return ap.parse_args()
+    args = ap.parse_args()
+    set_workload(args)
+    return args
 
 
 # ---------------------------------------------------------------------------
@@ -152,8 +170,8 @@ def cpu_baseline(g, queries, sample_rows):
         _, s = ref.run_query(rs, q)
         secs += s
     return {"value": len(queries) * n / secs, "unit": UNIT, "cores": 1, "kind": "reference",
-            "sample": f"run_query_laq (reference C++, 1 thread) on the first {n} of 60M SF=10 lineorder rows, "
-                      f"full dims, the same six queries; {secs:.1f}s"}
+            "sample": f"run_query_laq (reference C++, 1 thread) on the first {n} of {len(g.fact['lo_part'])} "
+                      f"lineorder rows, full dims, the same six queries; {secs:.1f}s"}
 
 
 def run_reference(args, world, rank):
@@ -167,7 +185,7 @@ def run_reference(args, world, rank):
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/liblaq_ref.so was not built"}))
         return
-    g = gen.gen_star("Ssb", args.sf, 42, narrow=False)
+    g = gen.gen_star("Ssb", args.sf, 42, narrow=False, max_bytes=64 << 30)
     n = min(len(g.fact["lo_part"]), max(1_000_000, threads * 400_000))
     tables = [("lineorder", {c: a[:n] for c, a in g.fact.items()})]
     tables += [(t, dict(cols)) for t, cols in g.tables.items() if t != "lineorder"]
@@ -192,8 +210,8 @@ def run_reference(args, world, rank):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int64", "data": "synthetic (reference generator, seed 42)",
             "impl": "reference",
-            "config": {"workload": f"SSB SF={args.sf} Q1.1-Q2.3, sample of {n} lineorder rows",
-                       "queries": ["Q1.1", "Q1.2", "Q1.3", "Q2.1", "Q2.2", "Q2.3"]},
+            "config": {"workload": f"SSB SF={args.sf} {QNAMES[0]}-{QNAMES[-1]}, sample of {n} lineorder rows",
+                       "queries": QNAMES},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                              "sample": f"{n} lineorder rows split over {threads} threads, run_query_laq per "
                                        f"shard, group sums merged"},
@@ -222,7 +240,7 @@ def main():
 
     ctx = context(local)
     # Per-rank 60M-row shard; rank 0's is exactly the reference's SF=10 table.
-    g = gen.gen_star("Ssb", args.sf, 42, narrow=True, fact_tag=None if rank == 0 else f"rank{rank}")
+    g = gen.gen_star("Ssb", args.sf, 42, narrow=True, max_bytes=64 << 30, fact_tag=None if rank == 0 else f"rank{rank}")
     n_rows = len(g.fact["lo_part"])
     ds = star.upload_gen_star(g, ctx=ctx)
     queries = make_queries(ds.measure_selectivity, rank, world, dist)
@@ -286,7 +304,7 @@ def main():
     scan_ms = np.array([[ev[i][q][0].elapsed_time(ev[i][q][1]) for q in range(len(plans))] for i in range(args.steps)])
     bytes_per_launch = np.array([p.bytes_per_row * n_rows for p in plans], dtype=np.float64)
     achieved = float(bytes_per_launch.sum() / (scan_ms.mean(axis=0).sum() / 1e3) / 1e9)
-    traffic, traffic_src = ncu_traffic() or (None, None)
+    traffic, traffic_src = (ncu_traffic() if args.workload == "q1q2" else None) or (None, None)
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(peaks_path):
         peaks = json.load(open(peaks_path))
@@ -347,7 +365,7 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(g, queries, args.cpu_sample_rows)
         secondary = None
-        if not args.no_secondary and world == 1:
+        if not args.no_secondary and world == 1 and args.workload == "q1q2":
             secondary = {"cfg1": fused_predict_bench(ctx, args), "cfg3": ffn_bench(ctx, args, g)}
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -355,11 +373,13 @@ def main():
             "vs_baseline": None, "dtype": "int32",
             "data": "synthetic: the reference generator (benchgen.cpp, seed 42) restated bit-exactly; "
                     "rank r>0 draws its own lineorder shard over the same dims",
-            "config": {"workload": f"SSB SF={args.sf} Q1.1-Q2.3 (BASELINE configs[1]), {n_rows} lineorder rows per GPU",
-                       "queries": ["Q1.1", "Q1.2", "Q1.3", "Q2.1", "Q2.2", "Q2.3"],
+            "config": {"workload": f"SSB SF={args.sf} {QNAMES[0]}-{QNAMES[-1]} (BASELINE configs"
+                                   f"[{1 if args.workload == 'q1q2' else 3}]), {n_rows} lineorder rows per GPU",
+                       "queries": QNAMES,
                        "dials": [int(q.filters[-1].pred.lo) for q in queries],
                        "parallelism": f"row-sharded x{world}, NCCL all-reduce of group accumulators",
-                       "l2": "inputs 0.96 GB per query > 126 MB L2 (no flush needed)",
+                       "l2": f"inputs {min(plans, key=lambda p: p.bytes_per_row).bytes_per_row * n_rows / 1e9:.2f} GB "
+                             "or more per query > 126 MB L2 (no flush needed)",
                        "result_rows": [int(r.shape[0]) for r in results],
                        "per_query_scan_ms": [round(float(x), 4) for x in scan_ms.mean(axis=0)]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -284,7 +284,11 @@ typedef struct {
 } laq_query_desc;
 
 /* Prepare a plan: resolves names (LAQ_ERR_NAME), types (LAQ_ERR_TYPE) and the
- * dense group-id space; *h_n_groups = number of group-id slots G. */
+ * dense group-id space; *h_n_groups = number of group-id slots G.  A join with
+ * no filter and no group column whose fact keys all have a dim row (checked once
+ * per star on the device and cached) is left out of the scan: it cannot drop a
+ * fact row.  Plans snapshot that check: re-prepare after rewriting fact key
+ * columns registered with laq_star_add_table_device. */
 int laq_query_prepare(laq_ctx* ctx, const laq_star* star, const laq_query_desc* q, laq_plan** out,
                       int64_t* h_n_groups);
 /* Enqueue the plan on the context stream (no host sync; graph-capturable):

@@ -143,6 +143,16 @@ __global__ void count_pass_kernel(const int32_t* __restrict__ code, int64_t slot
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
 
+// Fact FK values without a matching dim row (referential coverage of a link).
+__global__ void fk_miss_kernel(const int32_t* __restrict__ fk, int64_t n, const ProbeView pv,
+                               unsigned long long* out) {
+  unsigned long long c = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    c += pv.row(__ldg(fk + i)) < 0 ? 1 : 0;
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
 // ---- kernel dispatch (instantiated per link count in ssb_scan_nl*.cu) -----
 
 void launch_scan(laq_ctx* ctx, const ScanArgs& a, int nl, int nf, int mode, int variant, bool vec, int grid,
@@ -174,6 +184,9 @@ struct laq_star {
   };
   std::vector<Link> links;
   std::map<std::string, std::unique_ptr<Probe>> probes;  // "dim/pk" -> probe
+  // "fk|dim/pk" -> every fact FK value has a dim row (computed once per star on
+  // the device; cleared whenever a table is added)
+  std::map<std::string, bool> covered;
 
   const DevTable* table(const std::string& n) const {
     for (const auto& t : tables)
@@ -406,6 +419,7 @@ int laq_star_destroy(laq_star* s) {
 static DevTable& new_table(laq_star* s, const char* name, int32_t is_fact, int64_t rows) {
   if (s->table(name)) fail(LAQ_ERR_NAME, std::string("duplicate table name: ") + name);
   if (is_fact && s->fact >= 0) fail(LAQ_ERR_SHAPE, "star schema already has a fact table");
+  s->covered.clear();
   s->tables.push_back(std::make_unique<DevTable>());
   DevTable& t = *s->tables.back();
   t.name = name;
@@ -506,6 +520,29 @@ int laq_star_add_link(laq_star* s, const char* fact_fk, const char* dim_name, co
   });
 }
 
+namespace laq {
+namespace {
+bool link_covered(laq_ctx* ctx, laq_star* s, const DevCol& fk, const DevTable& d, const DevCol& pk, const Probe& pr) {
+  if (std::getenv("LAQ_NO_LINK_ELISION")) return false;
+  const std::string key = fk.name + "|" + d.name + "/" + pk.name;
+  auto it = s->covered.find(key);
+  if (it != s->covered.end()) return it->second;
+  const int64_t n = s->tables[s->fact]->rows;
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(ctx->d_flags + 57);
+  LAQ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), ctx->stream));
+  if (n > 0) {
+    fk_miss_kernel<<<grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(fk.d, n, pr.view(), cnt);
+    launched(ctx);
+  }
+  LAQ_CUDA(cudaMemcpyAsync(ctx->h_pinned, cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  const bool cov = ctx->h_pinned[0] == 0;
+  s->covered[key] = cov;
+  return cov;
+}
+}  // namespace
+}  // namespace laq
+
 int laq_query_prepare(laq_ctx* ctx, const laq_star* cs, const laq_query_desc* q, laq_plan** out,
                       int64_t* h_n_groups) {
   laq_star* s = const_cast<laq_star*>(cs);
@@ -602,6 +639,7 @@ int laq_query_prepare(laq_ctx* ctx, const laq_star* cs, const laq_query_desc* q,
     plan->links.resize(q->n_joins);
     std::vector<const int32_t*> fks(q->n_joins);
     std::vector<const Probe*> probes(q->n_joins);
+    std::vector<char> elide(q->n_joins, 0);
     for (int j = 0; j < q->n_joins; ++j) {
       const laq_link_desc& l = q->joins[j];
       const DevCol& fk = int_col(fact, l.fact_fk);
@@ -631,9 +669,28 @@ int laq_query_prepare(laq_ctx* ctx, const laq_star* cs, const laq_query_desc* q,
       }
       fks[j] = fk.d;
       probes[j] = &pr;
-      note(fk);
+      elide[j] = ca.n_filters == 0 && ca.n_groups == 0 && link_covered(ctx, s, fk, *d, pk, pr);
+      if (!elide[j]) note(fk);
     }
-    plan->nl = q->n_joins;
+    // A link with no filter and no group column whose every fact key has a dim
+    // row changes nothing in multiway_star_join (no fact row drops, nothing is
+    // read from the dim): it is not scanned.  Removes its FK column read and its
+    // per-row probe (SSB Q3.x joins part this way).
+    {
+      std::vector<laq_plan::LinkCode> kl;
+      std::vector<const int32_t*> kf;
+      std::vector<const Probe*> kp;
+      for (int j = 0; j < q->n_joins; ++j)
+        if (!elide[j]) {
+          kl.push_back(std::move(plan->links[j]));
+          kf.push_back(fks[j]);
+          kp.push_back(probes[j]);
+        }
+      plan->links = std::move(kl);
+      fks = std::move(kf);
+      probes = std::move(kp);
+    }
+    plan->nl = static_cast<int>(plan->links.size());
     plan->vec = aligned;
     plan->mode = G == 1 ? 0 : (G <= kSmemBinsPipe ? 1 : (G <= kSmemBinsLdg ? 1 : 2));
     plan->bytes_per_row = 4 * (plan->nl + plan->nf + a.n_fgroups + (a.measure ? 1 : 0));

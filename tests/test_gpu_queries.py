@@ -114,3 +114,23 @@ def test_sf10_q21_against_oracle(gpu_ctx):
     for grp, qi, dial in ((1, 0, 30), (2, 0, 100), (3, 0, 90), (4, 0, 50)):
         q = Q.spec_with_dial(Q.group_defs(grp)[qi], grp, dial)
         assert np.array_equal(ds.run_query(q), O.run_query(g.tables, q))
+
+
+@pytest.mark.parametrize("dangling", [0.0, 0.05])
+def test_link_elision_respects_inner_join(gpu_ctx, dangling):
+    """Q3.x joins part with no filter / group column.  With every lo_part key
+    present the link is left out of the scan (one 4-byte column less per row);
+    with dangling keys (fact rows whose part is missing must drop, inner join,
+    laqops.cpp:283-298) it must stay.  Both must equal the oracle exactly."""
+    from paper_2306_08367_b200 import gen, star
+    g = gen.gen_star("Ssb", 1, 42, dangling=dangling, narrow=True)
+    ds = star.upload_gen_star(g)
+    for grp in (3, 4):
+        for q in ds.gen_queries(grp):
+            p = ds.prepare(q)
+            full = 4 * (len(q.joins) + 1 + sum(1 for f in q.filters if f.target == -1))
+            if dangling == 0.0 and grp == 3:
+                assert p.bytes_per_row == full - 4  # part link elided
+            if dangling > 0.0:
+                assert p.bytes_per_row == full
+            assert np.array_equal(ds.run_query(q), O.run_query(g.tables, q))
