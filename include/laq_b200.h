@@ -196,7 +196,7 @@ int laq_probe_join_rows(laq_ctx* ctx, const laq_probe* probe, const int32_t* con
  * and the products of predict_linear / dense_matmul (mlops.cpp:248-250,
  * matrix.cpp:158-174); the reference has no FFN, cfg3 composes these.  T is
  * gathered tile by tile into shared memory, never written.  fp64 inputs are
- * stored as a bf16x3 split; tcgen05 MMAs accumulate fp32 in TMEM (SURVEY.md
+ * stored as a scaled fp16x2 split; tcgen05 MMAs accumulate fp32 in TMEM (SURVEY.md
  * Appendix B: condition-aware 1e-5).  Output fp32 [rows x l].
  * Limits: 1..4 dims, sum of 8-padded dim widths <= 128, h multiple of 32 in
  * [32,256], l in [1,8] (LAQ_ERR_UNSUPPORTED otherwise); placements as in
@@ -213,6 +213,29 @@ int laq_ffn_predict_rows(laq_ctx* ctx, const laq_ffn* f, const int32_t* const* d
 int laq_ffn_predict_star(laq_ctx* ctx, const laq_ffn* f, const laq_probe* probe, const int32_t* const* d_fks,
                          int64_t n_fact, float* d_out, int64_t* d_survivors, int64_t* h_nnz);
 int laq_ffn_destroy(laq_ffn* f);
+
+/* ---- tensor-core contractions for the wide shapes (BASELINE configs[4]) ----
+ * A features object holds dims' tables B_j (fp64, rows x cols) in the fp16x2
+ * split block layout with their placements into the global feature width k
+ * (LAQ_ERR_MAPPING on overlap / out of range, as check_placements fusion.cpp:11-25).
+ *   laq_tc_gemm: C[m x n] (fp32) = T . W, T[r] = sum_j B_j[d_rows[j][r]] M_j
+ *     - prefuse_linear (fusion.cpp:50-62): one dim, d_rows = NULL (identity),
+ *       m = dim rows -> P_j = B_j (M_j W);
+ *     - non-fused predict (materialize laqops.cpp:338-374 + predict_linear
+ *       mlops.cpp:248-250): d_rows = join row maps, T never written.
+ *   W is k x n fp64 row-major.  tcgen05 fp16x2 split (3 MMAs), fp32 accumulate (condition-aware
+ *   1e-5).  Asynchronous.
+ *   laq_apply_fused_linear_f32: Y = ((P_0[i_0] + P_1[i_1]) + ...) over fp32 partials
+ *     (fusion.cpp:64-77), int32 row maps.  Synchronises. */
+typedef struct laq_tc_features laq_tc_features;
+int laq_tc_features_create(laq_ctx* ctx, int32_t n_dims, const double* const* d_dims, const int64_t* h_dim_rows,
+                           const int64_t* h_dim_cols, const int64_t* const* h_placements, int64_t k,
+                           laq_tc_features** out);
+int laq_tc_features_destroy(laq_tc_features* f);
+int laq_tc_gemm(laq_ctx* ctx, const laq_tc_features* f, const int32_t* const* d_rows, int64_t m, const double* d_W,
+                int64_t n, float* d_out);
+int laq_apply_fused_linear_f32(laq_ctx* ctx, int32_t n_parts, const int32_t* const* d_idx, int64_t rows,
+                               const float* const* d_partials, int64_t l, float* d_out);
 
 /* ---- aggregate-MM (laqops.hpp:112-166) --------------------------------- */
 

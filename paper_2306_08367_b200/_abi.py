@@ -74,6 +74,10 @@ _SIGS = {
     "laq_ffn_predict_rows": (C.c_int, [vp, vp, vp, i64, vp]),
     "laq_ffn_predict_star": (C.c_int, [vp, vp, vp, vp, i64, vp, vp, i64p]),
     "laq_ffn_destroy": (C.c_int, [vp]),
+    "laq_tc_features_create": (C.c_int, [vp, i32, vp, i64p, i64p, vp, i64, C.POINTER(vp)]),
+    "laq_tc_features_destroy": (C.c_int, [vp]),
+    "laq_tc_gemm": (C.c_int, [vp, vp, vp, i64, vp, i64, vp]),
+    "laq_apply_fused_linear_f32": (C.c_int, [vp, i32, vp, i64, vp, i64, vp]),
     "laq_groupby_sum_single": (C.c_int, [vp, vp, vp, i64, vp, vp, i64, vp, vp, i64p]),
     "laq_groupby_sum_multi": (C.c_int, [vp, i32, vp, vp, i64, vp, vp, i64, i64p]),
     "laq_star_create": (C.c_int, [vp, C.POINTER(vp)]),

@@ -129,6 +129,8 @@ inline int grid_for(int64_t n, int per_block, int max_blocks) {
 // min/max of an int64 or int32 array (device reduce, synchronises).
 void minmax_i64(laq_ctx* ctx, const int64_t* d, int64_t n, int64_t* mn, int64_t* mx);
 void minmax_i32(laq_ctx* ctx, const int32_t* d, int64_t n, int64_t* mn, int64_t* mx);
+// max |x| over a device fp64 array (synchronises); 0 for n == 0.
+double absmax_f64(laq_ctx* ctx, const double* d, int64_t n);
 // Exclusive scan of int64 counts (in place allowed); returns total (synchronises
 // only when h_total != nullptr).
 void exclusive_scan_i64(laq_ctx* ctx, const int64_t* d_in, int64_t* d_out, int64_t n, int64_t* h_total);

@@ -9,13 +9,15 @@
 // never written to HBM: each 128-row tile of T is gathered straight from the
 // dimension feature tables into shared memory and multiplied there.
 //
-// Numerics: fp64 inputs are stored once as a bf16x3 split
-// (x = hi + lo + O(2^-18|x|)); every tile runs hi.hi + hi.lo + lo.hi on tcgen05
-// with fp32 accumulation in TMEM, then ReLU and layer 2 in fp32 on the CUDA cores.
-// Accuracy is judged condition-aware at 1e-5 (tests/test_gpu_ffn.py).
+// Numerics: fp64 inputs are stored once as a scaled fp16x2
+// split (tc.cuh split_f16: x*s = hi + lo + O(2^-22)); every tile runs hi.hi + hi.lo
+// + lo.hi on tcgen05 with fp32 accumulation in TMEM, the epilogue unscales by the
+// exact power of two 1/(s_A s_W1), then ReLU and layer 2 in fp32 on the CUDA cores.
+// Accuracy is judged condition-aware at 1e-5 (tests/test_gpu_ffn.py).  (A bf16
+// split keeps only 16 significant bits, 1.5e-5 per element: measured to fail.)
 //
 // HBM layout: every dimension's features are cut into blocks of 32 columns; block b
-// is a bf16 table [rows_j x 64] whose row is (hi[32] | lo[32]) -- exactly one
+// is an fp16 table [rows_j x 64] whose row is (hi[32] | lo[32]) -- exactly one
 // 128-byte line, the unit one TMA gather moves.  W1 uses the same block layout
 // (W1^T rows = hidden units), so inside a 128-byte swizzled smem row the hi
 // operand sits at byte 0 and the lo operand at byte 64.
@@ -60,7 +62,7 @@ constexpr int kMaxL = 8;
 constexpr uint32_t kBlockBytes = kRows * 128u;  // one feature block of a stage
 
 struct Args {
-  const __nv_bfloat16* block[kMaxBlocks];  // block b: [rows x 64] bf16 = (hi32 | lo32)
+  const tc::elem* block[kMaxBlocks];  // block b: [rows x 64] fp16 = (hi32 | lo32)
   int n_blocks;
   int block_dim[kMaxBlocks];    // dimension owning block b
   int block_steps[kMaxBlocks];  // 16-feature MMA steps in block b (1 or 2)
@@ -71,9 +73,10 @@ struct Args {
   int probe_mode;
   int N;                    // hidden width (UMMA N)
   int l;
-  const __nv_bfloat16* w1;  // [n_blocks][N][64] (hi32 | lo32)
+  const tc::elem* w1;  // [n_blocks][N][64] (hi32 | lo32)
   const float* w2;          // [N x LP] (l padded to a power of two with zeros)
   float* y;                 // [n x l]
+  float unscale;            // 1 / (s_A s_W1), a power of two
   int stages;
   int64_t n_tiles;
   unsigned long long* miss;  // probe mode: rows missing some dimension
@@ -191,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant_
       if (a.diag != 1 && a.diag < 3) {
         const uint32_t abase = sbase + L.a + s * L.stage_bytes;
         for (int b = 0; b < NB; ++b) {
-          const __nv_bfloat16* base = a.block[b] + chunk * 8;
+          const tc::elem* base = a.block[b] + chunk * 8;
           const int j = a.block_dim[b];
           const uint32_t dbase = abase + b * kBlockBytes;
 #pragma unroll
@@ -212,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant_
   } else if (warp == kMmaWarp) {
     // ================= MMA issuer =================
     if (lane == 0) {
-      const uint32_t idesc = tc::idesc_bf16_f32(kRows, N);
+      const uint32_t idesc = tc::idesc_f16_f32(kRows, N);
       int it = 0;
       for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x, ++it) {
         const int s = it % S, ab = it & 1;
@@ -230,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant_
             for (int st = 0; st < a.block_steps[b]; ++st) {
               const uint64_t ad = tc::sdesc_sw128(abase + b * kBlockBytes + pa + st * 32u);
               const uint64_t bd = tc::sdesc_sw128(sbase + L.b + b * (N * 128u) + pb + st * 32u);
-              tc::mma_bf16(d, ad, bd, idesc, acc);
+              tc::mma_f16(d, ad, bd, idesc, acc);
               acc = 1;
             }
         }
@@ -278,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant_
             }
 #pragma unroll
             for (int ii = 0; ii < 4; ++ii) {
-              const float h = fmaxf(__uint_as_float(v[i0 + ii]), 0.f);
+              const float h = fmaxf(__uint_as_float(v[i0 + ii]) * a.unscale, 0.f);
 #pragma unroll
               for (int c = 0; c < LP; ++c) y[ii][c] = fmaf(h, w[ii * LP + c], y[ii][c]);
             }
@@ -314,34 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant_
   }
 }
 
-// ---- layout preparation --------------------------------------------------------
-// Feature block: columns [f0, f0 + 32) of B_j (rows x cols fp64) -> bf16
-// [rows x 64] = (hi[32] | lo[32]), zero padded past `cols`.
-__global__ void split_block_kernel(const double* __restrict__ B, int64_t rows, int64_t cols, int64_t f0,
-                                   __nv_bfloat16* __restrict__ out) {
-  const int64_t total = rows * 32;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e >> 5, c = e & 31;
-    __nv_bfloat16 h = __float2bfloat16(0.f), q = __float2bfloat16(0.f);
-    if (f0 + c < cols) tc::split_bf16(B[r * cols + f0 + c], h, q);
-    out[r * 64 + c] = h;
-    out[r * 64 + 32 + c] = q;
-  }
-}
-// W1 (k x n fp64, row-major) -> [n_blocks][n][64]: block b, hidden unit col,
-// (hi | lo) of W1[perm[32 b + c]][col] (perm -1 = padding).
-__global__ void split_w1_kernel(const double* __restrict__ W, int64_t n, const int64_t* __restrict__ perm,
-                                int64_t n_blocks, __nv_bfloat16* __restrict__ out) {
-  const int64_t total = n_blocks * n * 32;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = e & 31, bc = e >> 5, b = bc / n, col = bc - b * n;
-    __nv_bfloat16 h = __float2bfloat16(0.f), o = __float2bfloat16(0.f);
-    const int64_t g = perm[b * 32 + c];
-    if (g >= 0) tc::split_bf16(W[g * n + col], h, o);
-    out[bc * 64 + c] = h;
-    out[bc * 64 + 32 + c] = o;
-  }
-}
+// ---- layout preparation (feature blocks / W1: tc::split_block_kernel, tc::split_w1_kernel) ----
 // W2 (h x l fp64) -> fp32 [h x lp], zero columns l..lp-1.
 __global__ void w2_pad_kernel(const double* __restrict__ x, int64_t h, int64_t l, int64_t lp, float* __restrict__ y) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < h * lp; e += (int64_t)gridDim.x * blockDim.x) {
@@ -365,8 +341,9 @@ struct laq_ffn {
   int block_dim[ffn::kMaxBlocks] = {}, block_steps[ffn::kMaxBlocks] = {};
   int N = 0, l = 0, lp = 1, stages = 0;
   int64_t k = 0;
-  DevMem<__nv_bfloat16> blocks[ffn::kMaxBlocks];  // [rows_j x 64] (hi32 | lo32)
-  DevMem<__nv_bfloat16> w1;  // [n_blocks][N][64]
+  double unscale = 1.0;
+  DevMem<tc::elem> blocks[ffn::kMaxBlocks];  // [rows_j x 64] (hi32 | lo32)
+  DevMem<tc::elem> w1;  // [n_blocks][N][64]
   DevMem<float> w2;
   DevMem<unsigned long long> miss;
 };
@@ -389,6 +366,7 @@ ffn::Args make_args(const laq_ffn* f, int64_t n, float* y) {
   a.w1 = f->w1.get();
   a.w2 = f->w2.get();
   a.y = y;
+  a.unscale = static_cast<float>(f->unscale);
   a.stages = f->stages;
   a.n_tiles = (n + ffn::kRows - 1) / ffn::kRows;
   a.miss = f->miss.get();
@@ -466,12 +444,16 @@ int laq_ffn_create(laq_ctx* ctx, int32_t n_dims, const double* const* d_dims, co
       if (S == 0) fail(LAQ_ERR_UNSUPPORTED, "ffn: W1 tile does not fit shared memory");
       f->stages = S;
       const int g = ctx->sm_count * 8;
+      double amax = 0.0;
+      for (int j = 0; j < n_dims; ++j) amax = std::max(amax, absmax_f64(ctx, d_dims[j], h_dim_rows[j] * h_dim_cols[j]));
+      const double sa = tc::pow2_scale(amax), sw = tc::pow2_scale(absmax_f64(ctx, d_W1, k * h));
+      f->unscale = 1.0 / (sa * sw);
       for (int b = 0; b < f->n_blocks; ++b) {
         const int j = src[b].first;
         const int64_t r = h_dim_rows[j];
-        f->blocks[b] = DevMem<__nv_bfloat16>(static_cast<size_t>(std::max<int64_t>(r, 1) * 64));
+        f->blocks[b] = DevMem<tc::elem>(static_cast<size_t>(std::max<int64_t>(r, 1) * 64));
         if (r > 0) {
-          ffn::split_block_kernel<<<g, 256, 0, ctx->stream>>>(d_dims[j], r, h_dim_cols[j], src[b].second,
+          tc::split_block_kernel<<<g, 256, 0, ctx->stream>>>(d_dims[j], r, h_dim_cols[j], src[b].second, sa,
                                                               f->blocks[b].get());
           launched(ctx);
         } else {
@@ -481,8 +463,8 @@ int laq_ffn_create(laq_ctx* ctx, int32_t n_dims, const double* const* d_dims, co
       DevBuf<int64_t> dperm(ctx, perm.size());
       LAQ_CUDA(cudaMemcpyAsync(dperm.get(), perm.data(), perm.size() * sizeof(int64_t), cudaMemcpyHostToDevice,
                                ctx->stream));
-      f->w1 = DevMem<__nv_bfloat16>(static_cast<size_t>(f->n_blocks * h * 64));
-      ffn::split_w1_kernel<<<g, 256, 0, ctx->stream>>>(d_W1, h, dperm.get(), f->n_blocks, f->w1.get());
+      f->w1 = DevMem<tc::elem>(static_cast<size_t>(f->n_blocks * h * 64));
+      tc::split_w1_kernel<<<g, 256, 0, ctx->stream>>>(d_W1, h, dperm.get(), f->n_blocks, sw, f->w1.get());
       launched(ctx);
       f->w2 = DevMem<float>(static_cast<size_t>(h * f->lp));
       ffn::w2_pad_kernel<<<g, 256, 0, ctx->stream>>>(d_W2, h, l, f->lp, f->w2.get());

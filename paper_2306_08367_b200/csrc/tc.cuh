@@ -3,14 +3,16 @@
 // and instruction descriptors, tcgen05.mma / commit / ld wrappers.
 //
 // Operand layout used everywhere: K-major, 128-byte swizzle.  A tile of R rows x 64
-// bf16 (128 B per row) occupies R*128 bytes; 8-row groups ("atoms", 1024 B) are
+// 16-bit elements (128 B per row) occupies R*128 bytes; 8-row groups ("atoms", 1024 B) are
 // consecutive (SBO = 1024 B) and inside an atom the 16-byte chunk c of row r sits at
 // chunk position c ^ (r & 7).  Every atom is 1024-byte aligned (descriptor base
-// offset 0).  One MMA consumes K = 16 bf16 = 32 bytes of each row, so stepping K
+// offset 0).  One MMA consumes K = 16 elements = 32 bytes of each row, so stepping K
 // inside the 128-byte atom advances the descriptor start address by 32 bytes.
 #pragma once
 
-#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <cmath>
 #include <stdint.h>
 
 namespace laq {
@@ -123,17 +125,17 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
   d |= static_cast<uint64_t>(2u) << 61;                // layout: SWIZZLE_128B
   return d;
 }
-// Instruction descriptor, kind::f16: bf16 x bf16 -> fp32, both K-major.
-__host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t M, uint32_t N) {
+// Instruction descriptor, kind::f16: f16 x f16 -> fp32, both K-major.
+__host__ __device__ constexpr uint32_t idesc_f16_f32(uint32_t M, uint32_t N) {
   return (1u << 4)           // D format f32
-         | (1u << 7)         // A bf16
-         | (1u << 10)        // B bf16
+         | (0u << 7)         // A f16
+         | (0u << 10)        // B f16
          | ((N >> 3) << 17)  // N / 8
          | ((M >> 4) << 24); // M / 16
 }
 
 // D[tmem] (+)= A[smem] . B[smem]^T, issued by one thread.
-__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                          uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -162,13 +164,62 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// ---- bf16x3 split --------------------------------------------------------------
-// x = hi + lo + O(2^-18 |x|): hi = RN_bf16(x), lo = RN_bf16(x - hi) (the residual
-// taken in fp64, so lo captures the next 8 significant bits exactly).
-__device__ __forceinline__ void split_bf16(double x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
-  hi = __double2bfloat16(x);
-  lo = __double2bfloat16(x - static_cast<double>(__bfloat162float(hi)));
+// ---- f16x2 split ("3-product" emulation of ~fp32 products) ------------------------
+// Operands are stored as two fp16 halves of the scaled value y = x * scale:
+//   hi = RN_f16(y), lo = RN_f16(y - hi)   (the residual taken in fp64)
+// so y = hi + lo + O(2^-22 |y|).  A product is hi.hi + hi.lo + lo.hi (the dropped
+// lo.lo is O(2^-22)); fp16 products are exact in the fp32 TMEM accumulator.
+// `scale` is a power of two that puts the table's largest magnitude at 2^14: no
+// overflow, and every element >= 2^-17 of the maximum keeps its lo half normal
+// (smaller ones lose relative precision but are below 1e-5 of the condition
+// bound).  The accumulator is multiplied back by 1/(scale_A scale_W), exactly.
+using elem = __half;
+__device__ __forceinline__ void split_f16(double x, double scale, elem& hi, elem& lo) {
+  const double y = x * scale;
+  hi = __double2half(y);
+  lo = __double2half(y - static_cast<double>(__half2float(hi)));
 }
+// Power-of-two scale putting max|x| at [2^13, 2^14).
+inline double pow2_scale(double maxabs) {
+  if (!(maxabs > 0.0) || !std::isfinite(maxabs)) return 1.0;
+  int e = 0;
+  std::frexp(maxabs, &e);  // maxabs in [2^(e-1), 2^e)
+  return std::ldexp(1.0, 14 - e);
+}
+
+// ---- split block layout (shared by the tcgen05 operators) ------------------------
+// Features are cut into blocks of 32 columns; a block row is one 128-byte line
+// (hi[32] | lo[32]) in fp16 halves (split_f16), so inside a 128-byte swizzled smem row the hi operand
+// starts at byte 0 and the lo operand at byte 64.
+namespace {
+// Feature block: columns [f0, f0 + 32) of B_j (rows x cols fp64) -> fp16 halves
+// [rows x 64] = (hi[32] | lo[32]), zero padded past `cols`.
+__global__ void split_block_kernel(const double* __restrict__ B, int64_t rows, int64_t cols, int64_t f0,
+                                   double scale, elem* __restrict__ out) {
+  const int64_t total = rows * 32;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e >> 5, c = e & 31;
+    elem h = __float2half(0.f), q = __float2half(0.f);
+    if (f0 + c < cols) split_f16(B[r * cols + f0 + c], scale, h, q);
+    out[r * 64 + c] = h;
+    out[r * 64 + 32 + c] = q;
+  }
+}
+// W1 (k x n fp64, row-major) -> [n_blocks][n][64]: block b, hidden unit col,
+// (hi | lo) of W1[perm[32 b + c]][col] (perm -1 = padding).
+__global__ void split_w1_kernel(const double* __restrict__ W, int64_t n, const int64_t* __restrict__ perm,
+                                int64_t n_blocks, double scale, elem* __restrict__ out) {
+  const int64_t total = n_blocks * n * 32;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e & 31, bc = e >> 5, b = bc / n, col = bc - b * n;
+    elem h = __float2half(0.f), o = __float2half(0.f);
+    const int64_t g = perm[b * 32 + c];
+    if (g >= 0) split_f16(W[g * n + col], scale, h, o);
+    out[bc * 64 + c] = h;
+    out[bc * 64 + 32 + c] = o;
+  }
+}
+}  // namespace
 
 }  // namespace tc
 }  // namespace laq

@@ -4,6 +4,8 @@
 #include <climits>
 #include <cmath>
 
+#include <cstring>
+
 #include "common.cuh"
 
 namespace laq {
@@ -74,6 +76,31 @@ void exclusive_scan_i64(laq_ctx* ctx, const int64_t* d_in, int64_t* d_out, int64
     sync(ctx);
     *h_total = ctx->h_pinned[0] + ctx->h_pinned[1];
   }
+}
+
+namespace {
+__global__ void absmax_kernel(const double* __restrict__ x, int64_t n, unsigned long long* out) {
+  double m = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(x[i]));
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(m)));
+}
+}  // namespace
+
+double absmax_f64(laq_ctx* ctx, const double* d, int64_t n) {
+  unsigned long long* f = reinterpret_cast<unsigned long long*>(ctx->d_flags + 58);
+  LAQ_CUDA(cudaMemsetAsync(f, 0, sizeof(unsigned long long), ctx->stream));
+  if (n > 0) {
+    absmax_kernel<<<grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(d, n, f);
+    launched(ctx);
+  }
+  LAQ_CUDA(cudaMemcpyAsync(ctx->h_pinned, f, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  double m;
+  const int64_t bits = ctx->h_pinned[0];
+  std::memcpy(&m, &bits, sizeof(m));
+  return m;
 }
 
 }  // namespace laq

@@ -10,7 +10,7 @@ k/l = 64/256, so the planner runs this non-fused operator, which never writes T:
 tiles of T are gathered into shared memory and multiplied by tcgen05 MMAs
 (csrc/ffn.cu).
 
-Numerics: bf16x3 split, fp32 accumulation, fp32 output; checked
+Numerics: scaled fp16x2 split (hi.hi + hi.lo + lo.hi), fp32 accumulation, fp32 output; checked
 condition-aware at 1e-5 against oracle.laq_oracle.ffn_predict.
 """
 from __future__ import annotations
@@ -28,7 +28,7 @@ f64 = torch.float64
 
 
 class StarFFN:
-    """Feature tables (bf16x3, device layout) + W1/W2 bound once; __call__ runs
+    """Feature tables (fp16x2 split, device layout) + W1/W2 bound once; __call__ runs
     join + FFN over fact keys (probe tables built once) or explicit row maps."""
 
     def __init__(self, dims, placements, W1, W2, dim_pks=None):

@@ -2,7 +2,7 @@
 csrc/ffn.cu) against the composed oracle (materialize + predict_linear + ReLU +
 predict_linear, oracle.laq_oracle.ffn_predict).
 
-Tolerance: bf16x3 split with fp32 accumulation cannot
+Tolerance: a split 16-bit product with fp32 accumulation cannot
 meet a per-element 1e-5 relative bound on cancelling sums, so every element is
 checked condition-aware:  |Y_gpu - Y_ref| <= 1e-5 * bound  with
 bound = sum_n |W2| (|T| |W1|) + |ReLU(H)| |W2|  (the magnitude of every term the
