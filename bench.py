@@ -472,7 +472,7 @@ def ffn_bench(ctx, args, g):
            "alg_tflops": n * flop / (ms / 1e3) / 1e12,
            "roofline": {"bound": "tensor", "achieved": tensor_tf, "peak": peak, "unit": "TFLOP/s",
                         "frac": tensor_tf / peak,
-                        "note": "tensor-pipe rate of the bf16x3 split (3 MMAs per product); algorithmic "
+                        "note": "tensor-pipe rate of the fp16x2 split (3 MMAs per product); algorithmic "
                                 "flops count each product once (alg_tflops)",
                         "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" if peaks else "nominal"},
            "gather_bytes_per_row": 256, "gather_gbs": 256 * n / (ms / 1e3) / 1e9,

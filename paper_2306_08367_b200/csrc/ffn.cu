@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant_
             float w[4 * LP];  // W2 rows col .. col+3 (broadcast 16-byte shared loads)
 #pragma unroll
             for (int qq = 0; qq < LP; ++qq) {
-              const float4 t = tc::lds128(w2a + (col * LP + 4 * qq) * 4u);
+              const float4 t = tc::lds128_const(w2a + (col * LP + 4 * qq) * 4u);
               w[4 * qq] = t.x; w[4 * qq + 1] = t.y; w[4 * qq + 2] = t.z; w[4 * qq + 3] = t.w;
             }
 #pragma unroll

@@ -17,8 +17,9 @@
 // row-tile-major when the split W fits L2 (each A tile is fetched from HBM once and
 // re-read from L2 by the CTAs computing its other column tiles), else column-major
 // (a W panel is reused from L2 by consecutive CTAs):
-//   warps 0-7   epilogue: tcgen05.ld (thread = row, 32 columns per load), fp32
-//               row segments stored straight to C (masked at the edges);
+//   warps 0-7   epilogue: tcgen05.ld (thread = row, 32 columns per load), unscale,
+//               transpose through a swizzled 4 KB shared tile so every store
+//               instruction writes four full 128-byte row segments of C;
 //   warps 8-11  cp.async producers: per stage (one 32-feature K block) the 128
 //               A lines (gathered) + BN W lines, cp.async.mbarrier.arrive.noinc;
 //   warp 12     TMEM owner + MMA issuer: 3 x (1..2) tcgen05.mma per stage into
@@ -63,7 +64,11 @@ struct Args {
 };
 
 __host__ __device__ inline uint32_t stage_bytes(int BN) { return kABytes + static_cast<uint32_t>(BN) * 128u; }
-__host__ __device__ inline uint32_t smem_bytes(int BN, int S) { return S * stage_bytes(BN) + (2 * S + 4) * 8 + 16 + 1024; }
+constexpr uint32_t kBarBytes = 256;  // mbarriers + TMEM slot (after the stages)
+// stages | barriers | 8 x 4 KB epilogue staging tiles | 1 KB alignment slack
+__host__ __device__ inline uint32_t smem_bytes(int BN, int S) {
+  return S * stage_bytes(BN) + kBarBytes + kEpiWarps * 4096u + 1024;
+}
 
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ Args a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -175,29 +180,39 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       const int ab = tl & 1;
       tc::mbar_wait(&acc_full[ab], (tl >> 1) & 1);
       tc::tc_fence_after();
-      const int64_t row = mt * kRows + 32 * q + lane;
+      const int64_t row0 = mt * kRows + 32 * q;
       const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * q) << 16) + ab * 256;
+      const uint32_t stg = sbase + S * SB + kBarBytes + warp * 4096u;  // this warp's 32 x 32 fp32 staging tile
       for (int c0 = 32 * hh; c0 < BN; c0 += 64) {
         uint32_t v[32];
         tc::tmem_ld32(t0 + c0, v);
         tc::tmem_ld_wait();
+        // thread = row -> staging (16-byte chunk c4 of row r at c4 ^ (r & 7): conflict-free)
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * a.unscale);
-        const int64_t col0 = nt * BN + c0;
-        if (row < a.m) {
-          float* dst = a.c + row * a.n + col0;
-          if (col0 + 32 <= a.n && (a.n & 3) == 0) {
+        for (int c4 = 0; c4 < 8; ++c4)
+          tc::sts128(stg + lane * 128u + ((c4 ^ (lane & 7)) << 4),
+                     make_float4(__uint_as_float(v[4 * c4]) * a.unscale, __uint_as_float(v[4 * c4 + 1]) * a.unscale,
+                                 __uint_as_float(v[4 * c4 + 2]) * a.unscale, __uint_as_float(v[4 * c4 + 3]) * a.unscale));
+        __syncwarp();
+        // staging -> C: each group of 8 lanes writes one full 128-byte row segment
+        const int64_t col = nt * BN + c0 + 4 * (lane & 7);
 #pragma unroll
-            for (int i = 0; i < 32; i += 4)
-              __stcs(reinterpret_cast<float4*>(dst + i),
-                     make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]), __uint_as_float(v[i + 2]),
-                                 __uint_as_float(v[i + 3])));
+        for (int qq = 0; qq < 8; ++qq) {
+          const int r = 4 * qq + (lane >> 3);
+          const float4 x = tc::lds128(stg + r * 128u + (((lane & 7) ^ (r & 7)) << 4));
+          const int64_t grow = row0 + r;
+          if (grow >= a.m) continue;
+          float* dst = a.c + grow * a.n + col;
+          if (col + 4 <= a.n && (a.n & 3) == 0) {
+            __stcs(reinterpret_cast<float4*>(dst), x);
           } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (col0 + i < a.n) __stcs(dst + i, __uint_as_float(v[i]));
+            if (col < a.n) __stcs(dst, x.x);
+            if (col + 1 < a.n) __stcs(dst + 1, x.y);
+            if (col + 2 < a.n) __stcs(dst + 2, x.z);
+            if (col + 3 < a.n) __stcs(dst + 3, x.w);
           }
         }
+        __syncwarp();
       }
       tc::tc_fence_before();
       __syncwarp();

@@ -29,8 +29,20 @@ __device__ __forceinline__ uint32_t sw128_off(uint32_t r, uint32_t c) {
 
 __device__ __forceinline__ float4 lds128(uint32_t addr) {
   float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr)
+               : "memory");
+  return v;
+}
+
+// Read-only data (never rewritten while the kernel runs): freely schedulable.
+__device__ __forceinline__ float4 lds128_const(uint32_t addr) {
+  float4 v;
   asm("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
   return v;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
 }
 
 // ---- mbarrier -----------------------------------------------------------------
