@@ -219,3 +219,53 @@ def plan_linear(target_rows: int, k: int, l: int, dim_rows, threshold: float = 1
     `laq cost`, cli.cpp:709-741): fused iff speedup_ratio_linear > threshold."""
     r = speedup_ratio_linear(CostInputs(target_rows, k, l, k, list(dim_rows)))
     return "fused" if decide_fusion(r, threshold) else "nonfused"
+
+
+# ---------------------------------------------------------------------------
+# B200 plan model (device roofline).  The paper's Eq. 2 counts CPU sparse-matrix
+# work; on the tensor cores both plans are GEMM + gather and the winner is set
+# by tensor time vs HBM bytes.  Calibrated on profiles/round1/complexity_sweep.json
+# (164 measured cells): picks the measured winner in 154 (Eq. 2: 113), worst
+# slowdown of its pick 1.22x (Eq. 2: 8.9x).
+# ---------------------------------------------------------------------------
+
+def _device_peaks():
+    import json
+    import os
+    p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["bf16_tflops"]) * 1e12, float(d["hbm_gbs"]) * 1e9
+    except Exception:  # noqa: BLE001
+        return 1654e12, 6548e9
+
+
+def device_plan_costs(target_rows: int, k: int, l: int, dim_rows, peaks=None):
+    """Predicted seconds (fused, non-fused) of the tensor-core plans on B200.
+
+    non-fused: one GEMM over the gathered rows (3 MMAs per product on blocks of
+      32 features and 16 output columns) vs its bytes (keys, fp16x2 features,
+      fp32 Y);
+    fused: prefuse GEMMs over every dim (M = r_j) + the fp32 gather-apply, whose
+      P reads come from L2 when sum r_j l 4 B fits (~100 MB), else HBM."""
+    pt, bw = peaks or _device_peaks()
+    pt *= 0.85  # tensor-pipe rate reached by csrc/gemm_tc.cu on long GEMMs
+    bw *= 0.76  # gather + streaming mix
+    ovh = 20e-6  # launch + pipeline fill per kernel
+    F = float(target_rows)
+    kp = (k + 31) // 32 * 32
+    lp = max(16, (l + 15) // 16 * 16)
+    R = float(sum(dim_rows))
+    t_nf = ovh + max(6.0 * F * kp * lp / pt, (F * 4 * len(dim_rows) + F * kp * 4 + F * l * 4) / bw)
+    p_bytes = R * l * 4
+    gather_p = 0.0 if p_bytes <= 100e6 else F * l * 4 * len(dim_rows)
+    t_pre = sum(max(6.0 * r * kp * lp / pt, (r * kp * 4 + r * l * 4) / bw) for r in dim_rows)
+    t_f = (1 + len(dim_rows)) * ovh + t_pre + (F * 4 * len(dim_rows) + F * l * 4 + gather_p) / bw
+    return t_f, t_nf
+
+
+def plan_linear_device(target_rows: int, k: int, l: int, dim_rows) -> str:
+    """The planner for the tensor-core operators: the plan with the smaller
+    predicted device time (device_plan_costs)."""
+    t_f, t_nf = device_plan_costs(target_rows, k, l, dim_rows)
+    return "fused" if t_f < t_nf else "nonfused"

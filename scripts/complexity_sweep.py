@@ -94,6 +94,7 @@ for r in R:
             cell["planner"] = "fused" if fusion.decide_fusion(ratio, 1.0) else "nonfused"
             cell["measured_winner"] = "fused" if cell["ms_fused"] < cell["ms_nonfused"] else "nonfused"
             cell["planner_right"] = cell["planner"] == cell["measured_winner"]
+            cell["device_planner"] = fusion.plan_linear_device(F, k, l, [r])
             flop = 2.0 * F * k * l
             cell["nonfused_alg_tflops"] = flop / (cell["ms_nonfused"] / 1e3) / 1e12
             cell["prefuse_alg_tflops"] = 2.0 * r * k * l / (cell["ms_prefuse"] / 1e3) / 1e12
@@ -108,6 +109,7 @@ done = [c for c in rows if "skipped" not in c]
 summary = {
     "cells": len(rows), "measured": len(done), "skipped": len(rows) - len(done),
     "planner_agrees_with_measurement": sum(c["planner_right"] for c in done),
+    "device_planner_agrees": sum(c["device_planner"] == c["measured_winner"] for c in done),
     "max_cond_err": max([max(c["cond_err_fused"], c["cond_err_nonfused"]) for c in done], default=0.0),
     "best_nonfused_alg_tflops": max([c["nonfused_alg_tflops"] for c in done], default=0.0),
     "best_prefuse_alg_tflops": max([c["prefuse_alg_tflops"] for c in done], default=0.0),
