@@ -237,6 +237,26 @@ int laq_tc_gemm(laq_ctx* ctx, const laq_tc_features* f, const int32_t* const* d_
 int laq_apply_fused_linear_f32(laq_ctx* ctx, int32_t n_parts, const int32_t* const* d_idx, int64_t rows,
                                const float* const* d_partials, int64_t l, float* d_out);
 
+/* ---- decision-tree fusion (fusion.hpp:20-55, mlops.hpp:49-80) ----------
+ * laq_tree_partial: tree_partial (fusion.cpp:39-47) for one dimension B
+ * (rows x cols fp64): P[r, c] = sum over nodes n (in order) with
+ * B[r, node_col[n]] * scale[n] > thr[n] of 1 * path_rows[n, c]; node_col[n] = -1
+ * for a node whose feature the dim does not place (reads 0); scale[n] = the
+ * placement value (NULL = all 1).  Bit-identical to the
+ * reference.  predict_tree's scores (mlops.cpp:254-268) are the same call on T
+ * with every node.  d_out rows x l.  p <= 2048 nodes.  Synchronises.
+ * laq_apply_fused_tree: apply_fused_tree (fusion.cpp:146-168) /
+ * predict_tree's decode (mlops.cpp:269-280): scores = ((P_0[i_0] + P_1[i_1]) +
+ * ...), label = labels[c] of the unique leaf with scores[c] == path_score[c].
+ * d_idx NULL (or d_idx[j] NULL) = identity rows.  LAQ_ERR_MODEL for the first
+ * row matching no leaf or several (*h_bad_row, *h_bad_several).  Synchronises. */
+int laq_tree_partial(laq_ctx* ctx, const double* d_B, int64_t rows, int64_t cols, int64_t p,
+                     const int64_t* h_node_col, const double* h_node_scale, const double* h_thr,
+                     const double* h_path_rows, int64_t l, double* d_out);
+int laq_apply_fused_tree(laq_ctx* ctx, int32_t n_parts, const int64_t* const* d_idx, int64_t rows,
+                         const double* const* d_partials, int64_t l, const double* h_path_score,
+                         const int64_t* h_labels, int64_t* d_out, int64_t* h_bad_row, int32_t* h_bad_several);
+
 /* ---- aggregate-MM (laqops.hpp:112-166) --------------------------------- */
 
 /* groupby_sum_single (laqops.cpp:376-413): join R and S on key, sum R's values

@@ -542,6 +542,146 @@ DenseMat apply_fused_linear(std::span<const SparseCsr> i_maps, const FusedLinear
   return out;
 }
 
+// ---- decision trees (fusion.cpp:39-47, 128-179) ------------------------------
+namespace {
+// tree_partial on the device: node n tests B[r, c_n] * s_n > v_n where c_n is
+// the dim-local column placed on the node's feature and s_n the placement
+// value times the feature-map value (the single term of spmm(M_j, F_j)).
+DenseMat device_tree_partial(const DenseMat& dim, const ops::ColumnMap& col_map, const TreeDimBlock& part,
+                             index_t leaves) {
+  if (dim.cols() != col_map.mat.rows) throw ShapeError("fusion: column map does not fit dim table");
+  const SparseCsr& F = part.feature_map;
+  const index_t p = F.cols;
+  if (static_cast<index_t>(part.thresholds.size()) != p || part.path_rows.rows() != p)
+    throw ShapeError("tree_partial: block sizes");
+  std::vector<index_t> node_feat(static_cast<std::size_t>(p), -1);
+  std::vector<double> node_w(static_cast<std::size_t>(p), 0.0);
+  for (index_t g = 0; g < F.rows; ++g)
+    for (index_t jj = F.row_ptr[g]; jj < F.row_ptr[g + 1]; ++jj) {
+      if (node_feat[F.col_idx[jj]] >= 0)
+        throw Error("laq_b200: tree block with several features per node is outside the device path");
+      node_feat[F.col_idx[jj]] = g;
+      node_w[F.col_idx[jj]] = F.values[jj];
+    }
+  // global feature -> (local column, placement value)
+  std::vector<index_t> loc(static_cast<std::size_t>(col_map.mat.cols), -1);
+  std::vector<double> val(static_cast<std::size_t>(col_map.mat.cols), 0.0);
+  for (index_t c = 0; c < col_map.mat.rows; ++c)
+    for (index_t jj = col_map.mat.row_ptr[c]; jj < col_map.mat.row_ptr[c + 1]; ++jj) {
+      loc[col_map.mat.col_idx[jj]] = c;
+      val[col_map.mat.col_idx[jj]] = col_map.mat.values[jj];
+    }
+  std::vector<int64_t> node_col(static_cast<std::size_t>(p), -1);
+  std::vector<double> scale(static_cast<std::size_t>(p), 1.0);
+  for (index_t n = 0; n < p; ++n) {
+    const index_t g = node_feat[n];
+    if (g >= 0 && g < col_map.mat.cols && loc[g] >= 0) {
+      node_col[n] = loc[g];
+      scale[n] = val[g] * node_w[n];
+    }
+  }
+  DenseMat out(dim.rows(), leaves);
+  if (out.data().empty()) return out;
+  if (part.path_rows.cols() != leaves) throw ShapeError("tree_partial: leaf count");
+  Dev<double> db(dim.data()), dout(out.data().size());
+  check(laq_tree_partial(ctx(), db.p, dim.rows(), dim.cols(), p, node_col.data(), scale.data(),
+                         part.thresholds.data(), part.path_rows.data().data(), leaves, dout.p));
+  dout.down(out.data().data(), out.data().size());
+  return out;
+}
+
+// Decode ((scores) == h) -> labels on the device (identity rows over one score matrix,
+// or row maps over the partials); ModelError names the first offending row.
+std::vector<std::int64_t> device_decode(const std::vector<const double*>& parts, const std::vector<const int64_t*>* idx,
+                                        index_t rows, std::span<const double> path_score,
+                                        std::span<const std::int64_t> labels, const char* what) {
+  std::vector<std::int64_t> out(static_cast<std::size_t>(rows));
+  if (rows == 0) return out;
+  Dev<std::int64_t> dy(static_cast<std::size_t>(rows));
+  int64_t bad = -1;
+  int32_t several = 0;
+  const int rc = laq_apply_fused_tree(ctx(), static_cast<int32_t>(parts.size()), idx ? idx->data() : nullptr, rows,
+                                      parts.data(), static_cast<int64_t>(path_score.size()), path_score.data(),
+                                      labels.data(), dy.p, &bad, &several);
+  if (rc == LAQ_ERR_MODEL)
+    throw ModelError(std::string(what) + ": row " + std::to_string(bad) +
+                     (several ? " matches several leaves" : " matches no leaf"));
+  check(rc);
+  dy.down(out.data(), out.size());
+  return out;
+}
+}  // namespace
+
+FusedTree prefuse_tree(std::span<const DenseMat> dims, std::span<const ops::ColumnMap> col_maps,
+                       std::span<const TreeDimBlock> parts, std::span<const double> path_score,
+                       std::span<const std::int64_t> labels) {
+  if (dims.empty() || dims.size() != col_maps.size() || dims.size() != parts.size())
+    throw ShapeError("prefuse_tree: input list lengths");
+  if (path_score.size() != labels.size()) throw ShapeError("prefuse_tree: score/label lengths");
+  if (!col_maps.empty()) check_placements(col_maps, col_maps[0].mat.cols);
+  FusedTree f;
+  f.path_score.assign(path_score.begin(), path_score.end());
+  f.labels.assign(labels.begin(), labels.end());
+  for (std::size_t j = 0; j < dims.size(); ++j)
+    f.partials.push_back(device_tree_partial(dims[j], col_maps[j], parts[j], static_cast<index_t>(labels.size())));
+  return f;
+}
+
+std::vector<std::int64_t> apply_fused_tree(std::span<const SparseCsr> i_maps, const FusedTree& f) {
+  if (i_maps.empty() || i_maps.size() != f.partials.size())
+    throw ShapeError("apply_fused_tree: map/partial list lengths");
+  const index_t leaves = f.partials[0].cols();
+  if (static_cast<index_t>(f.path_score.size()) < leaves || f.labels.size() < f.path_score.size())
+    throw ShapeError("apply_fused_tree: score/label lengths");
+  bool row_maps = true;
+  for (const SparseCsr& m : i_maps) row_maps = row_maps && is_row_map(m) && m.rows == i_maps[0].rows;
+  for (const DenseMat& p : f.partials) row_maps = row_maps && p.cols() == leaves;
+  if (row_maps) {  // fused gather-sum + leaf select in one kernel
+    std::vector<Dev<std::int64_t>> idx;
+    std::vector<Dev<double>> parts;
+    std::vector<const int64_t*> pi;
+    std::vector<const double*> pp;
+    for (std::size_t j = 0; j < i_maps.size(); ++j) {
+      idx.emplace_back(i_maps[j].col_idx);
+      parts.emplace_back(f.partials[j].data());
+      pi.push_back(idx.back().p);
+      pp.push_back(parts.back().p);
+    }
+    return device_decode(pp, &pi, i_maps[0].rows, std::span<const double>(f.path_score.data(), leaves), f.labels,
+                         "apply_fused_tree");
+  }
+  // general CSR maps: spmm_dense (device) + add_inplace, then the device decode
+  DenseMat scores = spmm_dense(i_maps[0], f.partials[0]);
+  for (std::size_t j = 1; j < i_maps.size(); ++j) {
+    const DenseMat x = spmm_dense(i_maps[j], f.partials[j]);
+    for (std::size_t e = 0; e < scores.data().size(); ++e) scores.data()[e] += x.data()[e];
+  }
+  Dev<double> ds(scores.data());
+  return device_decode({ds.p}, nullptr, scores.rows(),
+                       std::span<const double>(f.path_score.data(), static_cast<std::size_t>(scores.cols())),
+                       f.labels, "apply_fused_tree");
+}
+
+FusedTree refresh_partial(FusedTree f, index_t dim_index, const DenseMat& new_dim, const ops::ColumnMap& col_map,
+                          const TreeDimBlock& part) {
+  if (dim_index < 0 || dim_index >= static_cast<index_t>(f.partials.size()))
+    throw IndexError("refresh_partial: dim index out of range");
+  DenseMat partial = device_tree_partial(new_dim, col_map, part, part.path_rows.cols());
+  if (partial.cols() != static_cast<index_t>(f.path_score.size())) throw ShapeError("refresh_partial: leaf count changed");
+  f.partials[dim_index] = std::move(partial);
+  return f;
+}
+
+FusedLinear refresh_partial(FusedLinear f, index_t dim_index, const DenseMat& new_dim, const ops::ColumnMap& col_map,
+                            const ml::LinearOperator& op) {
+  if (dim_index < 0 || dim_index >= static_cast<index_t>(f.partials.size()))
+    throw IndexError("refresh_partial: dim index out of range");
+  if (op.mat.cols() != f.out_width) throw ShapeError("refresh_partial: operator width changed");
+  if (new_dim.cols() != col_map.mat.rows) throw ShapeError("fusion: column map does not fit dim table");
+  f.partials[dim_index] = dense_matmul(new_dim, spmm_dense(col_map.mat, op.mat));  // linear_partial on the device
+  return f;
+}
+
 double speedup_ratio_linear(const CostInputs& c) {
   if (c.tree_features <= 0 || c.dim_rows.empty()) throw DomainError("cost model: all inputs must be positive");
   double r = 0;
@@ -571,6 +711,34 @@ bool decide_fusion(double ratio, double threshold) {
 // ============================================================================
 // cli.hpp: the query plan driver on the device
 // ============================================================================
+// ============================================================================
+// mlops.hpp: predict_tree (mlops.cpp:254-280) -- the one-block tree partial over
+// T with every node, then the device decode
+// ============================================================================
+namespace ml {
+std::vector<std::int64_t> predict_tree(const DenseMat& t, const TreeLA& m) {
+  if (t.cols() != m.feature_width())
+    throw ShapeError("predict_tree: input width " + std::to_string(t.cols()) + " vs model " +
+                     std::to_string(m.feature_width()));
+  fusion::TreeDimBlock all;
+  all.feature_map = m.feature_map;
+  all.thresholds = m.thresholds;
+  all.path_rows = m.paths;
+  ops::ColumnMap identity;
+  identity.mat.rows = identity.mat.cols = t.cols();
+  identity.mat.row_ptr.resize(static_cast<std::size_t>(t.cols()) + 1);
+  std::iota(identity.mat.row_ptr.begin(), identity.mat.row_ptr.end(), index_t{0});
+  identity.mat.col_idx.resize(static_cast<std::size_t>(t.cols()));
+  std::iota(identity.mat.col_idx.begin(), identity.mat.col_idx.end(), index_t{0});
+  identity.mat.values.assign(static_cast<std::size_t>(t.cols()), 1.0);
+  const DenseMat scores = fusion::device_tree_partial(t, identity, all, m.leaf_count());
+  Dev<double> ds(scores.data());
+  return fusion::device_decode({ds.p}, nullptr, scores.rows(),
+                               std::span<const double>(m.path_score.data(), static_cast<std::size_t>(scores.cols())),
+                               m.labels, "predict_tree");
+}
+}  // namespace ml
+
 namespace cli {
 
 DenseMat run_query_laq(const StarSchema& data, const bench::QuerySpec& q, StageTimes* stages) {

@@ -28,6 +28,14 @@ class MappingError(Exception):
     pass
 
 
+class TreeError(Exception):
+    pass
+
+
+class ModelError(Exception):
+    pass
+
+
 class ShapeError(Exception):
     pass
 
@@ -211,6 +219,99 @@ def ffn_predict(idx, dims, placements, k, W1, W2, exact_order=False):
     Y = mm(R, W2)
     bound = (np.abs(T) @ np.abs(W1)) @ np.abs(W2) + R @ np.abs(W2)
     return Y, bound
+
+
+# ---------------------------------------------------------------------------
+# decision trees (mlops.cpp:188-280, fusion.cpp:39-168)
+# A tree is a dict of node arrays (TreeNode, mlops.hpp:18-25): is_leaf,
+# feature, threshold, true_child, false_child, label; root = node 0.
+# ---------------------------------------------------------------------------
+
+def compile_tree(tree, input_width):
+    """mlops.cpp:188-243: pre-order walk, true branch first.  Returns
+    (node_feature[p], thresholds[p], paths p x l, path_score[l], labels[l])."""
+    is_leaf = np.asarray(tree["is_leaf"])
+    for i in range(len(is_leaf)):
+        if not is_leaf[i] and tree["feature"][i] >= input_width:
+            raise TreeError(f"tree feature {tree['feature'][i]} exceeds input width {input_width}")
+    feats, thr, cols, score, labels = [], [], [], [], []
+    stack = [(0, [], -1, 0.0)]
+    while stack:
+        nid, path, parent, sign = stack.pop()
+        path = path + ([(parent, sign)] if parent >= 0 else [])
+        if is_leaf[nid]:
+            cols.append(path)
+            score.append(float(sum(1 for _, sg in path if sg > 0)))
+            labels.append(int(tree["label"][nid]))
+        else:
+            pos = len(feats)
+            feats.append(int(tree["feature"][nid]))
+            thr.append(float(tree["threshold"][nid]))
+            stack.append((int(tree["false_child"][nid]), path, pos, -1.0))
+            stack.append((int(tree["true_child"][nid]), path, pos, 1.0))
+    H = np.zeros((len(feats), len(labels)))
+    for leaf, path in enumerate(cols):
+        for node, sg in path:
+            H[node, leaf] = sg
+    return (np.array(feats, np.int64), np.array(thr), H, np.array(score), np.array(labels, np.int64))
+
+
+def _scores_to_labels(scores, path_score, labels, what):
+    """mlops.cpp:269-280 / fusion.cpp:154-167: the unique leaf with score == h."""
+    eq = scores == np.asarray(path_score)[None, :]
+    cnt = eq.sum(axis=1)
+    bad = np.nonzero(cnt != 1)[0]
+    if len(bad):
+        i = int(bad[0])
+        raise ModelError(f"{what}: row {i} matches " + ("several leaves" if cnt[i] > 1 else "no leaf"))
+    return np.asarray(labels)[np.argmax(eq, axis=1)]
+
+
+def _node_scores(X, node_col, thr, H):
+    """dense_matmul((X F > v), H) with dense_matmul's sequential node order and
+    zero skipping (matrix.cpp:158-174): exact for any H."""
+    bits = np.stack([(X[:, c] if c >= 0 else np.zeros(len(X))) > t for c, t in zip(node_col, thr)], axis=1) \
+        if len(node_col) else np.zeros((len(X), 0), bool)
+    out = np.zeros((len(X), H.shape[1]))
+    for n in range(H.shape[0]):
+        b = bits[:, n]
+        if b.any():
+            out[b] = out[b] + 1.0 * H[n][None, :]
+    return out
+
+
+def predict_tree(T, compiled):
+    """mlops.cpp:254-280."""
+    feats, thr, H, score, labels = compiled
+    T = np.asarray(T, np.float64)
+    return _scores_to_labels(_node_scores(T, feats, thr, H), score, labels, "predict_tree")
+
+
+def partition_tree(compiled, feature_owner, dim_count):
+    """fusion.cpp:79-126 -> per dim (node_ids, node_feature, thresholds, path_rows)."""
+    feats, thr, H, _, _ = compiled
+    blocks = [[] for _ in range(dim_count)]
+    for node, f in enumerate(feats):
+        o = int(feature_owner[f])
+        if o < 0 or o >= dim_count:
+            raise MappingError(f"partition_tree: feature {f} has no owning dim")
+        blocks[o].append(node)
+    return [(np.array(b, np.int64), feats[b], thr[b], H[b]) for b in blocks]
+
+
+def prefuse_tree(dims, placements, parts):
+    """fusion.cpp:39-47, 128-144: P_j = ((B_j M_j F_j) > v_j) H_j."""
+    out = []
+    for B, pl, (_, nf, nt, H) in zip(dims, placements, parts):
+        inv = {int(g): c for c, g in enumerate(pl)}
+        cols = [inv.get(int(f), -1) for f in nf]
+        out.append(_node_scores(np.asarray(B, np.float64), cols, nt, H))
+    return out
+
+
+def apply_fused_tree(idx, partials, path_score, labels):
+    """fusion.cpp:146-168."""
+    return _scores_to_labels(apply_fused_linear(idx, partials), path_score, labels, "apply_fused_tree")
 
 
 # ---------------------------------------------------------------------------

@@ -81,6 +81,9 @@ def lib():
             "ref_fused_pipeline": [i32, vp, i64, vp, vp, vp, vp, vp, i64, vp, vp, vp],
             "ref_speedup_ratio": [i32, i64, i64, i64, i64, vp, i32, vp],
             "ref_decide_fusion": [dbl, dbl, vp],
+            "ref_gen_tree": [i64, i64, i64, C.c_uint64, i64, vp, vp, vp, vp, vp, vp, vp],
+            "ref_predict_tree": [i32, vp, vp, vp, vp, vp, vp, vp, i64, i64, vp],
+            "ref_fused_tree": [i32, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp, i64, vp, vp, i64, vp, vp],
         }
         for name, args in sigs.items():
             getattr(L, name).argtypes = args
@@ -419,3 +422,55 @@ def decide_fusion(ratio, threshold=1.0):
     out = C.c_int()
     _check(lib().ref_decide_fusion(C.c_double(ratio), C.c_double(threshold), C.byref(out)))
     return bool(out.value)
+
+
+# ---- decision trees -------------------------------------------------------------
+# A tree is a dict of node arrays: is_leaf (int32), feature, threshold, true_child,
+# false_child, label (TreeNode, mlops.hpp:18-25; root = node 0).
+
+def _tree_args(t):
+    a = [np.ascontiguousarray(t["is_leaf"], np.int32), np.ascontiguousarray(t["feature"], np.int64),
+         np.ascontiguousarray(t["threshold"], np.float64), np.ascontiguousarray(t["true_child"], np.int64),
+         np.ascontiguousarray(t["false_child"], np.int64), np.ascontiguousarray(t["label"], np.int64)]
+    return a, [x.ctypes.data for x in a]
+
+
+def gen_tree(k, p, leaves, seed):
+    """bench::gen_tree (benchgen.cpp:463-...)."""
+    cap = 2 * leaves + 1
+    t = {"is_leaf": np.zeros(cap, np.int32), "feature": np.zeros(cap, np.int64), "threshold": np.zeros(cap),
+         "true_child": np.zeros(cap, np.int64), "false_child": np.zeros(cap, np.int64),
+         "label": np.zeros(cap, np.int64)}
+    n = C.c_int64()
+    _check(lib().ref_gen_tree(k, p, leaves, seed, cap, *[t[x].ctypes.data for x in
+                                                          ("is_leaf", "feature", "threshold", "true_child",
+                                                           "false_child", "label")], C.byref(n)))
+    return {x: v[:n.value].copy() for x, v in t.items()}
+
+
+def predict_tree(tree, T):
+    keep, ptrs = _tree_args(tree)
+    T = np.ascontiguousarray(T, np.float64)
+    out = np.zeros(T.shape[0], np.int64)
+    _check(lib().ref_predict_tree(len(keep[0]), *ptrs, _pf(T), T.shape[0], T.shape[1], _p64(out)))
+    return out
+
+
+def fused_tree(tree, dims, placements, k, feature_owner, idx=None):
+    """Returns (labels or None, partials) through prefuse_tree / apply_fused_tree."""
+    keep, ptrs = _tree_args(tree)
+    dims_, pls, rows, cols = _dims_args(dims, placements)
+    owner = np.ascontiguousarray(feature_owner, np.int64)
+    leaves = int(np.sum(keep[0] != 0))
+    parts = [np.zeros((d.shape[0], leaves)) for d in dims_]
+    if idx is not None:
+        idx = [np.ascontiguousarray(i, np.int64) for i in idx]
+        m = len(idx[0])
+        out = np.zeros(m, np.int64)
+        ip = _ptr_array(idx, C.c_int64)
+    else:
+        m, out, ip = 0, None, None
+    _check(lib().ref_fused_tree(len(keep[0]), *ptrs, len(dims_), _ptr_array(dims_, C.c_double), rows, cols,
+                                _ptr_array(pls, C.c_int64), k, _p64(owner), ip, m,
+                                _p64(out) if out is not None else None, _ptr_array(parts, C.c_double)))
+    return out, parts

@@ -609,6 +609,70 @@ int ref_fused_pipeline(int n_links, const int64_t* const* fks, int64_t n, const 
 }
 
 // ---- cost model (fusion.cpp:259-302) --------------------------------------
+// ---- decision trees (mlops.cpp:188-280, fusion.cpp:39-168, benchgen.cpp:463-...) ----
+namespace {
+ml::TreeModel make_tree(int n_nodes, const int32_t* is_leaf, const int64_t* feature, const double* thr,
+                        const int64_t* tchild, const int64_t* fchild, const int64_t* label) {
+  ml::TreeModel t;
+  for (int i = 0; i < n_nodes; ++i)
+    t.nodes.push_back({is_leaf[i] != 0, feature[i], thr[i], tchild[i], fchild[i], label[i]});
+  return t;
+}
+}  // namespace
+
+// gen_tree -> node arrays (capacity cap); *n = node count.
+int ref_gen_tree(int64_t k, int64_t p, int64_t leaves, uint64_t seed, int64_t cap, int32_t* is_leaf,
+                 int64_t* feature, double* thr, int64_t* tchild, int64_t* fchild, int64_t* label, int64_t* n) {
+  return guard([&] {
+    const ml::TreeModel t = bench::gen_tree(k, p, leaves, seed);
+    *n = static_cast<int64_t>(t.nodes.size());
+    if (*n > cap) throw CapacityError("ref_gen_tree: capacity");
+    for (size_t i = 0; i < t.nodes.size(); ++i) {
+      const auto& nd = t.nodes[i];
+      is_leaf[i] = nd.is_leaf;
+      feature[i] = nd.feature;
+      thr[i] = nd.threshold;
+      tchild[i] = nd.true_child;
+      fchild[i] = nd.false_child;
+      label[i] = nd.label;
+    }
+  });
+}
+
+// compile_tree + predict_tree over T (rows x k).
+int ref_predict_tree(int n_nodes, const int32_t* is_leaf, const int64_t* feature, const double* thr,
+                     const int64_t* tchild, const int64_t* fchild, const int64_t* label, const double* T,
+                     int64_t rows, int64_t k, int64_t* out) {
+  return guard([&] {
+    const ml::TreeLA m = ml::compile_tree(make_tree(n_nodes, is_leaf, feature, thr, tchild, fchild, label), k);
+    const DenseMat t(rows, k, std::vector<double>(T, T + rows * k));
+    const auto y = ml::predict_tree(t, m);
+    std::copy(y.begin(), y.end(), out);
+  });
+}
+
+// compile_tree -> partition_tree(feature_owner) -> prefuse_tree -> apply_fused_tree over
+// row maps idx (m rows).  partials[j] receives r_j x leaves (may be NULL).
+int ref_fused_tree(int n_nodes, const int32_t* is_leaf, const int64_t* feature, const double* thr,
+                   const int64_t* tchild, const int64_t* fchild, const int64_t* label, int n_dims,
+                   const double* const* dims, const int64_t* rows, const int64_t* cols,
+                   const int64_t* const* placements, int64_t k, const int64_t* feature_owner,
+                   const int64_t* const* idx, int64_t m, int64_t* out, double* const* partials) {
+  return guard([&] {
+    const ml::TreeLA t = ml::compile_tree(make_tree(n_nodes, is_leaf, feature, thr, tchild, fchild, label), k);
+    StarMats s = make_mats(n_dims, dims, rows, cols, placements, k, idx, m);
+    const auto parts = fusion::partition_tree(t, std::vector<index_t>(feature_owner, feature_owner + k), n_dims);
+    const auto f = fusion::prefuse_tree(s.dims, s.maps, parts, t.path_score, t.labels);
+    if (partials)
+      for (int j = 0; j < n_dims; ++j)
+        if (partials[j]) std::copy(f.partials[j].data().begin(), f.partials[j].data().end(), partials[j]);
+    if (idx && out) {
+      const auto y = fusion::apply_fused_tree(s.imaps, f);
+      std::copy(y.begin(), y.end(), out);
+    }
+  });
+}
+
 int ref_speedup_ratio(int tree, int64_t i, int64_t k, int64_t l, int64_t p, const int64_t* dims,
                       int n, double* out) {
   return guard([&] {

@@ -78,6 +78,8 @@ _SIGS = {
     "laq_tc_features_destroy": (C.c_int, [vp]),
     "laq_tc_gemm": (C.c_int, [vp, vp, vp, i64, vp, i64, vp]),
     "laq_apply_fused_linear_f32": (C.c_int, [vp, i32, vp, i64, vp, i64, vp]),
+    "laq_tree_partial": (C.c_int, [vp, vp, i64, i64, i64, i64p, f64p, f64p, f64p, i64, vp]),
+    "laq_apply_fused_tree": (C.c_int, [vp, i32, vp, i64, vp, i64, f64p, i64p, vp, i64p, i32p]),
     "laq_groupby_sum_single": (C.c_int, [vp, vp, vp, i64, vp, vp, i64, vp, vp, i64p]),
     "laq_groupby_sum_multi": (C.c_int, [vp, i32, vp, vp, i64, vp, vp, i64, i64p]),
     "laq_star_create": (C.c_int, [vp, C.POINTER(vp)]),

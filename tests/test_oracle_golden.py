@@ -177,3 +177,32 @@ def test_live_reference_agrees_with_restatement():
         c, d = O.mm_join(r, s)
         assert np.array_equal(a, c) and np.array_equal(b, d)
         assert np.array_equal(ref.build_key_domain(r, s), O.build_key_domain(r, s))
+
+
+def test_tree_oracle_matches_reference():
+    """The numpy restatement of compile_tree / predict_tree / partition_tree /
+    prefuse_tree / apply_fused_tree against the reference compiled from its own
+    sources (bench::gen_tree trees): labels and partials bit-identical."""
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(1)
+    for trial in range(12):
+        k = int(rng.integers(2, 40))
+        leaves = int(rng.integers(2, 60))
+        t = ref.gen_tree(k, int(rng.integers(1, k + 1)), leaves, trial)
+        X = rng.random((300, k))
+        assert np.array_equal(ref.predict_tree(t, X), O.predict_tree(X, O.compile_tree(t, k)))
+        perm = rng.permutation(k)
+        cut = int(rng.integers(1, k)) if k > 1 else k
+        pl = [perm[:cut], perm[cut:]] if cut < k else [perm]
+        owner = np.zeros(k, np.int64)
+        for j, p in enumerate(pl):
+            owner[p] = j
+        dims = [rng.random((int(rng.integers(5, 50)), len(p))) for p in pl]
+        idx = [rng.integers(0, d.shape[0], 200) for d in dims]
+        ya, pa = ref.fused_tree(t, dims, pl, k, owner, idx)
+        comp = O.compile_tree(t, k)
+        pb = O.prefuse_tree(dims, pl, O.partition_tree(comp, owner, len(dims)))
+        assert all(np.array_equal(x, y) for x, y in zip(pa, pb))
+        assert np.array_equal(ya, O.apply_fused_tree(idx, pb, comp[3], comp[4]))
