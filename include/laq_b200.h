@@ -346,6 +346,8 @@ int laq_plan_build_codes(laq_ctx* ctx, laq_plan* plan);
 int laq_plan_scan(laq_ctx* ctx, laq_plan* plan, int64_t* d_acc, int32_t accumulate);
 /* Bytes of fact columns the scan streams per row (the roofline unit). */
 int64_t laq_plan_bytes_per_row(const laq_plan* plan);
+/* Joins the plan's scan actually probes (after eliding covered filter-free links). */
+int32_t laq_plan_scanned_links(const laq_plan* plan);
 /* Turn an accumulator (host copy, e.g. after an all-reduce) into the
  * run_query_laq result rows [group cols..., sum] (row-major), present groups
  * only, ascending (groupby_sum_multi + sort_rows; laqops.cpp:415-478).  A plain

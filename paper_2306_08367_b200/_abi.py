@@ -92,6 +92,7 @@ _SIGS = {
     "laq_plan_build_codes": (C.c_int, [vp, vp]),
     "laq_plan_scan": (C.c_int, [vp, vp, vp, i32]),
     "laq_plan_bytes_per_row": (i64, [vp]),
+    "laq_plan_scanned_links": (i32, [vp]),
     "laq_plan_emit": (C.c_int, [vp, i64p, f64p, i64, i64p, i64p]),
     "laq_plan_destroy": (C.c_int, [vp]),
     "laq_run_query": (C.c_int, [vp, vp, C.POINTER(QueryDesc), f64p, i64, i64p, i64p]),

@@ -19,6 +19,10 @@
 //   * per-group (count, sum) bins live in shared memory as 32-bit counters
 //     (native ATOMS.ADD; 64-bit shared atomics are CAS loops on this part),
 //     spilled into the global 64-bit accumulator before they could wrap.
+// scan_stream_kernel (default): register double-buffered 16-byte loads of 4 rows
+//   per thread.  Opt-in (LAQ_PACK=1): fact columns whose value range fits 8 or
+//   16 bits are read byte-packed relative to their minimum (Q1.x: 6 bytes per
+//   row instead of 16); slower as measured, see ssb.cu.
 // scan_ldg_kernel (fallback): plain vectorised loads, any 4-byte alignment.
 #pragma once
 
@@ -57,6 +61,14 @@ struct FactGroup {
   int64_t mn, stride;
 };
 
+// A fact column as the stream kernel reads it: int32, or byte-packed (1 or 2
+// bytes per row) relative to the column minimum `off` when the value range fits.
+struct Col {
+  const void* p;
+  int w;        // bytes per row: 1, 2 or 4
+  int32_t off;  // value = stored + off (w < 4)
+};
+
 struct ScanArgs {
   int64_t n;
   const int32_t* fk[kMaxLinks];
@@ -65,6 +77,10 @@ struct ScanArgs {
   int n_fgroups;
   FactGroup fg[kMaxFactGroups];
   const int32_t* measure;  // nullptr: count only
+  // stream kernel views of the same columns (packed where the range allows)
+  Col fkc[kMaxLinks];
+  Col ffc[kMaxFactFilters];
+  Col mc;
   int64_t n_groups;
   unsigned long long* acc;  // [2*G]: count, sum
   // pipe kernel layout
@@ -489,6 +505,36 @@ __device__ __forceinline__ int4 ld4_padded(const int32_t* p, int64_t row0, int64
   return row0 < n ? __ldcs(reinterpret_cast<const int4*>(p + row0)) : make_int4(0, 0, 0, 0);
 }
 
+// 4 consecutive rows of a (possibly packed) column; row0 is a multiple of 4 and
+// every allocation on this path has >= 16 readable bytes past the end.  The raw
+// words are kept as loaded (the register double buffer) and unpacked only when
+// the rows are processed, an iteration later, so the load latency stays hidden.
+__device__ __forceinline__ int4 ld4_raw(const Col& c, int64_t row0, int64_t n) {
+  if (row0 >= n) return make_int4(0, 0, 0, 0);
+  if (c.w == 1) {
+    const uint32_t v = __ldcs(reinterpret_cast<const unsigned int*>(static_cast<const uint8_t*>(c.p) + row0));
+    return make_int4(static_cast<int32_t>(v), 0, 0, 0);
+  }
+  if (c.w == 2) {
+    const uint2 v = __ldcs(reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(c.p) + row0));
+    return make_int4(static_cast<int32_t>(v.x), static_cast<int32_t>(v.y), 0, 0);
+  }
+  return __ldcs(reinterpret_cast<const int4*>(static_cast<const int32_t*>(c.p) + row0));
+}
+__device__ __forceinline__ int4 unpack4(const int4& r, const Col& c) {
+  if (c.w == 1) {
+    const uint32_t v = static_cast<uint32_t>(r.x);
+    return make_int4(static_cast<int32_t>(v & 0xffu) + c.off, static_cast<int32_t>((v >> 8) & 0xffu) + c.off,
+                     static_cast<int32_t>((v >> 16) & 0xffu) + c.off, static_cast<int32_t>(v >> 24) + c.off);
+  }
+  if (c.w == 2) {
+    const uint32_t x = static_cast<uint32_t>(r.x), y = static_cast<uint32_t>(r.y);
+    return make_int4(static_cast<int32_t>(x & 0xffffu) + c.off, static_cast<int32_t>(x >> 16) + c.off,
+                     static_cast<int32_t>(y & 0xffffu) + c.off, static_cast<int32_t>(y >> 16) + c.off);
+  }
+  return r;
+}
+
 template <int NL, int NF, int MODE>
 __global__ void __launch_bounds__(kStreamThreads) scan_stream_kernel(const ScanArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -515,10 +561,10 @@ __global__ void __launch_bounds__(kStreamThreads) scan_stream_kernel(const ScanA
 
   int4 kv[NL > 0 ? NL : 1], fv[NF > 0 ? NF : 1], mv = make_int4(0, 0, 0, 0);
 #pragma unroll
-  for (int j = 0; j < NL; ++j) kv[j] = ld4_padded(a.fk[j], row0, a.n);
+  for (int j = 0; j < NL; ++j) kv[j] = ld4_raw(a.fkc[j], row0, a.n);
 #pragma unroll
-  for (int f = 0; f < NF; ++f) fv[f] = ld4_padded(a.ff[f].col, row0, a.n);
-  if (a.measure) mv = ld4_padded(a.measure, row0, a.n);
+  for (int f = 0; f < NF; ++f) fv[f] = ld4_raw(a.ffc[f], row0, a.n);
+  if (a.measure) mv = ld4_raw(a.mc, row0, a.n);
 
   unsigned long long r_cnt = 0, r_sum = 0;
   for (int64_t it = 0; it < iters; ++it) {
@@ -526,10 +572,10 @@ __global__ void __launch_bounds__(kStreamThreads) scan_stream_kernel(const ScanA
     const int64_t nrow0 = row0 + step;
     int4 nkv[NL > 0 ? NL : 1], nfv[NF > 0 ? NF : 1], nmv = make_int4(0, 0, 0, 0);
 #pragma unroll
-    for (int j = 0; j < NL; ++j) nkv[j] = ld4_padded(a.fk[j], nrow0, a.n);
+    for (int j = 0; j < NL; ++j) nkv[j] = ld4_raw(a.fkc[j], nrow0, a.n);
 #pragma unroll
-    for (int f = 0; f < NF; ++f) nfv[f] = ld4_padded(a.ff[f].col, nrow0, a.n);
-    if (a.measure) nmv = ld4_padded(a.measure, nrow0, a.n);
+    for (int f = 0; f < NF; ++f) nfv[f] = ld4_raw(a.ffc[f], nrow0, a.n);
+    if (a.measure) nmv = ld4_raw(a.mc, nrow0, a.n);
 
     const int64_t left = a.n - row0;
     const int valid = left >= 4 ? 4 : (left > 0 ? static_cast<int>(left) : 0);
@@ -543,15 +589,17 @@ __global__ void __launch_bounds__(kStreamThreads) scan_stream_kernel(const ScanA
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
       const int32_t lo = a.ff[f].lo, hi = a.ff[f].hi;
+      const int4 fu = unpack4(fv[f], a.ffc[f]);
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        const int32_t v = comp(fv[f], r);
+        const int32_t v = comp(fu, r);
         alive[r] = alive[r] & (v >= lo) & (v <= hi);
       }
     }
 #pragma unroll
     for (int j = 0; j < NL; ++j)
-      if (alive[0] | alive[1] | alive[2] | alive[3]) probe4(a.link[j], kv[j], s_tab, alive, gid);
+      if (alive[0] | alive[1] | alive[2] | alive[3]) probe4(a.link[j], unpack4(kv[j], a.fkc[j]), s_tab, alive, gid);
+    const int4 mu = unpack4(mv, a.mc);
     for (int g = 0; g < a.n_fgroups; ++g)
 #pragma unroll
       for (int r = 0; r < 4; ++r)
@@ -564,7 +612,7 @@ __global__ void __launch_bounds__(kStreamThreads) scan_stream_kernel(const ScanA
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         c4 += alive[r] ? 1 : 0;
-        s4 += alive[r] ? comp(mv, r) : 0;
+        s4 += alive[r] ? comp(mu, r) : 0;
       }
       r_cnt += static_cast<unsigned long long>(c4);
       r_sum += static_cast<unsigned long long>(s4);
@@ -572,7 +620,7 @@ __global__ void __launch_bounds__(kStreamThreads) scan_stream_kernel(const ScanA
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         if (!alive[r]) continue;
-        const int32_t v = comp(mv, r);
+        const int32_t v = comp(mu, r);
         if constexpr (MODE == 1) {
           if (a.narrow_bins) {
             atomicAdd(b32 + gid[r], 1u);

@@ -51,6 +51,10 @@ class Plan:
     def bytes_per_row(self) -> int:
         return int(self.ctx.lib.laq_plan_bytes_per_row(self.h))
 
+    @property
+    def scanned_links(self) -> int:
+        return int(self.ctx.lib.laq_plan_scanned_links(self.h))
+
     def emit(self, acc_host: np.ndarray) -> np.ndarray:
         acc_host = np.ascontiguousarray(acc_host, np.int64)
         cap = max(1, 2 * self.n_groups) * (len(self.q.group_by) + 1)
