@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant_
     const uint4 v = *reinterpret_cast<const uint4*>(a.w1 + static_cast<int64_t>(row) * 64 + c * 8);
     *reinterpret_cast<uint4*>(smem + L.b + tc::sw128_off(row, c)) = v;  // N is a multiple of 8
   }
-  for (int e = threadIdx.x; e < N * LP; e += kThreads) s_w2[e] = a.w2[e];
+  for (int e = threadIdx.x; e < N * LP; e += kThreads) s_w2[e] = a.w2[e] * a.unscale;  // exact (power of two)
   if (warp == kMmaWarp) {
     if (lane == 0) {
       for (int s = 0; s < S; ++s) {
@@ -252,11 +252,13 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant_
       const int ab = it & 1;
       tc::mbar_wait(&acc_full[ab], (it >> 1) & 1);
       tc::tc_fence_after();
-      float y[4][LP];  // 4 independent accumulation chains
+      // 4 independent accumulation chains, two per packed f32x2 register (FFMA2)
+      constexpr int LQ = LP == 1 ? 1 : LP / 2;
+      float2 y2[2][LQ];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < 2; ++u)
 #pragma unroll
-        for (int c = 0; c < LP; ++c) y[u][c] = 0.f;
+        for (int c = 0; c < LQ; ++c) y2[u][c] = make_float2(0.f, 0.f);
       const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * q) << 16) + ab * N;
       // this warp's chunks: c0 = 32*hh, 32*hh + 64, ... (two per TMEM wait)
       for (int c0 = 32 * hh; c0 < (a.diag >= 3 ? (a.diag == 3 ? 0 : N) : N); c0 += 128) {
@@ -266,24 +268,33 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant_
         if (two) tc::tmem_ld32(t0 + c0 + 64, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
         tc::tmem_ld_wait();
         if (a.diag == 4) {
-          y[0][0] += __uint_as_float(v[0] ^ v[17] ^ v[33] ^ v[63]);
+          y2[0][0].x += __uint_as_float(v[0] ^ v[17] ^ v[33] ^ v[63]);
           continue;
         }
 #pragma unroll
         for (int i0 = 0; i0 < 64; i0 += 4) {
           if (i0 < 32 || two) {
             const int col = c0 + (i0 < 32 ? i0 : i0 + 32);
-            float w[4 * LP];  // W2 rows col .. col+3 (broadcast 16-byte shared loads)
+            float w[4 * LP];  // W2 rows col .. col+3, pre-multiplied by the unscale (broadcast loads)
 #pragma unroll
             for (int qq = 0; qq < LP; ++qq) {
               const float4 t = tc::lds128_const(w2a + (col * LP + 4 * qq) * 4u);
               w[4 * qq] = t.x; w[4 * qq + 1] = t.y; w[4 * qq + 2] = t.z; w[4 * qq + 3] = t.w;
             }
+            // ReLU(acc * s) = s * ReLU(acc) for the power-of-two s > 0 folded into W2
+            float h[4];
 #pragma unroll
-            for (int ii = 0; ii < 4; ++ii) {
-              const float h = fmaxf(__uint_as_float(v[i0 + ii]) * a.unscale, 0.f);
+            for (int ii = 0; ii < 4; ++ii) h[ii] = fmaxf(__uint_as_float(v[i0 + ii]), 0.f);
+            if constexpr (LP == 1) {
+              y2[0][0] = tc::ffma2(make_float2(h[0], h[1]), make_float2(w[0], w[1]), y2[0][0]);
+              y2[1][0] = tc::ffma2(make_float2(h[2], h[3]), make_float2(w[2], w[3]), y2[1][0]);
+            } else {
 #pragma unroll
-              for (int c = 0; c < LP; ++c) y[ii][c] = fmaf(h, w[ii * LP + c], y[ii][c]);
+              for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+                for (int c = 0; c < LQ; ++c)
+                  y2[ii & 1][c] = tc::ffma2(make_float2(h[ii], h[ii]), make_float2(w[ii * LP + 2 * c], w[ii * LP + 2 * c + 1]),
+                                            y2[ii & 1][c]);
             }
           }
         }
@@ -292,8 +303,15 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant_
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&acc_empty[ab]);
       float yy[LP];
+      if constexpr (LP == 1) {
+        yy[0] = (y2[0][0].x + y2[0][0].y) + (y2[1][0].x + y2[1][0].y);
+      } else {
 #pragma unroll
-      for (int c = 0; c < LP; ++c) yy[c] = (y[0][c] + y[1][c]) + (y[2][c] + y[3][c]);
+        for (int c = 0; c < LQ; ++c) {
+          yy[2 * c] = y2[0][c].x + y2[1][c].x;
+          yy[2 * c + 1] = y2[0][c].y + y2[1][c].y;
+        }
+      }
       if (hh == 1) {
 #pragma unroll
         for (int c = 0; c < LP; ++c) s_red[ab][q][lane][c] = yy[c];
