@@ -295,6 +295,16 @@ int laq_star_add_table_device(laq_star* star, const char* name, int32_t is_fact,
                               int32_t n_cols, const char* const* col_names,
                               const int32_t* col_kinds, const int32_t* const* d_cols);
 /* StarSchema link (storage.hpp:75-81); checks pk uniqueness (storage.cpp:200-214). */
+/* Register a table whose integer columns are caller-owned device buffers in a
+ * byte-packed layout (the compact transfer format): value = stored + offset[c],
+ * stored as uint8 (width 1), uint16 (width 2) or int32 (width 4, offset 0); each
+ * buffer has >= 16 readable bytes past its end.  Scans read packed columns
+ * directly (the stream kernel); a query that needs another scan variant on a
+ * packed-only column (fact InSet filter, fact group-by, G > 4096) fails with
+ * LAQ_ERR_UNSUPPORTED. */
+int laq_star_add_table_device_packed(laq_star* star, const char* name, int32_t is_fact, int64_t rows,
+                                     int32_t n_cols, const char* const* col_names, const int32_t* col_kinds,
+                                     const void* const* d_cols, const int32_t* widths, const int32_t* offsets);
 int laq_star_add_link(laq_star* star, const char* fact_fk, const char* dim_name,
                       const char* dim_pk);
 

@@ -86,6 +86,7 @@ _SIGS = {
     "laq_star_destroy": (C.c_int, [vp]),
     "laq_star_add_table": (C.c_int, [vp, C.c_char_p, i32, i64, i32, vp, i32p, i32, vp]),
     "laq_star_add_table_device": (C.c_int, [vp, C.c_char_p, i32, i64, i32, vp, i32p, vp]),
+    "laq_star_add_table_device_packed": (C.c_int, [vp, C.c_char_p, i32, i64, i32, vp, i32p, vp, i32p, i32p]),
     "laq_star_add_link": (C.c_int, [vp, C.c_char_p, C.c_char_p, C.c_char_p]),
     "laq_query_prepare": (C.c_int, [vp, vp, C.POINTER(QueryDesc), C.POINTER(vp), i64p]),
     "laq_plan_execute": (C.c_int, [vp, vp, vp, i32]),

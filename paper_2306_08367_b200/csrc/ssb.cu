@@ -104,6 +104,31 @@ __global__ void narrow_kernel(const int64_t* __restrict__ src, int32_t* __restri
   }
 }
 
+// min/max of a packed column's stored values (value = stored + offset).
+template <class T>
+__global__ void packed_minmax_kernel(const T* __restrict__ p, int64_t n, unsigned int* mnmx) {
+  unsigned int mn = 0xffffffffu, mx = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned int v = p[i];
+    mn = v < mn ? v : mn;
+    mx = v > mx ? v : mx;
+  }
+  for (int o = 16; o; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(mnmx, mn);
+    atomicMax(mnmx + 1, mx);
+  }
+}
+
+__device__ __forceinline__ int32_t col_value(const scan::Col& c, int64_t i) {
+  if (c.w == 1) return static_cast<int32_t>(static_cast<const uint8_t*>(c.p)[i]) + c.off;
+  if (c.w == 2) return static_cast<int32_t>(static_cast<const uint16_t*>(c.p)[i]) + c.off;
+  return static_cast<const int32_t*>(c.p)[i];
+}
+
 template <class T>
 __global__ void pack_kernel(const int32_t* __restrict__ src, int64_t n, int32_t off, T* __restrict__ dst) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -159,11 +184,10 @@ __global__ void count_pass_kernel(const int32_t* __restrict__ code, int64_t slot
 }
 
 // Fact FK values without a matching dim row (referential coverage of a link).
-__global__ void fk_miss_kernel(const int32_t* __restrict__ fk, int64_t n, const ProbeView pv,
-                               unsigned long long* out) {
+__global__ void fk_miss_kernel(const scan::Col fk, int64_t n, const ProbeView pv, unsigned long long* out) {
   unsigned long long c = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    c += pv.row(__ldg(fk + i)) < 0 ? 1 : 0;
+    c += pv.row(col_value(fk, i)) < 0 ? 1 : 0;
   for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
@@ -290,7 +314,8 @@ struct laq_plan {
   int nl = 0, nf = 0;
   bool vec = true;
   bool pipe = false;
-  int variant = 0;  // 0 ldg fallback, 1 TMA pipe, 2 resident-table stream
+  int variant = 0;  // 0 ldg fallback, 1 TMA pipe, 2 resident-table stream, 3 stream over packed columns
+  bool packed_only = false;
   int mode = 0;
   int grid = 1;
   size_t smem = 0;
@@ -386,7 +411,7 @@ void lay_out_scan(laq_ctx* ctx, laq_plan* p, const std::vector<const int32_t*>& 
   // plain-load kernel for unaligned / InSet / very wide group-id plans.
   const bool fast_ok = p->vec && all_padded && !fact_inset && nc >= 1 && (p->mode != 1 || p->G <= kSmemBinsPipe);
   const char* want = std::getenv("LAQ_SCAN");
-  const std::string pick = want ? std::string(want) : std::string("stream");
+  const std::string pick = p->packed_only ? std::string("stream") : (want ? std::string(want) : std::string("stream"));
   a.smem_tab_elems = static_cast<int>(tab_elems);
   a.narrow_bins = narrow ? 1 : 0;
   const size_t tab_bytes = static_cast<size_t>((tab_elems * 2 + 15) & ~15);
@@ -542,6 +567,55 @@ int laq_star_add_table_device(laq_star* s, const char* name, int32_t is_fact, in
   });
 }
 
+int laq_star_add_table_device_packed(laq_star* s, const char* name, int32_t is_fact, int64_t rows, int32_t n_cols,
+                                     const char* const* col_names, const int32_t* col_kinds,
+                                     const void* const* d_cols, const int32_t* widths, const int32_t* offsets) {
+  laq_ctx* ctx = s->ctx;
+  return guard(ctx, [&] {
+    DevTable& t = new_table(s, name, is_fact, rows);
+    unsigned int* mnmx = reinterpret_cast<unsigned int*>(ctx->d_flags + 30);
+    for (int c = 0; c < n_cols; ++c) {
+      DevCol col;
+      col.name = col_names[c];
+      col.kind = col_kinds[c];
+      if (col.kind == LAQ_COL_FLOAT) {
+        t.cols.push_back(col);
+        continue;
+      }
+      const int w = widths[c];
+      if (w != 1 && w != 2 && w != 4) fail(LAQ_ERR_SHAPE, "packed column width must be 1, 2 or 4");
+      col.padded = true;  // caller contract: >= 16 readable bytes past the end
+      if (w == 4) {
+        if (offsets[c] != 0) fail(LAQ_ERR_SHAPE, "4-byte packed columns carry no offset");
+        col.d = const_cast<int32_t*>(static_cast<const int32_t*>(d_cols[c]));
+        if (rows > 0) minmax_i32(ctx, col.d, rows, &col.mn, &col.mx);
+      } else {
+        col.pk = const_cast<void*>(d_cols[c]);
+        col.pw = w;
+        col.poff = offsets[c];
+        if (rows > 0) {
+          const unsigned int init[2] = {0xffffffffu, 0u};
+          LAQ_CUDA(cudaMemcpyAsync(mnmx, init, sizeof init, cudaMemcpyHostToDevice, ctx->stream));
+          const int g = grid_for(rows, 256 * 8, ctx->sm_count * 8);
+          if (w == 1)
+            packed_minmax_kernel<uint8_t><<<g, 256, 0, ctx->stream>>>(static_cast<const uint8_t*>(col.pk), rows, mnmx);
+          else
+            packed_minmax_kernel<uint16_t><<<g, 256, 0, ctx->stream>>>(static_cast<const uint16_t*>(col.pk), rows, mnmx);
+          launched(ctx);
+          LAQ_CUDA(cudaMemcpyAsync(ctx->h_pinned, mnmx, 2 * sizeof(unsigned int), cudaMemcpyDeviceToHost, ctx->stream));
+          sync(ctx);
+          const unsigned int* mm = reinterpret_cast<const unsigned int*>(ctx->h_pinned);
+          col.mn = static_cast<int64_t>(mm[0]) + col.poff;
+          col.mx = static_cast<int64_t>(mm[1]) + col.poff;
+        }
+      }
+      if (col.kind == LAQ_COL_KEY && rows > 0 && col.mn < 0)
+        fail(LAQ_ERR_FORMAT, "table: negative key in column '" + col.name + "'");
+      t.cols.push_back(col);
+    }
+  });
+}
+
 int laq_star_add_link(laq_star* s, const char* fact_fk, const char* dim_name, const char* dim_pk) {
   laq_ctx* ctx = s->ctx;
   return guard(ctx, [&] {
@@ -566,7 +640,7 @@ bool link_covered(laq_ctx* ctx, laq_star* s, const DevCol& fk, const DevTable& d
   unsigned long long* cnt = reinterpret_cast<unsigned long long*>(ctx->d_flags + 57);
   LAQ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), ctx->stream));
   if (n > 0) {
-    fk_miss_kernel<<<grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(fk.d, n, pr.view(), cnt);
+    fk_miss_kernel<<<grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(fk.view(), n, pr.view(), cnt);
     launched(ctx);
   }
   LAQ_CUDA(cudaMemcpyAsync(ctx->h_pinned, cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
@@ -632,15 +706,17 @@ int laq_query_prepare(laq_ctx* ctx, const laq_star* cs, const laq_query_desc* q,
     a.n = fact.rows;
     a.n_groups = G;
     bool aligned = true, padded = true;
+    bool packed_only = false;  // some scanned column exists only byte-packed (stream kernel only)
     auto note = [&](const DevCol& c) {
-      aligned = aligned && (reinterpret_cast<uintptr_t>(c.d) % 16 == 0);
+      aligned = aligned && (reinterpret_cast<uintptr_t>(c.d ? static_cast<const void*>(c.d) : c.pk) % 16 == 0);
       padded = padded && c.padded;
+      packed_only = packed_only || c.d == nullptr;
     };
     // Measure (cli.cpp:100-101); NULL = count survivors only.
     int64_t mmin = 0, mmax = 0;
     if (q->measure) {
       const DevCol& mcol = int_col(fact, q->measure);
-      a.measure = mcol.d;
+      a.measure = mcol.d ? mcol.d : static_cast<const int32_t*>(mcol.pk);  // (stream kernel: "has a measure")
       a.mc = mcol.view();
       mmin = mcol.mn;
       mmax = mcol.mx;
@@ -669,6 +745,7 @@ int laq_query_prepare(laq_ctx* ctx, const laq_star* cs, const laq_query_desc* q,
     for (int g = 0; g < ng; ++g) {
       if (q->group_by[g].target != -1) continue;
       if (a.n_fgroups >= kMaxFactGroups) fail(LAQ_ERR_UNSUPPORTED, "at most 4 fact group columns");
+      if (!gc[g]->d) fail(LAQ_ERR_UNSUPPORTED, "group-by on a byte-packed fact column");
       a.fg[a.n_fgroups++] = FactGroup{gc[g]->d, plan->gcols[g].mn, plan->gcols[g].stride};
     }
 
@@ -736,8 +813,15 @@ int laq_query_prepare(laq_ctx* ctx, const laq_star* cs, const laq_query_desc* q,
     plan->vec = aligned;
     plan->mode = G == 1 ? 0 : (G <= kSmemBinsPipe ? 1 : (G <= kSmemBinsLdg ? 1 : 2));
     plan->bytes_per_row = 4 * (plan->nl + plan->nf + a.n_fgroups + (a.measure ? 1 : 0));
+    plan->packed_only = packed_only;
     lay_out_scan(ctx, plan.get(), fks, fkcols, probes, mmin, mmax, padded);
+    if (packed_only && plan->variant != 2)
+      fail(LAQ_ERR_UNSUPPORTED, "byte-packed fact columns need the stream scan (no fact InSet filter, G <= 4096)");
     if (plan->variant == 2) {  // the stream kernel reads the packed views
+      bool any_packed = a.measure && a.mc.w != 4;
+      for (int j = 0; j < plan->nl; ++j) any_packed = any_packed || a.fkc[j].w != 4;
+      for (int f = 0; f < plan->nf; ++f) any_packed = any_packed || a.ffc[f].w != 4;
+      if (any_packed) plan->variant = 3;
       int64_t b = 4 * a.n_fgroups + (a.measure ? a.mc.w : 0);
       for (int j = 0; j < plan->nl; ++j) b += a.fkc[j].w;
       for (int f = 0; f < plan->nf; ++f) b += a.ffc[f].w;

@@ -535,7 +535,20 @@ __device__ __forceinline__ int4 unpack4(const int4& r, const Col& c) {
   return r;
 }
 
-template <int NL, int NF, int MODE>
+// PK: some column is byte-packed (width dispatch per load); false: every column
+// is int32 and the loads are plain 16-byte vectors (no per-load width branch).
+template <int NL, int NF, int MODE, bool PK>
+__device__ __forceinline__ int4 ld_batch(const Col& c, int64_t row0, int64_t n) {
+  if constexpr (PK) return ld4_raw(c, row0, n);
+  else return ld4_padded(static_cast<const int32_t*>(c.p), row0, n);
+}
+template <bool PK>
+__device__ __forceinline__ int4 unpack_batch(const int4& r, const Col& c) {
+  if constexpr (PK) return unpack4(r, c);
+  else return r;
+}
+
+template <int NL, int NF, int MODE, bool PK>
 __global__ void __launch_bounds__(kStreamThreads) scan_stream_kernel(const ScanArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   int16_t* s_tab = reinterpret_cast<int16_t*>(smem);
@@ -561,10 +574,10 @@ __global__ void __launch_bounds__(kStreamThreads) scan_stream_kernel(const ScanA
 
   int4 kv[NL > 0 ? NL : 1], fv[NF > 0 ? NF : 1], mv = make_int4(0, 0, 0, 0);
 #pragma unroll
-  for (int j = 0; j < NL; ++j) kv[j] = ld4_raw(a.fkc[j], row0, a.n);
+  for (int j = 0; j < NL; ++j) kv[j] = ld_batch<NL, NF, MODE, PK>(a.fkc[j], row0, a.n);
 #pragma unroll
-  for (int f = 0; f < NF; ++f) fv[f] = ld4_raw(a.ffc[f], row0, a.n);
-  if (a.measure) mv = ld4_raw(a.mc, row0, a.n);
+  for (int f = 0; f < NF; ++f) fv[f] = ld_batch<NL, NF, MODE, PK>(a.ffc[f], row0, a.n);
+  if (a.measure) mv = ld_batch<NL, NF, MODE, PK>(a.mc, row0, a.n);
 
   unsigned long long r_cnt = 0, r_sum = 0;
   for (int64_t it = 0; it < iters; ++it) {
@@ -572,10 +585,10 @@ __global__ void __launch_bounds__(kStreamThreads) scan_stream_kernel(const ScanA
     const int64_t nrow0 = row0 + step;
     int4 nkv[NL > 0 ? NL : 1], nfv[NF > 0 ? NF : 1], nmv = make_int4(0, 0, 0, 0);
 #pragma unroll
-    for (int j = 0; j < NL; ++j) nkv[j] = ld4_raw(a.fkc[j], nrow0, a.n);
+    for (int j = 0; j < NL; ++j) nkv[j] = ld_batch<NL, NF, MODE, PK>(a.fkc[j], nrow0, a.n);
 #pragma unroll
-    for (int f = 0; f < NF; ++f) nfv[f] = ld4_raw(a.ffc[f], nrow0, a.n);
-    if (a.measure) nmv = ld4_raw(a.mc, nrow0, a.n);
+    for (int f = 0; f < NF; ++f) nfv[f] = ld_batch<NL, NF, MODE, PK>(a.ffc[f], nrow0, a.n);
+    if (a.measure) nmv = ld_batch<NL, NF, MODE, PK>(a.mc, nrow0, a.n);
 
     const int64_t left = a.n - row0;
     const int valid = left >= 4 ? 4 : (left > 0 ? static_cast<int>(left) : 0);
@@ -589,7 +602,7 @@ __global__ void __launch_bounds__(kStreamThreads) scan_stream_kernel(const ScanA
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
       const int32_t lo = a.ff[f].lo, hi = a.ff[f].hi;
-      const int4 fu = unpack4(fv[f], a.ffc[f]);
+      const int4 fu = unpack_batch<PK>(fv[f], a.ffc[f]);
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int32_t v = comp(fu, r);
@@ -598,8 +611,8 @@ __global__ void __launch_bounds__(kStreamThreads) scan_stream_kernel(const ScanA
     }
 #pragma unroll
     for (int j = 0; j < NL; ++j)
-      if (alive[0] | alive[1] | alive[2] | alive[3]) probe4(a.link[j], unpack4(kv[j], a.fkc[j]), s_tab, alive, gid);
-    const int4 mu = unpack4(mv, a.mc);
+      if (alive[0] | alive[1] | alive[2] | alive[3]) probe4(a.link[j], unpack_batch<PK>(kv[j], a.fkc[j]), s_tab, alive, gid);
+    const int4 mu = unpack_batch<PK>(mv, a.mc);
     for (int g = 0; g < a.n_fgroups; ++g)
 #pragma unroll
       for (int r = 0; r < 4; ++r)

@@ -6,7 +6,8 @@
 namespace laq {
 namespace scan {
 
-// variant: 0 = ldg fallback, 1 = TMA pipe, 2 = resident-table stream.
+// variant: 0 = ldg fallback, 1 = TMA pipe, 2 = resident-table stream (int32),
+// 3 = the stream kernel over byte-packed columns.
 template <int NL, int NF, int MODE>
 void launch_variant(laq_ctx* ctx, const ScanArgs& a, int variant, bool vec, int grid, size_t smem) {
   cudaStream_t s = ctx->stream;
@@ -14,8 +15,8 @@ void launch_variant(laq_ctx* ctx, const ScanArgs& a, int variant, bool vec, int 
   if (variant == 1) {
     LAQ_CUDA(cudaFuncSetAttribute(scan_pipe_kernel<NL, NF, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     scan_pipe_kernel<NL, NF, MODE><<<grid, kPipeThreads, smem, s>>>(a);
-  } else if (variant == 2) {
-    auto kern = scan_stream_kernel<NL, NF, MODE>;
+  } else if (variant == 2 || variant == 3) {
+    auto kern = variant == 3 ? scan_stream_kernel<NL, NF, MODE, true> : scan_stream_kernel<NL, NF, MODE, false>;
     LAQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     int per_sm = 0;
     LAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStreamThreads, smem));

@@ -147,6 +147,27 @@ class DeviceStar:
                                                               len(names), cn, kd, ptrs))
         self.rows[name] = rows
 
+    def add_table_device_packed(self, name, cols: dict, kinds: dict, is_fact=False):
+        """Byte-packed CUDA tensors {column: (tensor, width, offset)} used in place
+        (value = stored + offset; uint8 / int16-bits / int32 storage, see
+        pack_columns).  Each tensor needs >= 16 bytes of padding past the rows."""
+        names = list(cols)
+        rows = self._packed_rows(cols)
+        self._keep.append(cols)
+        cn = (C.c_char_p * len(names))(*[c.encode() for c in names])
+        kd = (C.c_int32 * len(names))(*[kinds[c] for c in names])
+        ptrs = _abi.ptr_array([cols[c][0].data_ptr() for c in names])
+        w = (C.c_int32 * len(names))(*[int(cols[c][1]) for c in names])
+        off = (C.c_int32 * len(names))(*[int(cols[c][2]) for c in names])
+        self.ctx.check(self.ctx.lib.laq_star_add_table_device_packed(
+            self.star_h, name.encode(), 1 if is_fact else 0, rows, len(names), cn, kd, ptrs, w, off))
+        self.rows[name] = rows
+
+    @staticmethod
+    def _packed_rows(cols):
+        t, w, _ = next(iter(cols.values()))[:3]
+        return (t.numel() * t.element_size() - 16) // int(w)
+
     @property
     def star_h(self):
         return self.h
@@ -192,3 +213,27 @@ def upload_gen_star(g, ctx=None, row_range=None) -> DeviceStar:
     """Upload a gen.GenStar (or oracle RefStar-like object with .tables/.kinds/.links())."""
     links = g.links() if callable(getattr(g, "links", None)) else g.links
     return DeviceStar.from_tables(g.tables, g.kinds, links, row_range=row_range, ctx=ctx)
+
+
+def pack_columns(cols: dict) -> dict:
+    """Host-side compact transfer format for integer columns: value - min stored
+    as uint8 when the range fits 8 bits, uint16 when it fits 16, else int32
+    (offset 0); each array carries 16 bytes of zero padding.  Returns
+    {column: (numpy array, width, offset)}."""
+    out = {}
+    for c, a in cols.items():
+        a = np.asarray(a)
+        if a.dtype.kind == "f":
+            continue
+        mn, mx = (int(a.min()), int(a.max())) if a.size else (0, 0)
+        rng = mx - mn
+        if rng < 256:
+            w, dt, off = 1, np.uint8, mn
+        elif rng < 65536:
+            w, dt, off = 2, np.uint16, mn
+        else:
+            w, dt, off = 4, np.int32, 0
+        buf = np.zeros(a.size * w + 16, np.uint8)
+        buf[: a.size * w].view(dt)[:] = (a.astype(np.int64) - off).astype(dt)
+        out[c] = (buf, w, off)
+    return out

@@ -133,3 +133,28 @@ def test_link_elision_respects_inner_join(gpu_ctx, dangling):
             if dangling > 0.0:
                 assert p.scanned_links == len(q.joins)
             assert np.array_equal(ds.run_query(q), O.run_query(g.tables, q))
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN, "ssb_sf1.json")), reason="sf1 goldens not generated")
+def test_packed_fact_table_reference_checksums(gpu_ctx):
+    """The compact transfer format (star.pack_columns: uint8/uint16 offsets from the
+    column minimum) registered in place with laq_star_add_table_device_packed:
+    all 12 SSB sf=1 queries still reproduce the reference checksums."""
+    import torch
+    from paper_2306_08367_b200 import gen, star
+    G = load_golden("ssb_sf1.json")
+    g = gen.gen_star("Ssb", 1, 42, narrow=True)
+    packed = star.pack_columns(g.fact)
+    assert {w for _, w, _ in packed.values()} >= {1, 2}  # discount/quantity bytes, dates/supplier halves
+    ds = star.DeviceStar()
+    dev = {c: (torch.from_numpy(b).cuda(), w, off) for c, (b, w, off) in packed.items()}
+    ds.add_table_device_packed("lineorder", dev, g.kinds["lineorder"], is_fact=True)
+    for t, cols in g.tables.items():
+        if t != "lineorder":
+            ds.add_table(t, cols, g.kinds[t])
+    for l in g.links():
+        ds.add_link(*l)
+    for qg in G["queries"]:
+        m = ds.run_query(_q(qg["group"], qg["id"], qg["dial"]))
+        assert np.array_equal(m.ravel(), fa(qg["result"])), qg["id"]
+        assert str(O.checksum_rows(m)) == qg["checksum"], qg["id"]
