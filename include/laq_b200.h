@@ -354,6 +354,11 @@ int laq_plan_execute(laq_ctx* ctx, laq_plan* plan, int64_t* d_acc, int32_t accum
  * per-link code tables (dimension filters), then the fused fact scan. */
 int laq_plan_build_codes(laq_ctx* ctx, laq_plan* plan);
 int laq_plan_scan(laq_ctx* ctx, laq_plan* plan, int64_t* d_acc, int32_t accumulate);
+/* Scan only fact rows [row0, row0 + rows) (row0 a multiple of 4) with the code
+ * tables of the last build: lets a caller overlap the upload of later row
+ * chunks with the scan of earlier ones (accumulate = 1 after the first chunk). */
+int laq_plan_scan_range(laq_ctx* ctx, laq_plan* plan, int64_t row0, int64_t rows, int64_t* d_acc,
+                        int32_t accumulate);
 /* Bytes of fact columns the scan streams per row (the roofline unit). */
 int64_t laq_plan_bytes_per_row(const laq_plan* plan);
 /* Joins the plan's scan actually probes (after eliding covered filter-free links). */

@@ -92,6 +92,7 @@ _SIGS = {
     "laq_plan_execute": (C.c_int, [vp, vp, vp, i32]),
     "laq_plan_build_codes": (C.c_int, [vp, vp]),
     "laq_plan_scan": (C.c_int, [vp, vp, vp, i32]),
+    "laq_plan_scan_range": (C.c_int, [vp, vp, i64, i64, vp, i32]),
     "laq_plan_bytes_per_row": (i64, [vp]),
     "laq_plan_scanned_links": (i32, [vp]),
     "laq_plan_emit": (C.c_int, [vp, i64p, f64p, i64, i64p, i64p]),

@@ -849,6 +849,35 @@ int laq_plan_scan(laq_ctx* ctx, laq_plan* p, int64_t* d_acc, int32_t accumulate)
   });
 }
 
+int laq_plan_scan_range(laq_ctx* ctx, laq_plan* p, int64_t row0, int64_t rows, int64_t* d_acc, int32_t accumulate) {
+  return guard(ctx, [&] {
+    if (row0 < 0 || rows < 0 || row0 + rows > p->fact_rows) fail(LAQ_ERR_INDEX, "scan range outside the fact table");
+    if (row0 % 4) fail(LAQ_ERR_SHAPE, "scan range must start at a multiple of 4 rows");
+    if (!accumulate) LAQ_CUDA(cudaMemsetAsync(d_acc, 0, 2 * p->G * sizeof(int64_t), ctx->stream));
+    if (rows == 0) return;
+    ScanArgs a = p->scan;
+    a.n = rows;
+    auto shift = [&](scan::Col& c) {
+      if (c.p) c.p = static_cast<const uint8_t*>(c.p) + row0 * c.w;
+    };
+    for (int j = 0; j < p->nl; ++j) {
+      if (a.fk[j]) a.fk[j] += row0;
+      shift(a.fkc[j]);
+    }
+    for (int f = 0; f < p->nf; ++f) {
+      if (a.ff[f].col) a.ff[f].col += row0;
+      shift(a.ffc[f]);
+    }
+    for (int g = 0; g < a.n_fgroups; ++g) a.fg[g].col += row0;
+    if (a.measure) {  // int32 column (other variants) or the stream kernel's "has a measure" flag
+      a.measure += row0;
+      shift(a.mc);
+    }
+    a.acc = reinterpret_cast<unsigned long long*>(d_acc);
+    launch_scan(ctx, a, p->nl, p->nf, p->mode, p->variant, p->vec, p->grid, p->smem);
+  });
+}
+
 int laq_plan_execute(laq_ctx* ctx, laq_plan* p, int64_t* d_acc, int32_t accumulate) {
   const int rc = laq_plan_build_codes(ctx, p);
   return rc ? rc : laq_plan_scan(ctx, p, d_acc, accumulate);

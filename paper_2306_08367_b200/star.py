@@ -47,6 +47,13 @@ class Plan:
         self.ctx.check(self.ctx.lib.laq_plan_scan(self.ctx.h, self.h, acc.data_ptr(), 1 if accumulate else 0))
         return acc
 
+    def scan_range(self, row0: int, rows: int, acc: torch.Tensor | None = None, accumulate: bool = False):
+        """Scan fact rows [row0, row0 + rows) with the current code tables."""
+        acc = self.acc if acc is None else acc
+        self.ctx.check(self.ctx.lib.laq_plan_scan_range(self.ctx.h, self.h, row0, rows, acc.data_ptr(),
+                                                        1 if accumulate else 0))
+        return acc
+
     @property
     def bytes_per_row(self) -> int:
         return int(self.ctx.lib.laq_plan_bytes_per_row(self.h))

@@ -158,3 +158,22 @@ def test_packed_fact_table_reference_checksums(gpu_ctx):
         m = ds.run_query(_q(qg["group"], qg["id"], qg["dial"]))
         assert np.array_equal(m.ravel(), fa(qg["result"])), qg["id"]
         assert str(O.checksum_rows(m)) == qg["checksum"], qg["id"]
+
+
+def test_scan_ranges_sum_to_whole(gpu_ctx):
+    """laq_plan_scan_range over consecutive row chunks (the chunked-upload path of
+    bench.py's e2e) accumulates to exactly the whole-table scan."""
+    from paper_2306_08367_b200 import gen, star
+    G = load_golden("ssb_s2_sf2.json")
+    g = gen.gen_star(G["setting"], G["sf"], G["seed"], narrow=True)
+    ds = star.upload_gen_star(g)
+    n = len(g.fact["lo_part"])
+    cuts = [0, (n // 7) // 4 * 4, (n // 2) // 4 * 4, n]
+    for qg in G["queries"]:
+        p = ds.prepare(_q(qg["group"], qg["id"], qg["dial"]))
+        whole = p.execute().clone()
+        p.build_codes()
+        acc = None
+        for k in range(3):
+            acc = p.scan_range(cuts[k], cuts[k + 1] - cuts[k], acc=None if acc is None else acc, accumulate=k > 0)
+        assert np.array_equal(acc.cpu().numpy(), whole.cpu().numpy()), qg["id"]
