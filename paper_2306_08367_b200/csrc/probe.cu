@@ -429,6 +429,7 @@ struct laq_probe {
   DevMem<char> scan_tmp;
   size_t scan_tmp_bytes = 0;
   int64_t chunk_cap = 0;
+  DevMem<unsigned long long> miss{1};  // optimistic single pass: chunks with a missing key
 };
 
 namespace laq {
@@ -521,30 +522,39 @@ void run_slot_predict(laq_ctx* ctx, laq_probe* p, const int32_t* const* d_fks, i
   }
   const size_t smem = static_cast<size_t>(words_total) * 4;
   const size_t smem_w = static_cast<size_t>((words_total * 4 + 15) & ~int64_t{15}) + static_cast<size_t>(doubles) * 8;
-  auto launch = [&](auto count_k, auto write_k) {
+  // l == 1 and no LAQ_PREDICT_TWO_PASS: optimistic single pass + device-decided
+  // compaction fallback (direct_chunks_kernel); otherwise count + scan + write.
+  const bool optimistic = l == 1 && !std::getenv("LAQ_PREDICT_TWO_PASS");
+  if (optimistic) LAQ_CUDA(cudaMemsetAsync(p->miss.get(), 0, sizeof(unsigned long long), ctx->stream));
+  auto launch = [&](auto count_k, auto direct_k, auto write_k) {
     LAQ_CUDA(cudaFuncSetAttribute(write_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_w)));
+    LAQ_CUDA(cudaFuncSetAttribute(direct_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_w)));
     const int64_t want = (n_chunks + slot::kWarpThreads / 32 - 1) / (slot::kWarpThreads / 32);
     int per_sm = 0;
-    LAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, count_k, slot::kWarpThreads, smem));
-    const unsigned g1 = static_cast<unsigned>(std::min<int64_t>(want, int64_t{ctx->sm_count} * std::max(per_sm, 1)));
+    if (optimistic) {
+      LAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, direct_k, slot::kWarpThreads, smem_w));
+      const unsigned g0 = static_cast<unsigned>(std::min<int64_t>(want, int64_t{ctx->sm_count} * std::max(per_sm, 1)));
+      direct_k<<<g0, slot::kWarpThreads, smem_w, ctx->stream>>>(a, n_chunks, p->chunk_counts.get(), p->miss.get());
+    } else {
+      LAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, count_k, slot::kWarpThreads, smem));
+      const unsigned g1 = static_cast<unsigned>(std::min<int64_t>(want, int64_t{ctx->sm_count} * std::max(per_sm, 1)));
+      count_k<<<g1, slot::kWarpThreads, smem, ctx->stream>>>(a, n_chunks, p->chunk_counts.get());
+    }
     LAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, write_k, slot::kWarpThreads, smem_w));
     const unsigned g2 = static_cast<unsigned>(std::min<int64_t>(want, int64_t{ctx->sm_count} * std::max(per_sm, 1)));
-    count_k<<<g1, slot::kWarpThreads, smem, ctx->stream>>>(a, n_chunks, p->chunk_counts.get());
     size_t bytes = p->scan_tmp_bytes;
     LAQ_CUDA(cub::DeviceScan::ExclusiveSum(p->scan_tmp.get(), bytes, p->chunk_counts.get(), p->chunk_offsets.get(),
                                            n_chunks, ctx->stream));
-    write_k<<<g2, slot::kWarpThreads, smem_w, ctx->stream>>>(a, n_chunks, p->chunk_offsets.get());
+    write_k<<<g2, slot::kWarpThreads, smem_w, ctx->stream>>>(a, n_chunks, p->chunk_offsets.get(),
+                                                             optimistic ? p->miss.get() : nullptr);
     ctx->launches += 2;
   };
   switch (p->n_links) {
-    case 1: launch(slot::count_chunks_kernel<1>, slot::write_chunks_kernel<1>); break;
-    case 2: launch(slot::count_chunks_kernel<2>, slot::write_chunks_kernel<2>); break;
-    case 3: launch(slot::count_chunks_kernel<3>, slot::write_chunks_kernel<3>); break;
-    case 4: launch(slot::count_chunks_kernel<4>, slot::write_chunks_kernel<4>); break;
-    case 5: launch(slot::count_chunks_kernel<5>, slot::write_chunks_kernel<5>); break;
-    case 6: launch(slot::count_chunks_kernel<6>, slot::write_chunks_kernel<6>); break;
-    case 7: launch(slot::count_chunks_kernel<7>, slot::write_chunks_kernel<7>); break;
-    case 8: launch(slot::count_chunks_kernel<8>, slot::write_chunks_kernel<8>); break;
+#define LAQ_SLOT_CASE(N) \
+    case N: launch(slot::count_chunks_kernel<N>, slot::direct_chunks_kernel<N>, slot::write_chunks_kernel<N>); break;
+    LAQ_SLOT_CASE(1) LAQ_SLOT_CASE(2) LAQ_SLOT_CASE(3) LAQ_SLOT_CASE(4)
+    LAQ_SLOT_CASE(5) LAQ_SLOT_CASE(6) LAQ_SLOT_CASE(7) LAQ_SLOT_CASE(8)
+#undef LAQ_SLOT_CASE
     default: fail(LAQ_ERR_UNSUPPORTED, "fused predict supports 1..8 dimensions");
   }
   launched(ctx);
