@@ -817,11 +817,18 @@ int laq_query_prepare(laq_ctx* ctx, const laq_star* cs, const laq_query_desc* q,
     lay_out_scan(ctx, plan.get(), fks, fkcols, probes, mmin, mmax, padded);
     if (packed_only && plan->variant != 2)
       fail(LAQ_ERR_UNSUPPORTED, "byte-packed fact columns need the stream scan (no fact InSet filter, G <= 4096)");
-    if (plan->variant == 2) {  // the stream kernel reads the packed views
+    if (plan->variant == 2) {  // the stream kernels read the packed views
       bool any_packed = a.measure && a.mc.w != 4;
       for (int j = 0; j < plan->nl; ++j) any_packed = any_packed || a.fkc[j].w != 4;
       for (int f = 0; f < plan->nf; ++f) any_packed = any_packed || a.ffc[f].w != 4;
       if (any_packed) plan->variant = 3;
+      // The direct-probe form of the same kernel (ssb_scan.cuh) when every link
+      // is a DIRECT table, the group id comes from the links only and the bins
+      // are narrow: every SSB query.  LAQ_SCAN=stream keeps the generic form.
+      bool direct = a.n_fgroups == 0 && plan->mode != 2 && (plan->mode == 0 || a.narrow_bins);
+      for (int j = 0; j < plan->nl; ++j) direct = direct && a.link[j].kind == PROBE_DIRECT;
+      const char* want = std::getenv("LAQ_SCAN");
+      if (direct && !(want && std::string(want) == "stream")) plan->variant += 2;
       int64_t b = 4 * a.n_fgroups + (a.measure ? a.mc.w : 0);
       for (int j = 0; j < plan->nl; ++j) b += a.fkc[j].w;
       for (int f = 0; f < plan->nf; ++f) b += a.ffc[f].w;

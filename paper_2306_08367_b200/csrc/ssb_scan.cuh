@@ -681,5 +681,172 @@ __global__ void __launch_bounds__(kStreamThreads) scan_stream_kernel(const ScanA
   }
 }
 
+// ---------------------------------------------------------------------------
+// direct: the stream kernel's data flow with the per-row instruction count cut
+// to what the query needs, for plans whose links are all DIRECT probe tables
+// and whose group id comes from the links only (every SSB query).  Measured on
+// Q2.1 (ncu source page) the stream kernel issued ~410 warp instructions per
+// 128 rows: per-row generic->shared address construction (S2R SR_CgaCtaId),
+// 64-bit row bounds, a 64-bit modulo per iteration for the bin-spill test and
+// the runtime probe-kind dispatch.  Here: shared code tables and bins are
+// addressed with 32-bit shared-window addresses computed once, full grid
+// steps run without row bounds (one bounded tail step), the spill test is a
+// countdown, and each probe is  slot = key - base; slot < size ? table[slot]
+// : -1  with the shared/global choice a warp-uniform branch per link.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ int32_t lds_s16(uint32_t addr) {
+  int16_t v;
+  asm volatile("ld.shared.s16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return static_cast<int32_t>(v);
+}
+__device__ __forceinline__ void reds_add(uint32_t addr, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+template <int NL, int NF, int MODE, bool PK, bool TAIL>
+__device__ __forceinline__ void direct_rows(const ScanArgs& a, int64_t row0, const int4 (&kv)[NL > 0 ? NL : 1],
+                                            const int4 (&fv)[NF > 0 ? NF : 1], const int4& mv,
+                                            const uint32_t (&tab_addr)[NL > 0 ? NL : 1], uint32_t bins,
+                                            unsigned long long& r_cnt, unsigned long long& r_sum) {
+  bool alive[4];
+  int32_t gid[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    alive[r] = TAIL ? row0 + r < a.n : true;
+    gid[r] = 0;
+  }
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    const int32_t lo = a.ff[f].lo, hi = a.ff[f].hi;
+    const int4 fu = unpack_batch<PK>(fv[f], a.ffc[f]);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int32_t v = comp(fu, r);
+      alive[r] = alive[r] & (v >= lo) & (v <= hi);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NL; ++j) {
+    const uint32_t base = static_cast<uint32_t>(a.link[j].base), size = static_cast<uint32_t>(a.link[j].size);
+    const int4 k = unpack_batch<PK>(kv[j], a.fkc[j]);
+    int32_t c[4];
+    if (a.link[j].smem_off >= 0) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint32_t s = static_cast<uint32_t>(comp(k, r)) - base;
+        c[r] = -1;
+        if (alive[r] && s < size) c[r] = lds_s16(tab_addr[j] + 2 * s);
+      }
+    } else {
+      const int32_t* code = a.link[j].code;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint32_t s = static_cast<uint32_t>(comp(k, r)) - base;
+        c[r] = -1;
+        if (alive[r] && s < size) c[r] = __ldg(code + s);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      alive[r] = alive[r] & (c[r] >= 0);
+      gid[r] += c[r];
+    }
+  }
+  const int4 mu = unpack_batch<PK>(mv, a.mc);
+  if constexpr (MODE == 0) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      r_cnt += alive[r] ? 1u : 0u;
+      r_sum += alive[r] ? static_cast<unsigned long long>(static_cast<long long>(comp(mu, r))) : 0ull;
+    }
+  } else {
+    const uint32_t sum_off = static_cast<uint32_t>(a.n_groups) * 4u;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      if (alive[r]) {
+        const uint32_t ad = bins + 4u * static_cast<uint32_t>(gid[r]);
+        reds_add(ad, 1u);
+        if (a.measure) reds_add(ad + sum_off, static_cast<uint32_t>(comp(mu, r)));
+      }
+    }
+  }
+}
+
+// MODE 0 (one group: register accumulation) or MODE 1 with narrow (u32) bins.
+template <int NL, int NF, int MODE, bool PK>
+__global__ void __launch_bounds__(kStreamThreads) scan_direct_kernel(const ScanArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  int16_t* s_tab = reinterpret_cast<int16_t*>(smem);
+  uint32_t* b32 = reinterpret_cast<uint32_t*>(smem + ((a.smem_tab_elems * 2 + 15) & ~15));
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < NL; ++j) {
+    const LinkProbe& p = a.link[j];
+    if (p.smem_off >= 0)
+      for (int64_t s = tid; s < p.size; s += kStreamThreads) s_tab[p.smem_off + s] = static_cast<int16_t>(__ldg(p.code + s));
+  }
+  if constexpr (MODE == 1)
+    for (int64_t g = tid; g < 2 * a.n_groups; g += kStreamThreads) b32[g] = 0;
+  __syncthreads();
+
+  const uint32_t s_base = smem_u32(smem);
+  const uint32_t bins = smem_u32(b32);
+  uint32_t tab_addr[NL > 0 ? NL : 1];
+#pragma unroll
+  for (int j = 0; j < NL; ++j) tab_addr[j] = s_base + 2u * static_cast<uint32_t>(a.link[j].smem_off > 0 ? a.link[j].smem_off : 0);
+
+  const int64_t step = static_cast<int64_t>(gridDim.x) * kStreamThreads * 4;
+  const int64_t iters = (a.n + step - 1) / step;  // uniform across the block
+  const int64_t full = a.n / step;                // steps with every row in range
+  int64_t row0 = (static_cast<int64_t>(blockIdx.x) * kStreamThreads + tid) * 4;
+
+  int4 kv[NL > 0 ? NL : 1], fv[NF > 0 ? NF : 1], mv = make_int4(0, 0, 0, 0);
+#pragma unroll
+  for (int j = 0; j < NL; ++j) kv[j] = ld_batch<NL, NF, MODE, PK>(a.fkc[j], row0, a.n);
+#pragma unroll
+  for (int f = 0; f < NF; ++f) fv[f] = ld_batch<NL, NF, MODE, PK>(a.ffc[f], row0, a.n);
+  if (a.measure) mv = ld_batch<NL, NF, MODE, PK>(a.mc, row0, a.n);
+
+  unsigned long long r_cnt = 0, r_sum = 0;
+  int64_t until_flush = a.narrow_bins ? a.flush_every : INT64_MAX;
+  for (int64_t it = 0; it < iters; ++it) {
+    const int64_t nrow0 = row0 + step;
+    int4 nkv[NL > 0 ? NL : 1], nfv[NF > 0 ? NF : 1], nmv = make_int4(0, 0, 0, 0);
+#pragma unroll
+    for (int j = 0; j < NL; ++j) nkv[j] = ld_batch<NL, NF, MODE, PK>(a.fkc[j], nrow0, a.n);
+#pragma unroll
+    for (int f = 0; f < NF; ++f) nfv[f] = ld_batch<NL, NF, MODE, PK>(a.ffc[f], nrow0, a.n);
+    if (a.measure) nmv = ld_batch<NL, NF, MODE, PK>(a.mc, nrow0, a.n);
+
+    if (it < full) direct_rows<NL, NF, MODE, PK, false>(a, row0, kv, fv, mv, tab_addr, bins, r_cnt, r_sum);
+    else direct_rows<NL, NF, MODE, PK, true>(a, row0, kv, fv, mv, tab_addr, bins, r_cnt, r_sum);
+
+    if constexpr (MODE == 1) {
+      if (--until_flush == 0) {
+        until_flush = a.flush_every;
+        if (it + 1 < iters) {
+          __syncthreads();
+          spill_bins32(b32, a.n_groups, a.acc, tid, kStreamThreads);
+          __syncthreads();
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NL; ++j) kv[j] = nkv[j];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) fv[f] = nfv[f];
+    mv = nmv;
+    row0 = nrow0;
+  }
+
+  if constexpr (MODE == 0) {
+    flush_single(r_cnt, r_sum, a.acc);
+  } else {
+    __syncthreads();
+    spill_bins32(b32, a.n_groups, a.acc, tid, kStreamThreads);
+  }
+}
+
 }  // namespace scan
 }  // namespace laq

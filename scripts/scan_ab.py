@@ -1,5 +1,6 @@
 """A/B timing of the K4 scan variants on the six bench queries (SSB SF=10).
-LAQ_SCAN=ldg forces the vectorised-load fallback; default is the TMA pipeline."""
+LAQ_SCAN=ldg forces the vectorised-load fallback, =pipe the TMA pipeline, =stream the
+generic stream kernel; default (direct) is the direct-probe stream kernel."""
 import os
 import sys
 
@@ -13,7 +14,7 @@ DIALS = {(1, 0): 222, (1, 1): 200, (1, 2): 133, (2, 0): 500, (2, 1): 199, (2, 2)
 g = gen.gen_star("Ssb", int(os.environ.get("LAQ_SF", "10")), 42, narrow=True)
 ds = star.upload_gen_star(g)
 res = {}
-for variant in ("stream", "pipe", "ldg"):
+for variant in ("direct", "stream", "pipe", "ldg"):
     os.environ["LAQ_SCAN"] = variant
     plans = [ds.prepare(Q.spec_with_dial(Q.group_defs(gr)[qi], gr, d)) for (gr, qi), d in DIALS.items()]
     out = []
@@ -35,7 +36,7 @@ for variant in ("stream", "pipe", "ldg"):
     res[variant] = out
     print(variant, out, flush=True)
 bad = 0
-for a, b in list(zip(res["pipe"], res["ldg"])) + list(zip(res["stream"], res["ldg"])):
+for a, b in list(zip(res["pipe"], res["ldg"])) + list(zip(res["stream"], res["ldg"])) + list(zip(res["direct"], res["ldg"])):
     if a[3:] != b[3:]:
         bad += 1
         print("MISMATCH", a, b)
