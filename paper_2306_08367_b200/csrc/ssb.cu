@@ -175,6 +175,40 @@ __global__ void code_kernel(const CodeArgs a) {
   }
 }
 
+// Every link's code table of a query in one launch, one thread per probe slot:
+// slot -> dim row (probe table) -> filters -> group code, -1 for an empty slot
+// or a failing row.  Replaces a memset + code_kernel pair per link (bench
+// step: 2 launches per query instead of 2 per link + 1).
+constexpr int kMaxCodeLinks = 8;
+struct MultiCodeArgs {
+  int n;
+  int64_t start[kMaxCodeLinks + 1];  // prefix of slot counts
+  const int32_t* slot_row[kMaxCodeLinks];
+  CodeArgs link[kMaxCodeLinks];
+};
+
+__global__ void codes_kernel(const MultiCodeArgs m) {
+  const int64_t total = m.start[m.n];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int j = 0;
+    while (i >= m.start[j + 1]) ++j;
+    const CodeArgs& a = m.link[j];
+    const int64_t s = i - m.start[j];
+    const int32_t r = m.slot_row[j] ? __ldg(m.slot_row[j] + s) : -1;
+    int64_t code = -1;
+    if (r >= 0) {
+      bool pass = true;
+      for (int f = 0; f < a.n_filters && pass; ++f)
+        pass = scan::pred_eval(a.f[f].kind, a.f[f].col[r], a.f[f].lo, a.f[f].hi, a.f[f].set, a.f[f].set_len);
+      if (pass) {
+        code = 0;
+        for (int g = 0; g < a.n_groups; ++g) code += (static_cast<int64_t>(a.g[g].col[r]) - a.g[g].mn) * a.g[g].stride;
+      }
+    }
+    a.code[s] = static_cast<int32_t>(code);
+  }
+}
+
 __global__ void count_pass_kernel(const int32_t* __restrict__ code, int64_t slots, unsigned long long* out) {
   unsigned long long c = 0;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < slots; s += (int64_t)gridDim.x * blockDim.x)
@@ -306,7 +340,9 @@ struct laq_plan {
   struct LinkCode {
     CodeArgs args;
     DevMem<int32_t> code;
-    int64_t slots;
+    int64_t slots;       // allocated (>= 1)
+    int64_t slots_used;  // slots the fused code kernel writes (= slots)
+    const int32_t* slot_row = nullptr;
   };
   std::vector<LinkCode> links;  // in query join order
   DevMem<int64_t> sets;         // INSET values of every filter
@@ -326,6 +362,20 @@ namespace laq {
 namespace {
 
 void build_codes(laq_ctx* ctx, laq_plan* p) {
+  if (!p->links.empty() && p->links.size() <= kMaxCodeLinks && !std::getenv("LAQ_CODES_PER_LINK")) {
+    MultiCodeArgs m{};
+    m.n = static_cast<int>(p->links.size());
+    for (int j = 0; j < m.n; ++j) {
+      m.link[j] = p->links[j].args;
+      m.slot_row[j] = p->links[j].slot_row;
+      m.start[j + 1] = m.start[j] + p->links[j].slots_used;
+    }
+    if (m.start[m.n] > 0) {
+      codes_kernel<<<grid_for(m.start[m.n], 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(m);
+      launched(ctx);
+    }
+    return;
+  }
   for (auto& lc : p->links) {
     LAQ_CUDA(cudaMemsetAsync(lc.code.get(), 0xFF, lc.slots * sizeof(int32_t), ctx->stream));
     if (lc.args.rows > 0) {
@@ -763,6 +813,8 @@ int laq_query_prepare(laq_ctx* ctx, const laq_star* cs, const laq_query_desc* q,
       const Probe& pr = s->probe(*d, pk);
       auto& lc = plan->links[j];
       lc.slots = std::max<int64_t>(pr.size, 1);
+      lc.slots_used = lc.slots;
+      lc.slot_row = d->rows > 0 && pr.size > 0 ? pr.rows.get() : nullptr;  // nullptr: every slot empty
       lc.code = DevMem<int32_t>(lc.slots);
       CodeArgs& ca = lc.args;
       ca.rows = d->rows;
@@ -829,6 +881,13 @@ int laq_query_prepare(laq_ctx* ctx, const laq_star* cs, const laq_query_desc* q,
       for (int j = 0; j < plan->nl; ++j) direct = direct && a.link[j].kind == PROBE_DIRECT;
       const char* want = std::getenv("LAQ_SCAN");
       if (direct && !(want && std::string(want) == "stream")) plan->variant += 2;
+      // L2 prefetch of the fact rows 2 grid steps ahead when some link gathers
+      // from L2 (Q2.x: 0.184 -> 0.169 ms); plans probing shared memory only are
+      // already at the copy bandwidth and measured slower with it (0.144 -> 0.160).
+      bool gathers = false;
+      for (int j = 0; j < plan->nl; ++j) gathers = gathers || a.link[j].smem_off < 0;
+      a.prefetch = gathers ? 2 : 0;
+      if (const char* pf = std::getenv("LAQ_PREFETCH")) a.prefetch = std::atoi(pf);
       int64_t b = 4 * a.n_fgroups + (a.measure ? a.mc.w : 0);
       for (int j = 0; j < plan->nl; ++j) b += a.fkc[j].w;
       for (int f = 0; f < plan->nf; ++f) b += a.ffc[f].w;

@@ -88,6 +88,7 @@ struct ScanArgs {
   int smem_tab_elems;   // int16 elements of staged code tables
   int narrow_bins;      // 1: u32 (count, sum) bins, spilled every flush_every tiles
   int64_t flush_every;  // tiles per CTA after which u32 bins could overflow
+  int prefetch;         // direct kernel: L2 prefetch distance in grid steps (0: off)
 };
 
 __device__ __forceinline__ bool pred_eval(int kind, int64_t v, int64_t lo, int64_t hi, const int64_t* set, int n) {
@@ -704,6 +705,11 @@ __device__ __forceinline__ void reds_add(uint32_t addr, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
+// One 128-byte line per 8 lanes (8 lanes x 4 rows x 4 B) of a column.
+__device__ __forceinline__ void prefetch_l2(const Col& c, int64_t row0) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<const uint8_t*>(c.p) + row0 * c.w));
+}
+
 template <int NL, int NF, int MODE, bool PK, bool TAIL>
 __device__ __forceinline__ void direct_rows(const ScanArgs& a, int64_t row0, const int4 (&kv)[NL > 0 ? NL : 1],
                                             const int4 (&fv)[NF > 0 ? NF : 1], const int4& mv,
@@ -818,6 +824,16 @@ __global__ void __launch_bounds__(kStreamThreads) scan_direct_kernel(const ScanA
 #pragma unroll
     for (int f = 0; f < NF; ++f) nfv[f] = ld_batch<NL, NF, MODE, PK>(a.ffc[f], nrow0, a.n);
     if (a.measure) nmv = ld_batch<NL, NF, MODE, PK>(a.mc, nrow0, a.n);
+    if (a.prefetch) {  // pull the rows `prefetch` steps ahead into L2 (no registers held)
+      const int64_t prow = row0 + a.prefetch * step;
+      if ((tid & 7) == 0 && prow < a.n) {
+#pragma unroll
+        for (int j = 0; j < NL; ++j) prefetch_l2(a.fkc[j], prow);
+#pragma unroll
+        for (int f = 0; f < NF; ++f) prefetch_l2(a.ffc[f], prow);
+        if (a.measure) prefetch_l2(a.mc, prow);
+      }
+    }
 
     if (it < full) direct_rows<NL, NF, MODE, PK, false>(a, row0, kv, fv, mv, tab_addr, bins, r_cnt, r_sum);
     else direct_rows<NL, NF, MODE, PK, true>(a, row0, kv, fv, mv, tab_addr, bins, r_cnt, r_sum);
