@@ -182,11 +182,16 @@ __global__ void code_kernel(const CodeArgs a) {
 constexpr int kMaxCodeLinks = 8;
 struct MultiCodeArgs {
   int n;
-  int64_t start[kMaxCodeLinks + 1];  // prefix of slot counts
+  int64_t start[kMaxCodeLinks + 1];  // prefix of slot counts, each rounded up to 32
+  int64_t slots[kMaxCodeLinks];
   const int32_t* slot_row[kMaxCodeLinks];
+  int fmt[kMaxCodeLinks];
+  void* packed[kMaxCodeLinks];
   CodeArgs link[kMaxCodeLinks];
 };
 
+// Links start at multiples of 32 slots, so a warp's 32 consecutive indices are
+// 32 consecutive slots of one link (the bitmap word is one warp ballot).
 __global__ void codes_kernel(const MultiCodeArgs m) {
   const int64_t total = m.start[m.n];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -194,7 +199,8 @@ __global__ void codes_kernel(const MultiCodeArgs m) {
     while (i >= m.start[j + 1]) ++j;
     const CodeArgs& a = m.link[j];
     const int64_t s = i - m.start[j];
-    const int32_t r = m.slot_row[j] ? __ldg(m.slot_row[j] + s) : -1;
+    const bool in = s < m.slots[j];
+    const int32_t r = in && m.slot_row[j] ? __ldg(m.slot_row[j] + s) : -1;
     int64_t code = -1;
     if (r >= 0) {
       bool pass = true;
@@ -205,7 +211,16 @@ __global__ void codes_kernel(const MultiCodeArgs m) {
         for (int g = 0; g < a.n_groups; ++g) code += (static_cast<int64_t>(a.g[g].col[r]) - a.g[g].mn) * a.g[g].stride;
       }
     }
-    a.code[s] = static_cast<int32_t>(code);
+    if (in) a.code[s] = static_cast<int32_t>(code);
+    const int fmt = m.fmt[j];
+    if (fmt == scan::kFmtS16) {
+      if (in) static_cast<int16_t*>(m.packed[j])[s] = static_cast<int16_t>(code);
+    } else if (fmt == scan::kFmtU8) {
+      if (in) static_cast<uint8_t*>(m.packed[j])[s] = code < 0 ? 255 : static_cast<uint8_t>(code);
+    } else if (fmt == scan::kFmtBit) {
+      const unsigned bits = __ballot_sync(0xffffffffu, code >= 0);
+      if ((threadIdx.x & 31) == 0) static_cast<uint32_t*>(m.packed[j])[s >> 5] = bits;
+    }
   }
 }
 
@@ -343,6 +358,10 @@ struct laq_plan {
     int64_t slots;       // allocated (>= 1)
     int64_t slots_used;  // slots the fused code kernel writes (= slots)
     const int32_t* slot_row = nullptr;
+    int64_t max_code = 0;  // largest group-id contribution of this link
+    int fmt = scan::kFmtGlobal;  // compact copy for the direct scan (ssb_scan.cuh)
+    DevMem<uint8_t> packed;
+    int64_t packed_bytes = 0;  // multiple of 16
   };
   std::vector<LinkCode> links;  // in query join order
   DevMem<int64_t> sets;         // INSET values of every filter
@@ -362,13 +381,19 @@ namespace laq {
 namespace {
 
 void build_codes(laq_ctx* ctx, laq_plan* p) {
-  if (!p->links.empty() && p->links.size() <= kMaxCodeLinks && !std::getenv("LAQ_CODES_PER_LINK")) {
+  bool compact = false;
+  for (auto& lc : p->links) compact = compact || lc.fmt != scan::kFmtGlobal;
+  if (!p->links.empty() && p->links.size() <= kMaxCodeLinks && (compact || !std::getenv("LAQ_CODES_PER_LINK"))) {
     MultiCodeArgs m{};
     m.n = static_cast<int>(p->links.size());
     for (int j = 0; j < m.n; ++j) {
-      m.link[j] = p->links[j].args;
-      m.slot_row[j] = p->links[j].slot_row;
-      m.start[j + 1] = m.start[j] + p->links[j].slots_used;
+      const auto& lc = p->links[j];
+      m.link[j] = lc.args;
+      m.slot_row[j] = lc.slot_row;
+      m.slots[j] = lc.slots_used;
+      m.fmt[j] = lc.fmt;
+      m.packed[j] = lc.packed.get();
+      m.start[j + 1] = m.start[j] + ((lc.slots_used + 31) & ~int64_t{31});
     }
     if (m.start[m.n] > 0) {
       codes_kernel<<<grid_for(m.start[m.n], 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(m);
@@ -418,6 +443,81 @@ void lay_out_scan(laq_ctx* ctx, laq_plan* p, const std::vector<const int32_t*>& 
   const bool narrow = a.measure == nullptr || (measure_min >= 0 && vmax < (int64_t{1} << 21));
   const int64_t bin_bytes = p->mode == 1 ? (narrow ? 8 : 16) * p->G : 0;
   const int64_t tab_budget = budget - bin_bytes - 4 * stage_bytes;
+
+  // The direct-probe kernel (ssb_scan.cuh) when every link is a DIRECT table,
+  // the group id comes from the links only and the bins are narrow: every SSB
+  // query.  LAQ_SCAN=stream|pipe|ldg selects the generic kernels.
+  const char* want_env = std::getenv("LAQ_SCAN");
+  bool inset_filter = false;
+  for (int f = 0; f < p->nf; ++f) inset_filter = inset_filter || a.ff[f].inset;
+  bool direct = (!want_env || std::string(want_env) == "direct") && p->vec && all_padded && !inset_filter && nc >= 1 && a.n_fgroups == 0 && p->mode != 2 &&
+                (p->mode == 0 || narrow) && nl <= static_cast<int>(kMaxCodeLinks);
+  for (int j = 0; j < nl; ++j) direct = direct && probes[j]->kind == PROBE_DIRECT;
+  if (direct) {
+    const int64_t dbins = p->mode == 1 ? 8 * p->G : 0;
+    int64_t room = budget - dbins;
+    // Each link's most compact shared format; smallest tables first while they fit.
+    std::vector<int64_t> need(nl, 0);
+    std::vector<int> fmt(nl, scan::kFmtGlobal);
+    for (int j = 0; j < nl; ++j) {
+      const auto& lc = p->links[j];
+      const int64_t slots = probes[j]->size;
+      if (lc.args.n_groups == 0) fmt[j] = scan::kFmtBit, need[j] = ((slots + 31) / 32) * 4;
+      else if (lc.max_code <= 254) fmt[j] = scan::kFmtU8, need[j] = slots;
+      else if (lc.max_code <= 32767) fmt[j] = scan::kFmtS16, need[j] = 2 * slots;
+      need[j] = (need[j] + 15) & ~int64_t{15};
+    }
+    std::vector<int> by(nl);
+    std::iota(by.begin(), by.end(), 0);
+    std::stable_sort(by.begin(), by.end(), [&](int x, int y) { return need[x] < need[y]; });
+    int64_t off = 0;
+    std::vector<int64_t> smem_off(nl, -1);
+    for (int j : by) {
+      auto& lc = p->links[j];
+      lc.fmt = scan::kFmtGlobal;
+      if (std::getenv("LAQ_NOSMEMTAB") || need[j] > room) continue;
+      lc.fmt = fmt[j];
+      lc.packed_bytes = need[j];
+      lc.packed = DevMem<uint8_t>(need[j]);
+      smem_off[j] = off;  // bytes
+      off += need[j];
+      room -= need[j];
+    }
+    build_codes(ctx, p);  // fills the compact copies
+    std::vector<double> rank(nl);
+    for (int j = 0; j < nl; ++j) rank[j] = (p->links[j].fmt != scan::kFmtGlobal ? 1.0 : 8.0) / std::max(1.0 - frac[j], 1e-9);
+    std::vector<int> order(nl);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return rank[x] < rank[y]; });
+    bool gathers = false;
+    for (int q = 0; q < nl; ++q) {
+      const int j = order[q];
+      const Probe& pr = *probes[j];
+      const auto& lc = p->links[j];
+      a.fk[q] = fks[j];
+      a.fkc[q] = fkcols[j];
+      LinkProbe lp{pr.kind, pr.base, pr.size, pr.keys.get(), lc.code.get(), -1};
+      lp.fmt = lc.fmt;
+      lp.smem_byte = lc.fmt != scan::kFmtGlobal ? static_cast<int>(smem_off[j]) : 0;
+      lp.smem_bytes = static_cast<int>(lc.packed_bytes);
+      lp.packed = lc.packed.get();
+      a.link[q] = lp;
+      gathers = gathers || lc.fmt == scan::kFmtGlobal;
+    }
+    a.smem_tab_elems = static_cast<int>(off);  // bytes for this kernel
+    a.narrow_bins = narrow ? 1 : 0;
+    a.flush_every = std::max<int64_t>(1, (int64_t{1} << 32) / (int64_t{scan::kDirectThreads} * 4 * vmax) - 1);
+    // L2 prefetch of the fact rows 2 grid steps ahead when some link gathers
+    // from L2 (Q2.x at SF=10: 0.184 -> 0.169 ms); plans probing shared memory
+    // only run at the copy bandwidth and measured slower with it (0.144 -> 0.160).
+    a.prefetch = gathers ? 2 : 0;
+    if (const char* pf = std::getenv("LAQ_PREFETCH")) a.prefetch = std::atoi(pf);
+    p->variant = 4;
+    p->smem = static_cast<size_t>(off + dbins);
+    p->grid = ctx->sm_count;  // one 1024-thread CTA per SM
+    p->pipe = false;
+    return;
+  }
 
   // 1) Which code tables live in shared memory: smallest first while they fit.
   std::vector<int> by_size(nl);
@@ -833,6 +933,7 @@ int laq_query_prepare(laq_ctx* ctx, const laq_star* cs, const laq_query_desc* q,
         if (q->group_by[g].target != j) continue;
         if (ca.n_groups >= kMaxDimGroups) fail(LAQ_ERR_UNSUPPORTED, "at most 4 group columns per dimension");
         ca.g[ca.n_groups++] = DimGroup{gc[g]->d, plan->gcols[g].mn, plan->gcols[g].stride};
+        lc.max_code += (plan->gcols[g].range - 1) * plan->gcols[g].stride;
       }
       fks[j] = fk.d;
       fkcols[j] = fk.view();
@@ -867,27 +968,13 @@ int laq_query_prepare(laq_ctx* ctx, const laq_star* cs, const laq_query_desc* q,
     plan->bytes_per_row = 4 * (plan->nl + plan->nf + a.n_fgroups + (a.measure ? 1 : 0));
     plan->packed_only = packed_only;
     lay_out_scan(ctx, plan.get(), fks, fkcols, probes, mmin, mmax, padded);
-    if (packed_only && plan->variant != 2)
+    if (packed_only && plan->variant != 2 && plan->variant != 4)
       fail(LAQ_ERR_UNSUPPORTED, "byte-packed fact columns need the stream scan (no fact InSet filter, G <= 4096)");
-    if (plan->variant == 2) {  // the stream kernels read the packed views
+    if (plan->variant == 2 || plan->variant == 4) {  // the stream kernels read the packed views
       bool any_packed = a.measure && a.mc.w != 4;
       for (int j = 0; j < plan->nl; ++j) any_packed = any_packed || a.fkc[j].w != 4;
       for (int f = 0; f < plan->nf; ++f) any_packed = any_packed || a.ffc[f].w != 4;
-      if (any_packed) plan->variant = 3;
-      // The direct-probe form of the same kernel (ssb_scan.cuh) when every link
-      // is a DIRECT table, the group id comes from the links only and the bins
-      // are narrow: every SSB query.  LAQ_SCAN=stream keeps the generic form.
-      bool direct = a.n_fgroups == 0 && plan->mode != 2 && (plan->mode == 0 || a.narrow_bins);
-      for (int j = 0; j < plan->nl; ++j) direct = direct && a.link[j].kind == PROBE_DIRECT;
-      const char* want = std::getenv("LAQ_SCAN");
-      if (direct && !(want && std::string(want) == "stream")) plan->variant += 2;
-      // L2 prefetch of the fact rows 2 grid steps ahead when some link gathers
-      // from L2 (Q2.x: 0.184 -> 0.169 ms); plans probing shared memory only are
-      // already at the copy bandwidth and measured slower with it (0.144 -> 0.160).
-      bool gathers = false;
-      for (int j = 0; j < plan->nl; ++j) gathers = gathers || a.link[j].smem_off < 0;
-      a.prefetch = gathers ? 2 : 0;
-      if (const char* pf = std::getenv("LAQ_PREFETCH")) a.prefetch = std::atoi(pf);
+      if (any_packed) plan->variant += 1;
       int64_t b = 4 * a.n_fgroups + (a.measure ? a.mc.w : 0);
       for (int j = 0; j < plan->nl; ++j) b += a.fkc[j].w;
       for (int f = 0; f < plan->nf; ++f) b += a.ffc[f].w;

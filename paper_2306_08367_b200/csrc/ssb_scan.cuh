@@ -45,7 +45,19 @@ struct LinkProbe {
   const int64_t* keys;
   const int32_t* code;  // per slot, global
   int smem_off;         // >= 0: int16 code table staged in smem at this element offset
+  // direct kernel: the table's format and where it is staged
+  int fmt;              // kFmtGlobal / kFmtS16 / kFmtU8 / kFmtBit
+  int smem_byte;        // byte offset of the staged table (fmt != kFmtGlobal)
+  int smem_bytes;       // staged bytes (multiple of 16)
+  const void* packed;   // the compact table in global memory (fmt != kFmtGlobal)
 };
+
+// Code-table formats of the direct kernel (a link's code is its contribution to
+// the group id, -1 = the dim row fails the filters or the key has no row):
+//   global int32 (gathered through L2), shared int16, shared uint8 (255 = -1;
+//   the contribution fits 0..254), shared bitmap (the link filters only:
+//   contribution 0, bit = passes).
+enum : int { kFmtGlobal = 0, kFmtS16 = 1, kFmtU8 = 2, kFmtBit = 3 };
 
 // A fact predicate lowered to  lo <= v <= hi  over int32 (or InSet).
 struct FactFilter {
@@ -693,13 +705,32 @@ __global__ void __launch_bounds__(kStreamThreads) scan_stream_kernel(const ScanA
 // addressed with 32-bit shared-window addresses computed once, full grid
 // steps run without row bounds (one bounded tail step), the spill test is a
 // countdown, and each probe is  slot = key - base; slot < size ? table[slot]
-// : -1  with the shared/global choice a warp-uniform branch per link.
+// : -1  with the table format a warp-uniform branch per link.
+//
+// One 1024-thread CTA per SM (the register file holds 1024 threads at <= 64
+// registers anyway), so the SM's whole shared memory holds ONE copy of the
+// code tables, in the most compact format each link allows (int16, uint8,
+// or a pass bitmap for filter-only links): at SF=100 the 200K-slot supplier
+// table (Q3.x: uint8, 200 KB) and the 1.4M-slot part table (Q4.x: bitmap,
+// 175 KB) come out of L2 gathers into shared memory.
 // ---------------------------------------------------------------------------
+
+constexpr int kDirectThreads = 1024;
 
 __device__ __forceinline__ int32_t lds_s16(uint32_t addr) {
   int16_t v;
   asm volatile("ld.shared.s16 %0, [%1];" : "=h"(v) : "r"(addr));
   return static_cast<int32_t>(v);
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+  uint16_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(addr));
+  return static_cast<uint32_t>(v);
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
 }
 __device__ __forceinline__ void reds_add(uint32_t addr, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
@@ -736,22 +767,36 @@ __device__ __forceinline__ void direct_rows(const ScanArgs& a, int64_t row0, con
   for (int j = 0; j < NL; ++j) {
     const uint32_t base = static_cast<uint32_t>(a.link[j].base), size = static_cast<uint32_t>(a.link[j].size);
     const int4 k = unpack_batch<PK>(kv[j], a.fkc[j]);
+    const int fmt = a.link[j].fmt;
     int32_t c[4];
-    if (a.link[j].smem_off >= 0) {
+    uint32_t s[4];
+    bool ok[4];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const uint32_t s = static_cast<uint32_t>(comp(k, r)) - base;
-        c[r] = -1;
-        if (alive[r] && s < size) c[r] = lds_s16(tab_addr[j] + 2 * s);
-      }
+    for (int r = 0; r < 4; ++r) {
+      s[r] = static_cast<uint32_t>(comp(k, r)) - base;
+      ok[r] = alive[r] && s[r] < size;
+      c[r] = -1;
+    }
+    if (fmt == kFmtS16) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (ok[r]) c[r] = lds_s16(tab_addr[j] + 2 * s[r]);
+    } else if (fmt == kFmtU8) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (ok[r]) {
+          const uint32_t v = lds_u8(tab_addr[j] + s[r]);
+          c[r] = v == 255u ? -1 : static_cast<int32_t>(v);
+        }
+    } else if (fmt == kFmtBit) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (ok[r]) c[r] = ((lds_u32(tab_addr[j] + 4 * (s[r] >> 5)) >> (s[r] & 31)) & 1u) ? 0 : -1;
     } else {
       const int32_t* code = a.link[j].code;
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const uint32_t s = static_cast<uint32_t>(comp(k, r)) - base;
-        c[r] = -1;
-        if (alive[r] && s < size) c[r] = __ldg(code + s);
-      }
+      for (int r = 0; r < 4; ++r)
+        if (ok[r]) c[r] = __ldg(code + s[r]);
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
@@ -780,32 +825,35 @@ __device__ __forceinline__ void direct_rows(const ScanArgs& a, int64_t row0, con
 }
 
 // MODE 0 (one group: register accumulation) or MODE 1 with narrow (u32) bins.
+// Shared memory: [staged code tables (a.smem_tab_elems bytes)] [u32 bins 2G].
 template <int NL, int NF, int MODE, bool PK>
-__global__ void __launch_bounds__(kStreamThreads) scan_direct_kernel(const ScanArgs a) {
+__global__ void __launch_bounds__(kDirectThreads, 1) scan_direct_kernel(const ScanArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  int16_t* s_tab = reinterpret_cast<int16_t*>(smem);
-  uint32_t* b32 = reinterpret_cast<uint32_t*>(smem + ((a.smem_tab_elems * 2 + 15) & ~15));
+  uint32_t* b32 = reinterpret_cast<uint32_t*>(smem + a.smem_tab_elems);
   const int tid = threadIdx.x;
 #pragma unroll
   for (int j = 0; j < NL; ++j) {
     const LinkProbe& p = a.link[j];
-    if (p.smem_off >= 0)
-      for (int64_t s = tid; s < p.size; s += kStreamThreads) s_tab[p.smem_off + s] = static_cast<int16_t>(__ldg(p.code + s));
+    if (p.fmt != kFmtGlobal) {
+      const uint4* src = static_cast<const uint4*>(p.packed);
+      uint4* dst = reinterpret_cast<uint4*>(smem + p.smem_byte);
+      for (int w = tid; w < p.smem_bytes / 16; w += kDirectThreads) dst[w] = __ldg(src + w);
+    }
   }
   if constexpr (MODE == 1)
-    for (int64_t g = tid; g < 2 * a.n_groups; g += kStreamThreads) b32[g] = 0;
+    for (int64_t g = tid; g < 2 * a.n_groups; g += kDirectThreads) b32[g] = 0;
   __syncthreads();
 
   const uint32_t s_base = smem_u32(smem);
   const uint32_t bins = smem_u32(b32);
   uint32_t tab_addr[NL > 0 ? NL : 1];
 #pragma unroll
-  for (int j = 0; j < NL; ++j) tab_addr[j] = s_base + 2u * static_cast<uint32_t>(a.link[j].smem_off > 0 ? a.link[j].smem_off : 0);
+  for (int j = 0; j < NL; ++j) tab_addr[j] = s_base + static_cast<uint32_t>(a.link[j].smem_byte);
 
-  const int64_t step = static_cast<int64_t>(gridDim.x) * kStreamThreads * 4;
+  const int64_t step = static_cast<int64_t>(gridDim.x) * kDirectThreads * 4;
   const int64_t iters = (a.n + step - 1) / step;  // uniform across the block
   const int64_t full = a.n / step;                // steps with every row in range
-  int64_t row0 = (static_cast<int64_t>(blockIdx.x) * kStreamThreads + tid) * 4;
+  int64_t row0 = (static_cast<int64_t>(blockIdx.x) * kDirectThreads + tid) * 4;
 
   int4 kv[NL > 0 ? NL : 1], fv[NF > 0 ? NF : 1], mv = make_int4(0, 0, 0, 0);
 #pragma unroll
@@ -843,7 +891,7 @@ __global__ void __launch_bounds__(kStreamThreads) scan_direct_kernel(const ScanA
         until_flush = a.flush_every;
         if (it + 1 < iters) {
           __syncthreads();
-          spill_bins32(b32, a.n_groups, a.acc, tid, kStreamThreads);
+          spill_bins32(b32, a.n_groups, a.acc, tid, kDirectThreads);
           __syncthreads();
         }
       }
@@ -860,7 +908,7 @@ __global__ void __launch_bounds__(kStreamThreads) scan_direct_kernel(const ScanA
     flush_single(r_cnt, r_sum, a.acc);
   } else {
     __syncthreads();
-    spill_bins32(b32, a.n_groups, a.acc, tid, kStreamThreads);
+    spill_bins32(b32, a.n_groups, a.acc, tid, kDirectThreads);
   }
 }
 

@@ -22,11 +22,9 @@ void launch_variant(laq_ctx* ctx, const ScanArgs& a, int variant, bool vec, int 
     } else {
       auto kern = variant == 5 ? scan_direct_kernel<NL, NF, MODE, true> : scan_direct_kernel<NL, NF, MODE, false>;
       LAQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-      int per_sm = 0;
-      LAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStreamThreads, smem));
-      const int64_t blocks_needed = (a.n + kStreamThreads * 4 - 1) / (kStreamThreads * 4);
-      const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(int64_t{grid} * std::max(per_sm, 1), blocks_needed)));
-      kern<<<g, kStreamThreads, smem, s>>>(a);
+      const int64_t blocks_needed = (a.n + kDirectThreads * 4 - 1) / (kDirectThreads * 4);
+      const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(grid, blocks_needed)));
+      kern<<<g, kDirectThreads, smem, s>>>(a);
     }
   } else if (variant == 2 || variant == 3) {
     auto kern = variant == 3 ? scan_stream_kernel<NL, NF, MODE, true> : scan_stream_kernel<NL, NF, MODE, false>;
