@@ -422,7 +422,7 @@ def main():
                        "per_query_scan_ms": [round(float(x), 4) for x in scan_ms.mean(axis=0)]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                         "kernel": "scan_kernel (K4 ssb_scan_groupby)",
+                         "kernel": "scan_direct_kernel (K4 ssb_scan_groupby)",
                          "algorithmic_bytes_per_launch": [int(b) for b in bytes_per_launch],
                          "peak_source": peak_src},
             "cpu_baseline": cpu,
