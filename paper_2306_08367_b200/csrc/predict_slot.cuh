@@ -96,6 +96,7 @@ __device__ __forceinline__ unsigned long long resolve(unsigned long long* state,
 constexpr int kChunkRows = 1024;
 constexpr int kChunkSteps = kChunkRows / 32;
 constexpr int kWarpThreads = 256;
+constexpr int kDirectBT = 1024;  // direct_chunks_kernel CTA size (one CTA per SM)
 
 __device__ __forceinline__ void stage_bits(const Args& a, uint32_t* s_bits, int nl) {
   for (int j = 0; j < nl; ++j)
@@ -186,8 +187,11 @@ __global__ void __launch_bounds__(kWarpThreads) count_chunks_kernel(const Args a
 // the fallback decision is taken on the device, so the call stays capturable.
 // HBM per row: 4*J bytes of keys + 8 bytes of prediction (cfg1: 12 B).
 // ---------------------------------------------------------------------------
-template <int NL>
-__global__ void __launch_bounds__(kWarpThreads) direct_chunks_kernel(const Args a, int64_t n_chunks, int* counts,
+// BT threads per CTA: 1024 by default -- one CTA per SM holds ONE staged copy
+// of the partials (80 KB for cfg1), so residency is 32 warps/SM instead of the
+// 16 that two 256-thread CTAs with a copy each allow.
+template <int NL, int BT = kWarpThreads>
+__global__ void __launch_bounds__(BT, 1) direct_chunks_kernel(const Args a, int64_t n_chunks, int* counts,
                                                                      unsigned long long* miss) {
   extern __shared__ __align__(16) uint32_t s_bits[];
   double* s_p = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(s_bits) + ((a.smem_words * 4 + 15) & ~15));
@@ -195,14 +199,14 @@ __global__ void __launch_bounds__(kWarpThreads) direct_chunks_kernel(const Args 
 #pragma unroll
   for (int j = 0; j < NL; ++j)
     if (a.p_off[j] >= 0)
-      for (int64_t s = threadIdx.x; s < a.size[j]; s += kWarpThreads) s_p[a.p_off[j] + s] = __ldg(a.pslot[j] + s);
+      for (int64_t s = threadIdx.x; s < a.size[j]; s += BT) s_p[a.p_off[j] + s] = __ldg(a.pslot[j] + s);
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t warps = static_cast<int64_t>(gridDim.x) * (kWarpThreads / 32);
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (BT / 32);
   auto pval = [&](int j, uint32_t s) -> double {
     return a.p_off[j] >= 0 ? s_p[a.p_off[j] + s] : __ldg(a.pslot[j] + s);
   };
-  for (int64_t c = (static_cast<int64_t>(blockIdx.x) * kWarpThreads + threadIdx.x) >> 5; c < n_chunks; c += warps) {
+  for (int64_t c = (static_cast<int64_t>(blockIdx.x) * BT + threadIdx.x) >> 5; c < n_chunks; c += warps) {
     int cnt = 0;
     // Every key load of the chunk first (8 segments x 16 B per link and lane in
     // flight: the partials' shared-memory footprint caps residency at 2 CTAs/SM,

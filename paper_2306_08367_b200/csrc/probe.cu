@@ -526,15 +526,23 @@ void run_slot_predict(laq_ctx* ctx, laq_probe* p, const int32_t* const* d_fks, i
   // compaction fallback (direct_chunks_kernel); otherwise count + scan + write.
   const bool optimistic = l == 1 && !std::getenv("LAQ_PREDICT_TWO_PASS");
   if (optimistic) LAQ_CUDA(cudaMemsetAsync(p->miss.get(), 0, sizeof(unsigned long long), ctx->stream));
-  auto launch = [&](auto count_k, auto direct_k, auto write_k) {
+  auto launch = [&](auto count_k, auto direct_k, auto direct_small_k, auto write_k) {
     LAQ_CUDA(cudaFuncSetAttribute(write_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_w)));
-    LAQ_CUDA(cudaFuncSetAttribute(direct_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_w)));
     const int64_t want = (n_chunks + slot::kWarpThreads / 32 - 1) / (slot::kWarpThreads / 32);
     int per_sm = 0;
-    if (optimistic) {
-      LAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, direct_k, slot::kWarpThreads, smem_w));
+    // Large inputs: one 1024-thread CTA per SM (one staged copy of the partials,
+    // 32 warps/SM; 1e8 rows 0.278 -> 0.218 ms).  Below two chunks per warp of
+    // such a grid, 256-thread CTAs spread the chunks over every SM instead.
+    const bool big = n_chunks >= int64_t{ctx->sm_count} * (slot::kDirectBT / 32) * 2;
+    if (optimistic && big) {
+      LAQ_CUDA(cudaFuncSetAttribute(direct_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_w)));
+      const unsigned g0 = static_cast<unsigned>(ctx->sm_count);
+      direct_k<<<g0, slot::kDirectBT, smem_w, ctx->stream>>>(a, n_chunks, p->chunk_counts.get(), p->miss.get());
+    } else if (optimistic) {
+      LAQ_CUDA(cudaFuncSetAttribute(direct_small_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_w)));
+      LAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, direct_small_k, slot::kWarpThreads, smem_w));
       const unsigned g0 = static_cast<unsigned>(std::min<int64_t>(want, int64_t{ctx->sm_count} * std::max(per_sm, 1)));
-      direct_k<<<g0, slot::kWarpThreads, smem_w, ctx->stream>>>(a, n_chunks, p->chunk_counts.get(), p->miss.get());
+      direct_small_k<<<g0, slot::kWarpThreads, smem_w, ctx->stream>>>(a, n_chunks, p->chunk_counts.get(), p->miss.get());
     } else {
       LAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, count_k, slot::kWarpThreads, smem));
       const unsigned g1 = static_cast<unsigned>(std::min<int64_t>(want, int64_t{ctx->sm_count} * std::max(per_sm, 1)));
@@ -551,7 +559,8 @@ void run_slot_predict(laq_ctx* ctx, laq_probe* p, const int32_t* const* d_fks, i
   };
   switch (p->n_links) {
 #define LAQ_SLOT_CASE(N) \
-    case N: launch(slot::count_chunks_kernel<N>, slot::direct_chunks_kernel<N>, slot::write_chunks_kernel<N>); break;
+    case N: launch(slot::count_chunks_kernel<N>, slot::direct_chunks_kernel<N, slot::kDirectBT>, \
+                   slot::direct_chunks_kernel<N, slot::kWarpThreads>, slot::write_chunks_kernel<N>); break;
     LAQ_SLOT_CASE(1) LAQ_SLOT_CASE(2) LAQ_SLOT_CASE(3) LAQ_SLOT_CASE(4)
     LAQ_SLOT_CASE(5) LAQ_SLOT_CASE(6) LAQ_SLOT_CASE(7) LAQ_SLOT_CASE(8)
 #undef LAQ_SLOT_CASE
