@@ -737,8 +737,10 @@ __device__ __forceinline__ void reds_add(uint32_t addr, uint32_t v) {
 }
 
 // One 128-byte line per 8 lanes (8 lanes x 4 rows x 4 B) of a column.
+template <bool PK>
 __device__ __forceinline__ void prefetch_l2(const Col& c, int64_t row0) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<const uint8_t*>(c.p) + row0 * c.w));
+  const uint8_t* p = static_cast<const uint8_t*>(c.p) + (PK ? row0 * c.w : row0 * 4);
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
 template <int NL, int NF, int MODE, bool PK, bool TAIL>
@@ -854,38 +856,37 @@ __global__ void __launch_bounds__(kDirectThreads, 1) scan_direct_kernel(const Sc
   const int64_t iters = (a.n + step - 1) / step;  // uniform across the block
   const int64_t full = a.n / step;                // steps with every row in range
   int64_t row0 = (static_cast<int64_t>(blockIdx.x) * kDirectThreads + tid) * 4;
+  const bool pf_lane = a.prefetch && (tid & 7) == 0;
+  const int64_t pf_rows = static_cast<int64_t>(a.prefetch) * step;
 
-  int4 kv[NL > 0 ? NL : 1], fv[NF > 0 ? NF : 1], mv = make_int4(0, 0, 0, 0);
+  // Two register buffers used in turn (the loop is unrolled by two so the
+  // double buffer needs no register moves).
+  int4 kvA[NL > 0 ? NL : 1], fvA[NF > 0 ? NF : 1], mvA = make_int4(0, 0, 0, 0);
+  int4 kvB[NL > 0 ? NL : 1], fvB[NF > 0 ? NF : 1], mvB = make_int4(0, 0, 0, 0);
+  auto load = [&](int4 (&kv)[NL > 0 ? NL : 1], int4 (&fv)[NF > 0 ? NF : 1], int4& mv, int64_t r) {
 #pragma unroll
-  for (int j = 0; j < NL; ++j) kv[j] = ld_batch<NL, NF, MODE, PK>(a.fkc[j], row0, a.n);
+    for (int j = 0; j < NL; ++j) kv[j] = ld_batch<NL, NF, MODE, PK>(a.fkc[j], r, a.n);
 #pragma unroll
-  for (int f = 0; f < NF; ++f) fv[f] = ld_batch<NL, NF, MODE, PK>(a.ffc[f], row0, a.n);
-  if (a.measure) mv = ld_batch<NL, NF, MODE, PK>(a.mc, row0, a.n);
+    for (int f = 0; f < NF; ++f) fv[f] = ld_batch<NL, NF, MODE, PK>(a.ffc[f], r, a.n);
+    if (a.measure) mv = ld_batch<NL, NF, MODE, PK>(a.mc, r, a.n);
+  };
+  load(kvA, fvA, mvA, row0);
 
   unsigned long long r_cnt = 0, r_sum = 0;
   int64_t until_flush = a.narrow_bins ? a.flush_every : INT64_MAX;
-  for (int64_t it = 0; it < iters; ++it) {
-    const int64_t nrow0 = row0 + step;
-    int4 nkv[NL > 0 ? NL : 1], nfv[NF > 0 ? NF : 1], nmv = make_int4(0, 0, 0, 0);
+  // One grid step: prefetch the next rows into the other buffer, process these.
+  auto one = [&](int64_t it, const int4 (&kv)[NL > 0 ? NL : 1], const int4 (&fv)[NF > 0 ? NF : 1], const int4& mv,
+                 int4 (&nkv)[NL > 0 ? NL : 1], int4 (&nfv)[NF > 0 ? NF : 1], int4& nmv) {
+    load(nkv, nfv, nmv, row0 + step);
+    if (pf_lane && row0 + pf_rows < a.n) {  // the rows `prefetch` steps ahead into L2 (no registers held)
 #pragma unroll
-    for (int j = 0; j < NL; ++j) nkv[j] = ld_batch<NL, NF, MODE, PK>(a.fkc[j], nrow0, a.n);
+      for (int j = 0; j < NL; ++j) prefetch_l2<PK>(a.fkc[j], row0 + pf_rows);
 #pragma unroll
-    for (int f = 0; f < NF; ++f) nfv[f] = ld_batch<NL, NF, MODE, PK>(a.ffc[f], nrow0, a.n);
-    if (a.measure) nmv = ld_batch<NL, NF, MODE, PK>(a.mc, nrow0, a.n);
-    if (a.prefetch) {  // pull the rows `prefetch` steps ahead into L2 (no registers held)
-      const int64_t prow = row0 + a.prefetch * step;
-      if ((tid & 7) == 0 && prow < a.n) {
-#pragma unroll
-        for (int j = 0; j < NL; ++j) prefetch_l2(a.fkc[j], prow);
-#pragma unroll
-        for (int f = 0; f < NF; ++f) prefetch_l2(a.ffc[f], prow);
-        if (a.measure) prefetch_l2(a.mc, prow);
-      }
+      for (int f = 0; f < NF; ++f) prefetch_l2<PK>(a.ffc[f], row0 + pf_rows);
+      if (a.measure) prefetch_l2<PK>(a.mc, row0 + pf_rows);
     }
-
     if (it < full) direct_rows<NL, NF, MODE, PK, false>(a, row0, kv, fv, mv, tab_addr, bins, r_cnt, r_sum);
     else direct_rows<NL, NF, MODE, PK, true>(a, row0, kv, fv, mv, tab_addr, bins, r_cnt, r_sum);
-
     if constexpr (MODE == 1) {
       if (--until_flush == 0) {
         until_flush = a.flush_every;
@@ -896,12 +897,11 @@ __global__ void __launch_bounds__(kDirectThreads, 1) scan_direct_kernel(const Sc
         }
       }
     }
-#pragma unroll
-    for (int j = 0; j < NL; ++j) kv[j] = nkv[j];
-#pragma unroll
-    for (int f = 0; f < NF; ++f) fv[f] = nfv[f];
-    mv = nmv;
-    row0 = nrow0;
+    row0 += step;
+  };
+  for (int64_t it = 0; it < iters; it += 2) {
+    one(it, kvA, fvA, mvA, kvB, fvB, mvB);
+    if (it + 1 < iters) one(it + 1, kvB, fvB, mvB, kvA, fvA, mvA);
   }
 
   if constexpr (MODE == 0) {
