@@ -274,6 +274,24 @@ int laq_groupby_sum_multi(laq_ctx* ctx, int32_t n_cols, const int64_t* const* d_
                           const double* d_vals, int64_t n, int64_t* d_out_keys, double* d_out_sums,
                           int64_t capacity, int64_t* h_n_groups);
 
+/* ---- ingest: the reference's CSV table format parsed on the device
+ *      (load_csv storage.cpp:112-150; load_dataset cli.cpp:483-513) ---- */
+
+typedef struct laq_csv laq_csv;
+/* Index the lines of a CSV text already in device memory (caller-owned, kept
+ * alive until laq_csv_close): getline semantics -- '\n' separated, a final line
+ * without '\n' counts, a trailing '\n' opens none.  *h_lines = rows. */
+int laq_csv_open(laq_ctx* ctx, const char* d_text, int64_t nbytes, laq_csv** out, int64_t* h_lines);
+/* Parse every line into n_cols device columns (d_cols[c]: int64 for
+ * LAQ_COL_KEY / LAQ_COL_INT, double for LAQ_COL_FLOAT; capacity = lines),
+ * std::from_chars semantics per field.  The first failing line in file order
+ * returns LAQ_ERR_FORMAT with the reference's message ("line N: expected K
+ * fields" / "missing value" / "bad integer 'x'" / "bad float 'x'").
+ * LAQ_ERR_UNSUPPORTED for a float with > 19 significant digits whose dropped
+ * digits decide the rounding. */
+int laq_csv_parse(laq_ctx* ctx, const laq_csv* f, int32_t n_cols, const int32_t* h_kinds, void* const* d_cols);
+int laq_csv_close(laq_csv* f);
+
 /* ---- star schema + query plan driver (storage.hpp:75-100, cli.cpp:73-138) ---- */
 
 enum laq_col_kind { LAQ_COL_KEY = 0, LAQ_COL_INT = 1, LAQ_COL_FLOAT = 2 }; /* storage.hpp:14 */
@@ -282,7 +300,8 @@ enum laq_col_kind { LAQ_COL_KEY = 0, LAQ_COL_INT = 1, LAQ_COL_FLOAT = 2 }; /* st
  * device (range-checked; LAQ_ERR_CAPACITY if a value does not fit). */
 int laq_star_create(laq_ctx* ctx, laq_star** out);
 int laq_star_destroy(laq_star* star);
-/* Add a table from HOST columns: key/int kinds are int64 (the reference's
+/* Add a table from host (or, through unified addressing, device) columns:
+ * key/int kinds are int64 (the reference's
  * IntColumn, storage.hpp:35) when int_width == 8, or already-narrowed int32
  * when int_width == 4; float columns are double.  The table added with
  * is_fact=1 is the fact table.  Key columns must be non-negative

@@ -19,12 +19,14 @@
 //            multiway_star_join, materialize, groupby_sum_single/_multi
 //            (laqops.cpp:142-455);  prefuse_linear, apply_fused_linear,
 //            speedup_ratio_linear/_tree, decide_fusion (fusion.cpp:50-77, 199-224);
-//            run_query_laq (cli.cpp:73-138).
+//            run_query_laq (cli.cpp:73-138);  load_csv (storage.cpp:112-150).
 
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <chrono>
+#include <fstream>
+#include <iterator>
 #include <cstring>
 #include <numeric>
 #include <set>
@@ -36,6 +38,7 @@
 #include "laq/laqops.hpp"
 #include "laq/matrix.hpp"
 #include "laq/predicate.hpp"
+#include "laq/storage.hpp"
 #include "laq_b200.h"
 
 // ---- legal access to Predicate's private constants (explicit instantiation
@@ -823,4 +826,53 @@ DenseMat run_query_laq(const StarSchema& data, const bench::QuerySpec& q, StageT
 }
 
 }  // namespace cli
+
+// load_csv (storage.cpp:112-150): the file is read on the host, lines indexed
+// and fields parsed on the device (csv.cu; from_chars semantics, the same
+// FormatError messages), the columns copied back into the owning Table.
+Table load_csv(const std::filesystem::path& path, const Schema& schema) {
+  schema.validate();
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw FormatError("cannot open " + path.string());
+  const std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  const index_t ncols = schema.col_count();
+  Dev<char> d_text(text.size() + 16);
+  d_text.up(text.data(), text.size());
+  if (cudaMemset(d_text.p + text.size(), 0, 16) != cudaSuccess) throw Error("laq_b200: memset");
+  laq_csv* f = nullptr;
+  int64_t rows = 0;
+  check(laq_csv_open(ctx(), d_text.p, static_cast<int64_t>(text.size()), &f, &rows));
+  struct Close {
+    laq_csv* f;
+    ~Close() { laq_csv_close(f); }
+  } close_f{f};
+  std::vector<int32_t> kinds(ncols);
+  std::vector<Dev<char>> bufs;
+  std::vector<void*> ptrs(ncols);
+  bufs.reserve(ncols);
+  for (index_t c = 0; c < ncols; ++c) {
+    kinds[c] = schema.kind(c) == ColKind::Key ? LAQ_COL_KEY : schema.kind(c) == ColKind::Int ? LAQ_COL_INT : LAQ_COL_FLOAT;
+    bufs.emplace_back(static_cast<size_t>(std::max<int64_t>(rows, 1)) * 8);
+    ptrs[c] = bufs.back().p;
+  }
+  check(laq_csv_parse(ctx(), f, static_cast<int32_t>(ncols), kinds.data(), ptrs.data()));
+  if (cudaStreamSynchronize(nullptr) != cudaSuccess || laq_ctx_synchronize(ctx()) != LAQ_OK) throw Error("laq_b200: sync");
+  std::vector<Column> cols;
+  cols.reserve(ncols);
+  for (index_t c = 0; c < ncols; ++c) {
+    if (kinds[c] == LAQ_COL_FLOAT) {
+      FloatColumn v(static_cast<size_t>(rows));
+      if (rows && cudaMemcpy(v.data(), ptrs[c], rows * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+        throw Error("laq_b200: D2H");
+      cols.emplace_back(std::move(v));
+    } else {
+      IntColumn v(static_cast<size_t>(rows));
+      if (rows && cudaMemcpy(v.data(), ptrs[c], rows * sizeof(int64_t), cudaMemcpyDeviceToHost) != cudaSuccess)
+        throw Error("laq_b200: D2H");
+      cols.emplace_back(std::move(v));
+    }
+  }
+  return Table(schema, std::move(cols));
+}
+
 }  // namespace laq

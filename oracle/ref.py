@@ -58,6 +58,9 @@ def lib():
         L.ref_star_col_data.restype = C.c_void_p
         L.ref_star_col_data.argtypes = [C.c_void_p, C.c_int, C.c_int]
         L.ref_checksum_rows.restype = C.c_uint64
+        L.ref_write_dataset.argtypes = [C.c_int, C.c_int64, C.c_uint64, C.c_int64, C.c_double, C.c_char_p]
+        L.ref_load_csv.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_int32), C.c_int64, C.POINTER(C.c_void_p),
+                                   C.POINTER(C.c_int64)]
         L.ref_checksum_rows.argtypes = [f64p, C.c_int64, C.c_int64]
         L.ref_star_make_shards.argtypes = [C.c_void_p, C.c_int]
         vp, i64, i32, dbl = C.c_void_p, C.c_int64, C.c_int, C.c_double
@@ -474,3 +477,29 @@ def fused_tree(tree, dims, placements, k, feature_owner, idx=None):
                                 _ptr_array(pls, C.c_int64), k, _p64(owner), ip, m,
                                 _p64(out) if out is not None else None, _ptr_array(parts, C.c_double)))
     return out, parts
+
+
+# ---- dataset files (cli.cpp:430-481, storage.cpp:112-150) ---------------------
+
+SETTINGS = {"S1": 0, "S2": 1, "Ssb": 2}
+
+
+def write_dataset(directory, setting="S2", sf=1, seed=42, features=0, dangling=0.0):
+    """The reference's write_dataset (CSV tables + manifest.json) for gen_star(cfg)."""
+    L = lib()
+    rc = L.ref_write_dataset(SETTINGS[setting], sf, seed, features, dangling, str(directory).encode())
+    if rc:
+        raise RefError(rc, L.ref_last_error().decode())
+
+
+def load_csv(path, kinds, cap):
+    """The reference's load_csv -> (columns list, rows) or RefError(code, message)."""
+    L = lib()
+    cols = [np.zeros(max(cap, 1), np.float64 if k == 2 else np.int64) for k in kinds]
+    kd = (C.c_int32 * len(kinds))(*kinds)
+    ptrs = (C.c_void_p * len(kinds))(*[c.ctypes.data for c in cols])
+    rows = C.c_int64()
+    rc = L.ref_load_csv(str(path).encode(), len(kinds), kd, cap, ptrs, C.byref(rows))
+    if rc:
+        raise RefError(rc, L.ref_last_error().decode())
+    return [c[:rows.value] for c in cols], rows.value

@@ -15,6 +15,7 @@
 #include <cstring>
 #include <map>
 #include <numeric>
+#include <optional>
 #include <string>
 #include <thread>
 #include <vector>
@@ -157,6 +158,41 @@ void* ref_gen_star(int setting, int64_t sf, uint64_t seed, int64_t feature_width
     h->index();
   });
   return rc == LAQ_OK ? h : nullptr;
+}
+
+// ---- dataset files (cli.cpp:430-481 write_dataset, storage.cpp:112-150 load_csv) ----
+int ref_write_dataset(int setting, int64_t sf, uint64_t seed, int64_t feature_width, double dangling,
+                      const char* dir) {
+  return guard([&] {
+    bench::GenConfig cfg;
+    cfg.sf = sf;
+    cfg.setting = setting == 0 ? bench::Setting::S1 : setting == 1 ? bench::Setting::S2 : bench::Setting::Ssb;
+    cfg.seed = seed;
+    cfg.feature_width = feature_width;
+    cfg.dangling_fraction = dangling;
+    cli::write_dataset(bench::gen_star(cfg), cfg, std::nullopt, dir);
+  });
+}
+
+// load_csv into caller buffers (int64 for key/int, double for float; kinds per
+// storage.hpp:14 order Key=0, Int=1, Float=2).  *rows = rows read; LAQ_ERR_CAPACITY
+// if more than cap.
+int ref_load_csv(const char* path, int ncols, const int32_t* kinds, int64_t cap, void* const* out, int64_t* rows) {
+  return guard([&] {
+    Schema sc;
+    for (int c = 0; c < ncols; ++c)
+      sc.columns.emplace_back("c" + std::to_string(c), kinds[c] == 0 ? ColKind::Key : kinds[c] == 1 ? ColKind::Int
+                                                                                                    : ColKind::Float);
+    const Table t = load_csv(path, sc);
+    *rows = t.row_count();
+    if (t.row_count() > cap) throw CapacityError("ref_load_csv: capacity");
+    for (int c = 0; c < ncols; ++c) {
+      if (kinds[c] == 2)
+        std::memcpy(out[c], t.floats(c).data(), t.row_count() * sizeof(double));
+      else
+        std::memcpy(out[c], t.ints(c).data(), t.row_count() * sizeof(int64_t));
+    }
+  });
 }
 
 void ref_star_free(void* h) { delete static_cast<RefStar*>(h); }

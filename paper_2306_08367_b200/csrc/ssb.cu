@@ -654,7 +654,7 @@ int laq_star_add_table(laq_star* s, const char* name, int32_t is_fact, int64_t r
           const int64_t* src = static_cast<const int64_t*>(h_cols[c]);
           for (int64_t b = 0; b < rows; b += chunk) {
             const int64_t m = std::min(chunk, rows - b);
-            LAQ_CUDA(cudaMemcpyAsync(stage.get(), src + b, m * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+            LAQ_CUDA(cudaMemcpyAsync(stage.get(), src + b, m * sizeof(int64_t), cudaMemcpyDefault, ctx->stream));
             narrow_kernel<<<grid_for(m, 256 * 8, ctx->sm_count * 8), 256, 0, ctx->stream>>>(stage.get(), col.d + b, m,
                                                                                            mnmx, overflow);
             launched(ctx);
@@ -667,7 +667,7 @@ int laq_star_add_table(laq_star* s, const char* name, int32_t is_fact, int64_t r
           if (*reinterpret_cast<int*>(ctx->h_pinned + 2))
             fail(LAQ_ERR_CAPACITY, "column '" + col.name + "' has values outside int32 (device layout)");
         } else {
-          LAQ_CUDA(cudaMemcpyAsync(col.d, h_cols[c], rows * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+          LAQ_CUDA(cudaMemcpyAsync(col.d, h_cols[c], rows * sizeof(int32_t), cudaMemcpyDefault, ctx->stream));
           minmax_i32(ctx, col.d, rows, &col.mn, &col.mx);
         }
         if (col.kind == LAQ_COL_KEY && col.mn < 0)

@@ -142,6 +142,19 @@ class DeviceStar:
         self._keep.pop()  # host columns were copied to the device
         self.rows[name] = rows
 
+    def add_table_device64(self, name, cols: dict, kinds: dict, is_fact=False):
+        """int64 (key/int) / float64 CUDA tensors as the device CSV loader
+        produces them; integer columns are narrowed to int32 on the device
+        (range-checked), float columns are not kept (no float device path)."""
+        names = list(cols)
+        rows = cols[names[0]].numel() if names else 0
+        cn = (C.c_char_p * len(names))(*[c.encode() for c in names])
+        kd = (C.c_int32 * len(names))(*[kinds[c] for c in names])
+        ptrs = (C.c_void_p * len(names))(*[cols[c].data_ptr() for c in names])
+        self.ctx.check(self.ctx.lib.laq_star_add_table(self.star_h, name.encode(), 1 if is_fact else 0, rows,
+                                                       len(names), cn, kd, 8, ptrs))
+        self.rows[name] = rows
+
     def add_table_device(self, name, cols: dict, kinds: dict, is_fact=False):
         """int32 CUDA tensors, used in place (caller keeps them alive)."""
         names = list(cols)

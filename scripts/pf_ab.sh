@@ -1,5 +1,5 @@
 cd $GRAFT_REPO_ROOT
-for pf in 0 2 3 4 6; do LAQ_PREFETCH=$pf python - <<'PY'
+for pf in 0 1 2 3; do LAQ_PREFETCH=$pf python - <<'PY'
 import os,sys
 sys.argv=['x']
 exec(open('scripts/scan_ab.py').read().split('res = {}')[0])
