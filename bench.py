@@ -229,11 +229,20 @@ def main():
         return
 
     import torch
+    # LAQ_BENCH_SHARE_GPU=1 (test hook): every rank on cuda:0 over gloo, so the
+    # torchrun path can be exercised on a one-GPU box; the real run is one rank
+    # per GPU over NCCL.
+    share = os.environ.get("LAQ_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
 
     from paper_2306_08367_b200 import gen, star
     from paper_2306_08367_b200.device import context
