@@ -260,13 +260,23 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant_
 #pragma unroll
         for (int c = 0; c < LQ; ++c) y2[u][c] = make_float2(0.f, 0.f);
       const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * q) << 16) + ab * N;
+      bool released = false;
       // this warp's chunks: c0 = 32*hh, 32*hh + 64, ... (two per TMEM wait)
       for (int c0 = 32 * hh; c0 < (a.diag >= 3 ? (a.diag == 3 ? 0 : N) : N); c0 += 128) {
         uint32_t v[64];
         const bool two = c0 + 64 < N;
         tc::tmem_ld32(t0 + c0, *reinterpret_cast<uint32_t(*)[32]>(v));
         if (two) tc::tmem_ld32(t0 + c0 + 64, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
-        tc::tmem_ld_wait();
+        tc::tmem_ld_wait_regs(*reinterpret_cast<uint32_t(*)[32]>(v));
+        if (two) tc::reg_fence(*reinterpret_cast<uint32_t(*)[32]>(v + 32));
+        if (c0 + 128 >= N) {
+          // last TMEM read of this warp for the tile: release the accumulator
+          // before the arithmetic, so the MMA warp can start the tile after next
+          tc::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&acc_empty[ab]);
+          released = true;
+        }
         if (a.diag == 4) {
           y2[0][0].x += __uint_as_float(v[0] ^ v[17] ^ v[33] ^ v[63]);
           continue;
@@ -299,9 +309,11 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant_
           }
         }
       }
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&acc_empty[ab]);
+      if (!released) {
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&acc_empty[ab]);
+      }
       float yy[LP];
       if constexpr (LP == 1) {
         yy[0] = (y2[0][0].x + y2[0][0].y) + (y2[1][0].x + y2[1][0].y);
