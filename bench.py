@@ -338,28 +338,44 @@ def main():
         peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
 
     # ---- e2e: host columns (pinned) -> device each step, same six queries ----
-    # The fact table travels in the compact transfer format (star.pack_columns:
-    # uint8 / uint16 offsets from the column minimum where the range allows,
-    # prepared once on the host like the int32 narrowing) and is scanned in place.
+    # The fact table travels in the bit-packed transfer format (star.bitpack_columns:
+    # value - min in the fewest bits its range needs, a little-endian bitstream per
+    # column, prepared once on the host like the int32 narrowing: 71 bits per row
+    # for the six scanned columns at SF=10) and is scanned in place by the direct
+    # kernel (laq_star_add_table_device_bitpacked).  LAQ_E2E_FORMAT=bytes keeps the
+    # byte-packed format (uint8/uint16/int32 per column) for A/B.
     used_cols = sorted({c for p in plans for c in _fact_cols(p.q)})
-    packed = star.pack_columns(g.fact)
-    host_cols = {c: torch.from_numpy(packed[c][0]).pin_memory() for c in used_cols}
-    dev_cols = {c: (torch.from_numpy(b).cuda(), w, off) for c, (b, w, off) in packed.items()}
+    fmt = os.environ.get("LAQ_E2E_FORMAT", "bits")
     ds2 = star.DeviceStar(ctx)
-    ds2.add_table_device_packed("lineorder", dev_cols, g.kinds["lineorder"], is_fact=True)
+    if fmt == "bits":
+        packed = star.bitpack_columns(g.fact)
+        host_cols = {c: torch.from_numpy(packed[c][0].view(np.int32)).pin_memory() for c in used_cols}
+        dev_cols = {c: (torch.from_numpy(w.view(np.int32)).cuda(), b, off) for c, (w, b, off) in packed.items()}
+        ds2.add_table_device_bitpacked("lineorder", dev_cols, g.kinds["lineorder"], n_rows, is_fact=True)
+        # bytes of the bitstream per row range [r0, r1) (r0, r1 multiples of 32, or r1 = n)
+        span = {c: (lambda r0, r1, b=packed[c][1]: ((r0 // 32) * b, -(-r1 // 32) * b)) for c in used_cols}
+        h2d = sum(-(-n_rows * packed[c][1] // 32) * 4 for c in used_cols)
+        align = 128
+    else:
+        packed = star.pack_columns(g.fact)
+        host_cols = {c: torch.from_numpy(packed[c][0]).pin_memory() for c in used_cols}
+        dev_cols = {c: (torch.from_numpy(b).cuda(), w, off) for c, (b, w, off) in packed.items()}
+        ds2.add_table_device_packed("lineorder", dev_cols, g.kinds["lineorder"], is_fact=True)
+        span = {c: (lambda r0, r1, w=packed[c][1]: (r0 * w, r1 * w)) for c in used_cols}
+        h2d = sum(host_cols[c].numel() - 16 for c in used_cols)
+        align = 16
     for t, cols in g.tables.items():
         if t != "lineorder":
             ds2.add_table(t, cols, g.kinds[t])
     for l in g.links():
         ds2.add_link(*l)
     plans2 = [ds2.prepare(q) for q in queries]
-    h2d = sum(host_cols[c].numel() - 16 for c in used_cols)
     d2h = int(offs[-1]) * 8
 
-    # Row chunks (multiples of 16 rows): the H2D of chunk k+1 on a copy stream
+    # Row chunks (multiples of `align` rows): the H2D of chunk k+1 on a copy stream
     # overlaps the six scans of chunk k (laq_plan_scan_range) on the compute stream.
     n_chunks = 8
-    bounds = [min(n_rows, (n_rows * k // n_chunks) // 16 * 16) for k in range(n_chunks)] + [n_rows]
+    bounds = [min(n_rows, (n_rows * k // n_chunks) // align * align) for k in range(n_chunks)] + [n_rows]
     copy_stream = torch.cuda.Stream()
     chunk_ev = [torch.cuda.Event() for _ in range(n_chunks)]
 
@@ -371,8 +387,8 @@ def main():
             for k in range(n_chunks):
                 r0, r1 = bounds[k], bounds[k + 1]
                 for c in used_cols:
-                    w = dev_cols[c][1]
-                    dev_cols[c][0][r0 * w: r1 * w].copy_(host_cols[c][r0 * w: r1 * w], non_blocking=True)
+                    a0, a1 = span[c](r0, r1)
+                    dev_cols[c][0][a0:a1].copy_(host_cols[c][a0:a1], non_blocking=True)
                 chunk_ev[k].record(copy_stream)
         for p in plans2:
             p.build_codes()  # dimension code tables: independent of the fact upload
@@ -437,9 +453,12 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": total_rows / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                    "format": fmt,
                     "path": "laq_plan_build_codes + laq_plan_scan_range via C-ABI; fact columns H2D from pinned "
-                            "host memory each step in the compact transfer format (uint8/uint16 offsets where the "
-                            "value range allows), 8 row chunks, upload of chunk k+1 overlapping the scans of chunk k"},
+                            "host memory each step in the " + ("bit-packed transfer format (value - min in the "
+                            "fewest bits its range needs, prepared once on the host)" if fmt == "bits" else
+                            "byte-packed transfer format (uint8/uint16 offsets where the value range allows)") +
+                            ", 8 row chunks, upload of chunk k+1 overlapping the scans of chunk k"},
             "gpu_launches": launches,
             "clocks": clk,
             "secondary": secondary,

@@ -324,6 +324,17 @@ int laq_star_add_table_device(laq_star* star, const char* name, int32_t is_fact,
 int laq_star_add_table_device_packed(laq_star* star, const char* name, int32_t is_fact, int64_t rows,
                                      int32_t n_cols, const char* const* col_names, const int32_t* col_kinds,
                                      const void* const* d_cols, const int32_t* widths, const int32_t* offsets);
+/* Register a table whose integer columns are caller-owned device bitstreams
+ * (the bit-packed transfer format): column c stores bits[c] (1..32) bits per
+ * row, value = stored + offsets[c]; rows are little-endian bit fields packed
+ * back to back, so a group of 32 rows is bits[c] consecutive 32-bit words.
+ * Each buffer is 4-byte aligned and holds ceil(rows/128)*4*bits[c] words plus
+ * 16 bytes.  Only the direct scan reads these, with every scanned column
+ * bit-packed (LAQ_ERR_UNSUPPORTED otherwise); scan ranges start at multiples
+ * of 32 rows. */
+int laq_star_add_table_device_bitpacked(laq_star* star, const char* name, int32_t is_fact, int64_t rows,
+                                        int32_t n_cols, const char* const* col_names, const int32_t* col_kinds,
+                                        const void* const* d_cols, const int32_t* bits, const int32_t* offsets);
 int laq_star_add_link(laq_star* star, const char* fact_fk, const char* dim_name,
                       const char* dim_pk);
 

@@ -85,6 +85,7 @@ _SIGS = {
     "laq_star_create": (C.c_int, [vp, C.POINTER(vp)]),
     "laq_star_destroy": (C.c_int, [vp]),
     "laq_star_add_table": (C.c_int, [vp, C.c_char_p, i32, i64, i32, vp, i32p, i32, vp]),
+    "laq_star_add_table_device_bitpacked": (C.c_int, [vp, C.c_char_p, i32, i64, i32, vp, i32p, vp, i32p, i32p]),
     "laq_csv_open": (C.c_int, [vp, vp, i64, C.POINTER(vp), i64p]),
     "laq_csv_parse": (C.c_int, [vp, vp, i32, i32p, vp]),
     "laq_csv_close": (C.c_int, [vp]),

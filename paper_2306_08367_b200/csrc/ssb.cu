@@ -56,11 +56,12 @@ struct DevCol {
   bool padded = false;   // allocation has >= 16 readable bytes past the end
   // byte-packed copy (fact columns with a narrow range): value = stored + poff
   void* pk = nullptr;
-  int pw = 4;
+  int pw = 4;        // 0: bit-packed (pbits per row)
   int32_t poff = 0;
+  int pbits = 0;
 
   scan::Col view() const {  // what the stream kernel reads
-    return pk ? scan::Col{pk, pw, poff} : scan::Col{d, 4, 0};
+    return pk ? scan::Col{pk, pw, poff, pbits} : scan::Col{d, 4, 0, 0};
   }
 };
 
@@ -124,9 +125,35 @@ __global__ void packed_minmax_kernel(const T* __restrict__ p, int64_t n, unsigne
 }
 
 __device__ __forceinline__ int32_t col_value(const scan::Col& c, int64_t i) {
+  if (c.w == 0) {  // bit-packed: row i at bit (i & 31) * bits of group i >> 5
+    const uint32_t* g = static_cast<const uint32_t*>(c.p) + (i >> 5) * c.bits;
+    const int bit = static_cast<int>(i & 31) * c.bits;
+    const uint32_t lo = g[bit >> 5];
+    const uint32_t hi = (bit & 31) + c.bits > 32 ? g[(bit >> 5) + 1] : 0u;
+    const uint32_t v = __funnelshift_r(lo, hi, bit & 31);
+    return static_cast<int32_t>(v & (c.bits >= 32 ? 0xffffffffu : ((1u << c.bits) - 1u))) + c.off;
+  }
   if (c.w == 1) return static_cast<int32_t>(static_cast<const uint8_t*>(c.p)[i]) + c.off;
   if (c.w == 2) return static_cast<int32_t>(static_cast<const uint16_t*>(c.p)[i]) + c.off;
   return static_cast<const int32_t*>(c.p)[i];
+}
+
+// min/max of any column view (value = decoded + offset), as int64 keys ^ sign bit.
+__global__ void view_minmax_kernel(const scan::Col c, int64_t n, unsigned long long* mnmx) {
+  long long mn = LLONG_MAX, mx = LLONG_MIN;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const long long v = col_value(c, i);
+    mn = v < mn ? v : mn;
+    mx = v > mx ? v : mx;
+  }
+  for (int o = 16; o; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(mnmx, static_cast<unsigned long long>(mn) ^ 0x8000000000000000ull);
+    atomicMax(mnmx + 1, static_cast<unsigned long long>(mx) ^ 0x8000000000000000ull);
+  }
 }
 
 template <class T>
@@ -766,6 +793,47 @@ int laq_star_add_table_device_packed(laq_star* s, const char* name, int32_t is_f
   });
 }
 
+int laq_star_add_table_device_bitpacked(laq_star* s, const char* name, int32_t is_fact, int64_t rows, int32_t n_cols,
+                                        const char* const* col_names, const int32_t* col_kinds,
+                                        const void* const* d_cols, const int32_t* bits, const int32_t* offsets) {
+  laq_ctx* ctx = s->ctx;
+  return guard(ctx, [&] {
+    DevTable& t = new_table(s, name, is_fact, rows);
+    unsigned long long* mnmx = reinterpret_cast<unsigned long long*>(ctx->d_flags + 32);
+    for (int c = 0; c < n_cols; ++c) {
+      DevCol col;
+      col.name = col_names[c];
+      col.kind = col_kinds[c];
+      for (const auto& o : t.cols)
+        if (o.name == col.name) fail(LAQ_ERR_NAME, "duplicate column name: " + col.name);
+      if (col.kind == LAQ_COL_FLOAT) {
+        t.cols.push_back(col);
+        continue;
+      }
+      if (bits[c] < 1 || bits[c] > 32) fail(LAQ_ERR_SHAPE, "bit-packed column width must be 1..32 bits");
+      if ((reinterpret_cast<uintptr_t>(d_cols[c]) & 3) != 0) fail(LAQ_ERR_SHAPE, "bit-packed column must be 4-byte aligned");
+      col.padded = true;  // caller contract: whole 128-row blocks of words + 16 bytes
+      col.pk = const_cast<void*>(d_cols[c]);
+      col.pw = 0;
+      col.pbits = bits[c];
+      col.poff = offsets[c];
+      if (rows > 0) {
+        const unsigned long long init[2] = {~0ull, 0ull};
+        LAQ_CUDA(cudaMemcpyAsync(mnmx, init, sizeof init, cudaMemcpyHostToDevice, ctx->stream));
+        view_minmax_kernel<<<grid_for(rows, 256 * 8, ctx->sm_count * 8), 256, 0, ctx->stream>>>(col.view(), rows, mnmx);
+        launched(ctx);
+        LAQ_CUDA(cudaMemcpyAsync(ctx->h_pinned, mnmx, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        sync(ctx);
+        col.mn = static_cast<int64_t>(static_cast<unsigned long long>(ctx->h_pinned[0]) ^ 0x8000000000000000ull);
+        col.mx = static_cast<int64_t>(static_cast<unsigned long long>(ctx->h_pinned[1]) ^ 0x8000000000000000ull);
+      }
+      if (col.kind == LAQ_COL_KEY && rows > 0 && col.mn < 0)
+        fail(LAQ_ERR_FORMAT, "table: negative key in column '" + col.name + "'");
+      t.cols.push_back(col);
+    }
+  });
+}
+
 int laq_star_add_link(laq_star* s, const char* fact_fk, const char* dim_name, const char* dim_pk) {
   laq_ctx* ctx = s->ctx;
   return guard(ctx, [&] {
@@ -970,6 +1038,23 @@ int laq_query_prepare(laq_ctx* ctx, const laq_star* cs, const laq_query_desc* q,
     lay_out_scan(ctx, plan.get(), fks, fkcols, probes, mmin, mmax, padded);
     if (packed_only && plan->variant != 2 && plan->variant != 4)
       fail(LAQ_ERR_UNSUPPORTED, "byte-packed fact columns need the stream scan (no fact InSet filter, G <= 4096)");
+    {  // bit-packed columns (transfer format): only the direct kernel, and all-or-none
+      int nbit = 0, ncol = 0;
+      auto tally = [&](const scan::Col& c) { ++ncol; nbit += c.w == 0 ? 1 : 0; };
+      if (a.measure) tally(a.mc);
+      for (int j = 0; j < plan->nl; ++j) tally(a.fkc[j]);
+      for (int f = 0; f < plan->nf; ++f) tally(a.ffc[f]);
+      if (nbit > 0 && (nbit != ncol || plan->variant != 4 || a.n_fgroups > 0))
+        fail(LAQ_ERR_UNSUPPORTED, "bit-packed fact columns need the direct scan with every scanned column bit-packed");
+      if (nbit > 0) plan->variant = 6;
+    }
+    if (plan->variant == 6) {
+      int64_t b = 0;  // bytes per row, rounded up per column
+      if (a.measure) b += (a.mc.bits + 7) / 8;
+      for (int j = 0; j < plan->nl; ++j) b += (a.fkc[j].bits + 7) / 8;
+      for (int f = 0; f < plan->nf; ++f) b += (a.ffc[f].bits + 7) / 8;
+      plan->bytes_per_row = b;
+    }
     if (plan->variant == 2 || plan->variant == 4) {  // the stream kernels read the packed views
       bool any_packed = a.measure && a.mc.w != 4;
       for (int j = 0; j < plan->nl; ++j) any_packed = any_packed || a.fkc[j].w != 4;
@@ -1011,7 +1096,13 @@ int laq_plan_scan_range(laq_ctx* ctx, laq_plan* p, int64_t row0, int64_t rows, i
     ScanArgs a = p->scan;
     a.n = rows;
     auto shift = [&](scan::Col& c) {
-      if (c.p) c.p = static_cast<const uint8_t*>(c.p) + row0 * c.w;
+      if (!c.p) return;
+      if (c.w == 0) {  // bit-packed: whole 32-row groups of `bits` words
+        if (row0 % 32) fail(LAQ_ERR_SHAPE, "scan range over bit-packed columns must start at a multiple of 32 rows");
+        c.p = static_cast<const uint32_t*>(c.p) + (row0 / 32) * c.bits;
+      } else {
+        c.p = static_cast<const uint8_t*>(c.p) + row0 * c.w;
+      }
     };
     for (int j = 0; j < p->nl; ++j) {
       if (a.fk[j]) a.fk[j] += row0;

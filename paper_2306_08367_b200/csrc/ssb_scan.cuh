@@ -77,8 +77,9 @@ struct FactGroup {
 // bytes per row) relative to the column minimum `off` when the value range fits.
 struct Col {
   const void* p;
-  int w;        // bytes per row: 1, 2 or 4
-  int32_t off;  // value = stored + off (w < 4)
+  int w;         // bytes per row: 1, 2 or 4; 0 = bit-packed
+  int32_t off;   // value = stored + off (w < 4)
+  int bits = 0;  // w == 0: bits per row (1..32) of a little-endian bitstream
 };
 
 struct ScanArgs {
@@ -737,13 +738,70 @@ __device__ __forceinline__ void reds_add(uint32_t addr, uint32_t v) {
 }
 
 // One 128-byte line per 8 lanes (8 lanes x 4 rows x 4 B) of a column.
-template <bool PK>
+template <int PKM>
 __device__ __forceinline__ void prefetch_l2(const Col& c, int64_t row0) {
-  const uint8_t* p = static_cast<const uint8_t*>(c.p) + (PK ? row0 * c.w : row0 * 4);
+  if constexpr (PKM == 2) return;  // bit-packed (transfer format): no prefetch
+  const uint8_t* p = static_cast<const uint8_t*>(c.p) + (PKM == 1 ? row0 * c.w : row0 * 4);
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
-template <int NL, int NF, int MODE, bool PK, bool TAIL>
+// Direct-kernel column access by packing mode PKM: 0 int32, 1 byte-packed
+// (widths 1/2/4), 2 bit-packed.  Modes 0/1: a lane owns 4 consecutive rows
+// row0..row0+3.  Mode 2: the warp's 128 rows are 4 groups of 32 and a lane owns
+// row (group r, lane) -- the raw registers hold the lane's word of each group
+// (a group of 32 rows x b bits is b consecutive 32-bit words), unpacked with
+// two shuffles and a funnel shift.  Row order inside a step is irrelevant to
+// the aggregation, so the mapping only has to be consistent across columns.
+template <int PKM>
+__device__ __forceinline__ int64_t drow(int64_t row0, int r) {
+  if constexpr (PKM == 2) {
+    const int lane = threadIdx.x & 31;
+    return row0 - 3 * lane + 32 * r;  // warp base (row0 - 4 lane) + 32 r + lane
+  } else {
+    return row0 + r;
+  }
+}
+template <int PKM>
+__device__ __forceinline__ int4 dld(const Col& c, int64_t row0, int64_t n) {
+  if constexpr (PKM == 0) {
+    return ld4_padded(static_cast<const int32_t*>(c.p), row0, n);
+  } else if constexpr (PKM == 1) {
+    return ld4_raw(c, row0, n);
+  } else {
+    const int lane = threadIdx.x & 31;
+    const int64_t wbase = row0 - 4 * lane;
+    if (wbase >= n || lane >= c.bits) return make_int4(0, 0, 0, 0);
+    const uint32_t* w = static_cast<const uint32_t*>(c.p) + (wbase >> 5) * c.bits + lane;
+    const int b = c.bits;
+    return make_int4(static_cast<int32_t>(__ldcs(w)), static_cast<int32_t>(__ldcs(w + b)),
+                     static_cast<int32_t>(__ldcs(w + 2 * b)), static_cast<int32_t>(__ldcs(w + 3 * b)));
+  }
+}
+__device__ __forceinline__ int32_t bit_extract(uint32_t word, int bits, int off) {
+  const int lane = threadIdx.x & 31;
+  const int bit = lane * bits;
+  const int wi = bit >> 5, sh = bit & 31;
+  const uint32_t lo = __shfl_sync(0xffffffffu, word, wi);
+  const uint32_t hi = __shfl_sync(0xffffffffu, word, (wi + 1) & 31);
+  const uint32_t v = __funnelshift_r(lo, hi, sh);
+  const uint32_t mask = bits >= 32 ? 0xffffffffu : ((1u << bits) - 1u);
+  return static_cast<int32_t>(v & mask) + off;
+}
+template <int PKM>
+__device__ __forceinline__ int4 dunpack(const int4& r, const Col& c) {
+  if constexpr (PKM == 0) {
+    return r;
+  } else if constexpr (PKM == 1) {
+    return unpack4(r, c);
+  } else {
+    return make_int4(bit_extract(static_cast<uint32_t>(r.x), c.bits, c.off),
+                     bit_extract(static_cast<uint32_t>(r.y), c.bits, c.off),
+                     bit_extract(static_cast<uint32_t>(r.z), c.bits, c.off),
+                     bit_extract(static_cast<uint32_t>(r.w), c.bits, c.off));
+  }
+}
+
+template <int NL, int NF, int MODE, int PKM, bool TAIL>
 __device__ __forceinline__ void direct_rows(const ScanArgs& a, int64_t row0, const int4 (&kv)[NL > 0 ? NL : 1],
                                             const int4 (&fv)[NF > 0 ? NF : 1], const int4& mv,
                                             const uint32_t (&tab_addr)[NL > 0 ? NL : 1], uint32_t bins,
@@ -752,13 +810,13 @@ __device__ __forceinline__ void direct_rows(const ScanArgs& a, int64_t row0, con
   int32_t gid[4];
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
-    alive[r] = TAIL ? row0 + r < a.n : true;
+    alive[r] = TAIL ? drow<PKM>(row0, r) < a.n : true;
     gid[r] = 0;
   }
 #pragma unroll
   for (int f = 0; f < NF; ++f) {
     const int32_t lo = a.ff[f].lo, hi = a.ff[f].hi;
-    const int4 fu = unpack_batch<PK>(fv[f], a.ffc[f]);
+    const int4 fu = dunpack<PKM>(fv[f], a.ffc[f]);
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int32_t v = comp(fu, r);
@@ -768,7 +826,7 @@ __device__ __forceinline__ void direct_rows(const ScanArgs& a, int64_t row0, con
 #pragma unroll
   for (int j = 0; j < NL; ++j) {
     const uint32_t base = static_cast<uint32_t>(a.link[j].base), size = static_cast<uint32_t>(a.link[j].size);
-    const int4 k = unpack_batch<PK>(kv[j], a.fkc[j]);
+    const int4 k = dunpack<PKM>(kv[j], a.fkc[j]);
     const int fmt = a.link[j].fmt;
     int32_t c[4];
     uint32_t s[4];
@@ -806,7 +864,7 @@ __device__ __forceinline__ void direct_rows(const ScanArgs& a, int64_t row0, con
       gid[r] += c[r];
     }
   }
-  const int4 mu = unpack_batch<PK>(mv, a.mc);
+  const int4 mu = dunpack<PKM>(mv, a.mc);
   if constexpr (MODE == 0) {
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
@@ -828,7 +886,7 @@ __device__ __forceinline__ void direct_rows(const ScanArgs& a, int64_t row0, con
 
 // MODE 0 (one group: register accumulation) or MODE 1 with narrow (u32) bins.
 // Shared memory: [staged code tables (a.smem_tab_elems bytes)] [u32 bins 2G].
-template <int NL, int NF, int MODE, bool PK>
+template <int NL, int NF, int MODE, int PKM>
 __global__ void __launch_bounds__(kDirectThreads, 1) scan_direct_kernel(const ScanArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* b32 = reinterpret_cast<uint32_t*>(smem + a.smem_tab_elems);
@@ -856,7 +914,7 @@ __global__ void __launch_bounds__(kDirectThreads, 1) scan_direct_kernel(const Sc
   const int64_t iters = (a.n + step - 1) / step;  // uniform across the block
   const int64_t full = a.n / step;                // steps with every row in range
   int64_t row0 = (static_cast<int64_t>(blockIdx.x) * kDirectThreads + tid) * 4;
-  const bool pf_lane = a.prefetch && (tid & 7) == 0;
+  const bool pf_lane = PKM != 2 && a.prefetch && (tid & 7) == 0;
   const int64_t pf_rows = static_cast<int64_t>(a.prefetch) * step;
 
   // Two register buffers used in turn (the loop is unrolled by two so the
@@ -865,10 +923,10 @@ __global__ void __launch_bounds__(kDirectThreads, 1) scan_direct_kernel(const Sc
   int4 kvB[NL > 0 ? NL : 1], fvB[NF > 0 ? NF : 1], mvB = make_int4(0, 0, 0, 0);
   auto load = [&](int4 (&kv)[NL > 0 ? NL : 1], int4 (&fv)[NF > 0 ? NF : 1], int4& mv, int64_t r) {
 #pragma unroll
-    for (int j = 0; j < NL; ++j) kv[j] = ld_batch<NL, NF, MODE, PK>(a.fkc[j], r, a.n);
+    for (int j = 0; j < NL; ++j) kv[j] = dld<PKM>(a.fkc[j], r, a.n);
 #pragma unroll
-    for (int f = 0; f < NF; ++f) fv[f] = ld_batch<NL, NF, MODE, PK>(a.ffc[f], r, a.n);
-    if (a.measure) mv = ld_batch<NL, NF, MODE, PK>(a.mc, r, a.n);
+    for (int f = 0; f < NF; ++f) fv[f] = dld<PKM>(a.ffc[f], r, a.n);
+    if (a.measure) mv = dld<PKM>(a.mc, r, a.n);
   };
   load(kvA, fvA, mvA, row0);
 
@@ -880,13 +938,13 @@ __global__ void __launch_bounds__(kDirectThreads, 1) scan_direct_kernel(const Sc
     load(nkv, nfv, nmv, row0 + step);
     if (pf_lane && row0 + pf_rows < a.n) {  // the rows `prefetch` steps ahead into L2 (no registers held)
 #pragma unroll
-      for (int j = 0; j < NL; ++j) prefetch_l2<PK>(a.fkc[j], row0 + pf_rows);
+      for (int j = 0; j < NL; ++j) prefetch_l2<PKM>(a.fkc[j], row0 + pf_rows);
 #pragma unroll
-      for (int f = 0; f < NF; ++f) prefetch_l2<PK>(a.ffc[f], row0 + pf_rows);
-      if (a.measure) prefetch_l2<PK>(a.mc, row0 + pf_rows);
+      for (int f = 0; f < NF; ++f) prefetch_l2<PKM>(a.ffc[f], row0 + pf_rows);
+      if (a.measure) prefetch_l2<PKM>(a.mc, row0 + pf_rows);
     }
-    if (it < full) direct_rows<NL, NF, MODE, PK, false>(a, row0, kv, fv, mv, tab_addr, bins, r_cnt, r_sum);
-    else direct_rows<NL, NF, MODE, PK, true>(a, row0, kv, fv, mv, tab_addr, bins, r_cnt, r_sum);
+    if (it < full) direct_rows<NL, NF, MODE, PKM, false>(a, row0, kv, fv, mv, tab_addr, bins, r_cnt, r_sum);
+    else direct_rows<NL, NF, MODE, PKM, true>(a, row0, kv, fv, mv, tab_addr, bins, r_cnt, r_sum);
     if constexpr (MODE == 1) {
       if (--until_flush == 0) {
         until_flush = a.flush_every;

@@ -7,8 +7,8 @@ namespace laq {
 namespace scan {
 
 // variant: 0 = ldg fallback, 1 = TMA pipe, 2 = resident-table stream (int32),
-// 3 = the stream kernel over byte-packed columns, 4/5 = the direct-probe
-// kernel over int32 / byte-packed columns.
+// 3 = the stream kernel over byte-packed columns, 4/5/6 = the direct-probe
+// kernel over int32 / byte-packed / bit-packed columns.
 template <int NL, int NF, int MODE>
 void launch_variant(laq_ctx* ctx, const ScanArgs& a, int variant, bool vec, int grid, size_t smem) {
   cudaStream_t s = ctx->stream;
@@ -16,11 +16,13 @@ void launch_variant(laq_ctx* ctx, const ScanArgs& a, int variant, bool vec, int 
   if (variant == 1) {
     LAQ_CUDA(cudaFuncSetAttribute(scan_pipe_kernel<NL, NF, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     scan_pipe_kernel<NL, NF, MODE><<<grid, kPipeThreads, smem, s>>>(a);
-  } else if (variant == 4 || variant == 5) {
+  } else if (variant >= 4 && variant <= 6) {
     if constexpr (MODE == 2) {
       fail(LAQ_ERR_UNSUPPORTED, "direct scan: global-atomic group mode");
     } else {
-      auto kern = variant == 5 ? scan_direct_kernel<NL, NF, MODE, true> : scan_direct_kernel<NL, NF, MODE, false>;
+      auto kern = variant == 6   ? scan_direct_kernel<NL, NF, MODE, 2>
+                  : variant == 5 ? scan_direct_kernel<NL, NF, MODE, 1>
+                                 : scan_direct_kernel<NL, NF, MODE, 0>;
       LAQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       const int64_t blocks_needed = (a.n + kDirectThreads * 4 - 1) / (kDirectThreads * 4);
       const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(grid, blocks_needed)));

@@ -73,3 +73,19 @@ def test_tree_validation_errors():
     m = tree.compile_tree(t, 6)
     with pytest.raises(errors.MappingError):
         tree.partition_tree(m, np.zeros(5, np.int64), 1)  # ownership list must cover every feature
+
+
+def test_bitpack_roundtrip():
+    """The bit-packed transfer format: exact round trip, word count contract."""
+    import numpy as np
+    from paper_2306_08367_b200 import star
+    rng = np.random.default_rng(3)
+    for bits in (1, 4, 6, 12, 15, 20, 31, 32):
+        for n in (0, 1, 31, 32, 127, 128, 129, 10_007):
+            v = rng.integers(0, 2 ** bits, n, dtype=np.int64)
+            w = star.bitpack_words(v, bits)
+            assert w.dtype == np.uint32 and w.size == -(-n // 128) * 4 * bits + 4
+            assert np.array_equal(star.bitunpack_words(w, n, bits), v)
+    cols = {"a": np.array([5, 7, 6], np.int32), "b": np.array([100, 9999, 4000], np.int32)}
+    p = star.bitpack_columns(cols)
+    assert p["a"][1:] == (2, 5) and p["b"][1:] == (14, 100)
