@@ -497,18 +497,35 @@ void lay_out_scan(laq_ctx* ctx, laq_plan* p, const std::vector<const int32_t*>& 
     std::vector<int> by(nl);
     std::iota(by.begin(), by.end(), 0);
     std::stable_sort(by.begin(), by.end(), [&](int x, int y) { return need[x] < need[y]; });
+    std::vector<char> staged(nl, 0);
+    for (int j : by) {
+      if (std::getenv("LAQ_NOSMEMTAB") || fmt[j] == scan::kFmtGlobal || need[j] > room) continue;
+      staged[j] = 1;
+      room -= need[j];
+    }
+    // Second pass: a staged pass bitmap becomes a uint8 table (one LDS.U8 per
+    // probe instead of shift/LDS/shift/and) when the remaining room allows;
+    // upgrades never evict another link's table.
+    for (int j : by) {
+      if (!staged[j] || fmt[j] != scan::kFmtBit) continue;
+      const int64_t u8 = (probes[j]->size + 15) & ~int64_t{15};
+      if (u8 - need[j] <= room) {
+        room -= u8 - need[j];
+        fmt[j] = scan::kFmtU8;
+        need[j] = u8;
+      }
+    }
     int64_t off = 0;
     std::vector<int64_t> smem_off(nl, -1);
     for (int j : by) {
       auto& lc = p->links[j];
       lc.fmt = scan::kFmtGlobal;
-      if (std::getenv("LAQ_NOSMEMTAB") || need[j] > room) continue;
+      if (!staged[j]) continue;
       lc.fmt = fmt[j];
       lc.packed_bytes = need[j];
       lc.packed = DevMem<uint8_t>(need[j]);
       smem_off[j] = off;  // bytes
       off += need[j];
-      room -= need[j];
     }
     build_codes(ctx, p);  // fills the compact copies
     std::vector<double> rank(nl);
