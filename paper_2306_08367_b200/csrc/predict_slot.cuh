@@ -247,6 +247,48 @@ __global__ void __launch_bounds__(BT, 1) direct_chunks_kernel(const Args a, int6
   }
 }
 
+// Exclusive scan of the per-chunk survivor counts (one 1024-thread CTA: each
+// thread scans a contiguous run, then a block scan of the run totals).  After
+// an optimistic pass without misses it exits at once (the common case), so the
+// call costs one near-empty launch instead of a library scan.
+constexpr int kScanThreads = 1024;
+// miss (optimistic calls): the direct pass's miss counter is moved into
+// `decision` (read by the write pass) and cleared for the next call, so no
+// memset launch is needed and any sequence of graph replays stays exact.
+__global__ void __launch_bounds__(kScanThreads) scan_chunks_kernel(const int* __restrict__ counts, int64_t n,
+                                                                   int64_t* __restrict__ offsets,
+                                                                   unsigned long long* miss,
+                                                                   unsigned long long* decision) {
+  if (miss) {
+    const unsigned long long m = *miss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      *decision = m;
+      *miss = 0;
+    }
+    if (m == 0) return;
+  }
+  __shared__ int64_t s_tot[kScanThreads];
+  const int t = threadIdx.x;
+  const int64_t per = (n + kScanThreads - 1) / kScanThreads;
+  const int64_t b = t * per, e = min(n, b + per);
+  int64_t sum = 0;
+  for (int64_t i = b; i < e; ++i) sum += counts[i];
+  s_tot[t] = sum;
+  __syncthreads();
+  for (int o = 1; o < kScanThreads; o <<= 1) {  // Hillis-Steele inclusive scan of the run totals
+    const int64_t v = t >= o ? s_tot[t - o] : 0;
+    __syncthreads();
+    s_tot[t] += v;
+    __syncthreads();
+  }
+  int64_t run = t ? s_tot[t - 1] : 0;
+  for (int64_t i = b; i < e; ++i) {
+    offsets[i] = run;
+    run += counts[i];
+  }
+}
+
 template <int NL>
 __global__ void __launch_bounds__(kWarpThreads) write_chunks_kernel(const Args a, int64_t n_chunks,
                                                                     const int64_t* offsets,

@@ -429,7 +429,10 @@ struct laq_probe {
   DevMem<char> scan_tmp;
   size_t scan_tmp_bytes = 0;
   int64_t chunk_cap = 0;
-  DevMem<unsigned long long> miss{1};  // optimistic single pass: chunks with a missing key
+  // optimistic single pass: [0] chunks with a missing key (counted by the
+  // direct pass, moved to [1] and cleared by the scan pass), [1] the decision
+  // the write pass reads
+  DevMem<unsigned long long> miss{2};
 };
 
 namespace laq {
@@ -513,11 +516,6 @@ void run_slot_predict(laq_ctx* ctx, laq_probe* p, const int32_t* const* d_fks, i
   if (p->chunk_cap < n_chunks) {
     p->chunk_counts = DevMem<int>(n_chunks);
     p->chunk_offsets = DevMem<int64_t>(n_chunks);
-    size_t bytes = 0;
-    LAQ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, p->chunk_counts.get(), p->chunk_offsets.get(), n_chunks,
-                                           ctx->stream));
-    p->scan_tmp = DevMem<char>(std::max<size_t>(bytes, 1));
-    p->scan_tmp_bytes = bytes;
     p->chunk_cap = n_chunks;
   }
   const size_t smem = static_cast<size_t>(words_total) * 4;
@@ -525,7 +523,8 @@ void run_slot_predict(laq_ctx* ctx, laq_probe* p, const int32_t* const* d_fks, i
   // l == 1 and no LAQ_PREDICT_TWO_PASS: optimistic single pass + device-decided
   // compaction fallback (direct_chunks_kernel); otherwise count + scan + write.
   const bool optimistic = l == 1 && !std::getenv("LAQ_PREDICT_TWO_PASS");
-  if (optimistic) LAQ_CUDA(cudaMemsetAsync(p->miss.get(), 0, sizeof(unsigned long long), ctx->stream));
+  unsigned long long* miss = p->miss.get();
+  unsigned long long* decision = p->miss.get() + 1;
   auto launch = [&](auto count_k, auto direct_k, auto direct_small_k, auto write_k) {
     LAQ_CUDA(cudaFuncSetAttribute(write_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_w)));
     const int64_t want = (n_chunks + slot::kWarpThreads / 32 - 1) / (slot::kWarpThreads / 32);
@@ -537,12 +536,12 @@ void run_slot_predict(laq_ctx* ctx, laq_probe* p, const int32_t* const* d_fks, i
     if (optimistic && big) {
       LAQ_CUDA(cudaFuncSetAttribute(direct_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_w)));
       const unsigned g0 = static_cast<unsigned>(ctx->sm_count);
-      direct_k<<<g0, slot::kDirectBT, smem_w, ctx->stream>>>(a, n_chunks, p->chunk_counts.get(), p->miss.get());
+      direct_k<<<g0, slot::kDirectBT, smem_w, ctx->stream>>>(a, n_chunks, p->chunk_counts.get(), miss);
     } else if (optimistic) {
       LAQ_CUDA(cudaFuncSetAttribute(direct_small_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_w)));
       LAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, direct_small_k, slot::kWarpThreads, smem_w));
       const unsigned g0 = static_cast<unsigned>(std::min<int64_t>(want, int64_t{ctx->sm_count} * std::max(per_sm, 1)));
-      direct_small_k<<<g0, slot::kWarpThreads, smem_w, ctx->stream>>>(a, n_chunks, p->chunk_counts.get(), p->miss.get());
+      direct_small_k<<<g0, slot::kWarpThreads, smem_w, ctx->stream>>>(a, n_chunks, p->chunk_counts.get(), miss);
     } else {
       LAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, count_k, slot::kWarpThreads, smem));
       const unsigned g1 = static_cast<unsigned>(std::min<int64_t>(want, int64_t{ctx->sm_count} * std::max(per_sm, 1)));
@@ -550,11 +549,10 @@ void run_slot_predict(laq_ctx* ctx, laq_probe* p, const int32_t* const* d_fks, i
     }
     LAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, write_k, slot::kWarpThreads, smem_w));
     const unsigned g2 = static_cast<unsigned>(std::min<int64_t>(want, int64_t{ctx->sm_count} * std::max(per_sm, 1)));
-    size_t bytes = p->scan_tmp_bytes;
-    LAQ_CUDA(cub::DeviceScan::ExclusiveSum(p->scan_tmp.get(), bytes, p->chunk_counts.get(), p->chunk_offsets.get(),
-                                           n_chunks, ctx->stream));
+    slot::scan_chunks_kernel<<<1, slot::kScanThreads, 0, ctx->stream>>>(
+        p->chunk_counts.get(), n_chunks, p->chunk_offsets.get(), optimistic ? miss : nullptr, decision);
     write_k<<<g2, slot::kWarpThreads, smem_w, ctx->stream>>>(a, n_chunks, p->chunk_offsets.get(),
-                                                             optimistic ? p->miss.get() : nullptr);
+                                                             optimistic ? decision : nullptr);
     ctx->launches += 2;
   };
   switch (p->n_links) {
@@ -612,6 +610,7 @@ int laq_probe_build(laq_ctx* ctx, int32_t n_links, const int32_t* const* d_pks, 
   return guard(ctx, [&] {
     if (n_links < 1 || n_links > kMaxLinks) fail(LAQ_ERR_UNSUPPORTED, "fused star predict supports 1..8 dimensions");
     auto* p = new laq_probe();
+    LAQ_CUDA(cudaMemset(p->miss.get(), 0, 2 * sizeof(unsigned long long)));
     try {
       p->n_links = n_links;
       for (int j = 0; j < n_links; ++j)

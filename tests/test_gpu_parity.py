@@ -226,3 +226,45 @@ def test_predictor_graph_capturable(lib):
     pred.ctx.bind_stream()
     assert np.array_equal(out.cpu().numpy()[:, 0], P[fk, 0] + 0.0)
     assert int(pred.nnz_dev.item()) == 1_000_000
+
+
+def test_predictor_miss_fallback_alternating(lib):
+    """Optimistic single pass with device-decided compaction: calls with and
+    without missing keys in any order (the miss counter is moved and cleared
+    on the device) and graph replays over both kinds stay exact."""
+    import torch
+    _, fusion, _ = lib
+    rng = np.random.default_rng(21)
+    pk = np.arange(5_000) + 7
+    P = rng.random((5_000, 1))
+    pred = fusion.FusedStarPredictor([pk], [P])
+    full = rng.integers(7, 5_007, 700_001)
+    miss = full.copy()
+    miss[rng.random(full.size) < 0.01] = 1  # keys below the domain: dropped (inner join)
+
+    def check(fk, y, nnz):
+        keep = (fk >= 7) & (fk < 5_007)
+        want = P[fk[keep] - 7, 0] + 0.0
+        assert nnz == keep.sum() and np.array_equal(y[:nnz, 0], want)
+
+    for fk in (full, miss, miss, full, miss, full, full):
+        fk_d = torch.from_numpy(fk.astype(np.int32)).cuda()
+        out = torch.empty((fk.size, 1), dtype=torch.float64, device="cuda")
+        pred([fk_d], out=out, sync=False)
+        torch.cuda.synchronize()
+        check(fk, out.cpu().numpy(), int(pred.nnz_dev.item()))
+    # graph with one call, replayed over inputs that change between replays
+    fk_d = torch.from_numpy(full.astype(np.int32)).cuda()
+    out = torch.empty((full.size, 1), dtype=torch.float64, device="cuda")
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        pred.ctx.bind_stream(s)
+        with torch.cuda.graph(g, stream=s):
+            pred([fk_d], out=out, sync=False)
+    for fk in (full, miss, full, miss, miss, full):
+        fk_d.copy_(torch.from_numpy(fk.astype(np.int32)))
+        g.replay()
+        torch.cuda.synchronize()
+        check(fk, out.cpu().numpy(), int(pred.nnz_dev.item()))
+    pred.ctx.bind_stream()
