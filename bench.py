@@ -273,11 +273,12 @@ def main():
 
     def launch(k, i=None):
         b = k & 1
+        accs[b].zero_()                  # every query's accumulator: one memset
+        star.build_codes_batch(plans)    # every query's code tables: one launch
         for qi, p in enumerate(plans):
-            p.build_codes()
             if i is not None:
                 ev[i][qi][0].record(stream)
-            p.scan(accs[b][offs[qi]: offs[qi + 1]])
+            p.scan(accs[b][offs[qi]: offs[qi + 1]], accumulate=True)
             if i is not None:
                 ev[i][qi][1].record(stream)
         if dist is not None:
@@ -390,13 +391,13 @@ def main():
                     a0, a1 = span[c](r0, r1)
                     dev_cols[c][0][a0:a1].copy_(host_cols[c][a0:a1], non_blocking=True)
                 chunk_ev[k].record(copy_stream)
-        for p in plans2:
-            p.build_codes()  # dimension code tables: independent of the fact upload
+        acc.zero_()
+        star.build_codes_batch(plans2)  # dimension code tables: independent of the fact upload
         for k in range(n_chunks):
             stream.wait_event(chunk_ev[k])
             r0, r1 = bounds[k], bounds[k + 1]
             for qi, p in enumerate(plans2):
-                p.scan_range(r0, r1 - r0, acc[offs[qi]: offs[qi + 1]], accumulate=k > 0)
+                p.scan_range(r0, r1 - r0, acc[offs[qi]: offs[qi + 1]], accumulate=True)
         if dist is not None:
             dist.all_reduce(acc)
         acc_host.copy_(acc, non_blocking=True)
@@ -449,7 +450,10 @@ def main():
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "kernel": "scan_direct_kernel (K4 ssb_scan_groupby)",
                          "algorithmic_bytes_per_launch": [int(b) for b in bytes_per_launch],
-                         "peak_source": peak_src},
+                         "peak_source": peak_src,
+                         "note": "peak is the measured copy bandwidth (read+write stream); the scan only reads, "
+                                 "which HBM3e serves slightly faster, so frac can exceed 1 against it",
+                         "frac_vs_nominal_7700": achieved / 7700.0},
             "cpu_baseline": cpu,
             "e2e": {"value": total_rows / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,

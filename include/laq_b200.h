@@ -383,6 +383,9 @@ int laq_plan_execute(laq_ctx* ctx, laq_plan* plan, int64_t* d_acc, int32_t accum
 /* The two halves of laq_plan_execute, for per-kernel timing: rebuild the
  * per-link code tables (dimension filters), then the fused fact scan. */
 int laq_plan_build_codes(laq_ctx* ctx, laq_plan* plan);
+/* The code tables of a batch of plans (e.g. one step of queries) in one launch
+ * (falls back to one launch per plan beyond 24 links in total). */
+int laq_plans_build_codes(laq_ctx* ctx, int32_t n_plans, laq_plan* const* plans);
 int laq_plan_scan(laq_ctx* ctx, laq_plan* plan, int64_t* d_acc, int32_t accumulate);
 /* Scan only fact rows [row0, row0 + rows) (row0 a multiple of 4) with the code
  * tables of the last build: lets a caller overlap the upload of later row

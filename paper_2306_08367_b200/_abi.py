@@ -13,7 +13,7 @@ from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 NATIVE_DIR = os.path.join(_HERE, "_native")
-LIB_PATH = os.path.join(NATIVE_DIR, "liblaq_b200.so")
+LIB_PATH = os.environ.get("LAQ_LIB_PATH") or os.path.join(NATIVE_DIR, "liblaq_b200.so")  # override: A/B builds
 GEN_LIB_PATH = os.path.join(NATIVE_DIR, "liblaq_gen.so")
 
 i64 = C.c_int64
@@ -95,6 +95,7 @@ _SIGS = {
     "laq_query_prepare": (C.c_int, [vp, vp, C.POINTER(QueryDesc), C.POINTER(vp), i64p]),
     "laq_plan_execute": (C.c_int, [vp, vp, vp, i32]),
     "laq_plan_build_codes": (C.c_int, [vp, vp]),
+    "laq_plans_build_codes": (C.c_int, [vp, i32, vp]),
     "laq_plan_scan": (C.c_int, [vp, vp, vp, i32]),
     "laq_plan_scan_range": (C.c_int, [vp, vp, i64, i64, vp, i32]),
     "laq_plan_bytes_per_row": (i64, [vp]),

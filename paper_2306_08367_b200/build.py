@@ -55,7 +55,7 @@ def build_cuda(force=False, verbose=False):
         if force or _stale(o, [s] + hdrs):
             cmd = [NVCC, *ARCH, "-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC",
                    "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "--expt-relaxed-constexpr",
-                   "-c", s, "-o", o]
+                   "-c", s, "-o", o] + os.environ.get("LAQ_NVCC_FLAGS", "").split()
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
             jobs.append(cmd)

@@ -206,7 +206,7 @@ __global__ void code_kernel(const CodeArgs a) {
 // slot -> dim row (probe table) -> filters -> group code, -1 for an empty slot
 // or a failing row.  Replaces a memset + code_kernel pair per link (bench
 // step: 2 launches per query instead of 2 per link + 1).
-constexpr int kMaxCodeLinks = 8;
+constexpr int kMaxCodeLinks = 24;  // links per fused code launch (a batch of up to 6 SSB queries)
 struct MultiCodeArgs {
   int n;
   int64_t start[kMaxCodeLinks + 1];  // prefix of slot counts, each rounded up to 32
@@ -407,27 +407,37 @@ struct laq_plan {
 namespace laq {
 namespace {
 
+// Every link's code table of a batch of plans in one codes_kernel launch.
+// Returns false (nothing launched) when the batch has more links than one
+// launch carries.
+bool build_codes_fused(laq_ctx* ctx, laq_plan* const* ps, int np) {
+  MultiCodeArgs m{};
+  int n = 0;
+  for (int i = 0; i < np; ++i) n += static_cast<int>(ps[i]->links.size());
+  if (n == 0) return true;
+  if (n > kMaxCodeLinks) return false;
+  for (int i = 0; i < np; ++i)
+    for (const auto& lc : ps[i]->links) {
+      m.link[m.n] = lc.args;
+      m.slot_row[m.n] = lc.slot_row;
+      m.slots[m.n] = lc.slots_used;
+      m.fmt[m.n] = lc.fmt;
+      m.packed[m.n] = lc.packed.get();
+      m.start[m.n + 1] = m.start[m.n] + ((lc.slots_used + 31) & ~int64_t{31});
+      ++m.n;
+    }
+  if (m.start[m.n] > 0) {
+    codes_kernel<<<grid_for(m.start[m.n], 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(m);
+    launched(ctx);
+  }
+  return true;
+}
+
 void build_codes(laq_ctx* ctx, laq_plan* p) {
   bool compact = false;
   for (auto& lc : p->links) compact = compact || lc.fmt != scan::kFmtGlobal;
-  if (!p->links.empty() && p->links.size() <= kMaxCodeLinks && (compact || !std::getenv("LAQ_CODES_PER_LINK"))) {
-    MultiCodeArgs m{};
-    m.n = static_cast<int>(p->links.size());
-    for (int j = 0; j < m.n; ++j) {
-      const auto& lc = p->links[j];
-      m.link[j] = lc.args;
-      m.slot_row[j] = lc.slot_row;
-      m.slots[j] = lc.slots_used;
-      m.fmt[j] = lc.fmt;
-      m.packed[j] = lc.packed.get();
-      m.start[j + 1] = m.start[j] + ((lc.slots_used + 31) & ~int64_t{31});
-    }
-    if (m.start[m.n] > 0) {
-      codes_kernel<<<grid_for(m.start[m.n], 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(m);
-      launched(ctx);
-    }
-    return;
-  }
+  if ((compact || !std::getenv("LAQ_CODES_PER_LINK")) && build_codes_fused(ctx, &p, 1)) return;
+  if (compact) fail(LAQ_ERR_UNSUPPORTED, "more links than one code launch carries");
   for (auto& lc : p->links) {
     LAQ_CUDA(cudaMemsetAsync(lc.code.get(), 0xFF, lc.slots * sizeof(int32_t), ctx->stream));
     if (lc.args.rows > 0) {
@@ -1092,6 +1102,14 @@ int32_t laq_plan_scanned_links(const laq_plan* p) { return p ? p->nl : 0; }
 
 int laq_plan_build_codes(laq_ctx* ctx, laq_plan* p) {
   return guard(ctx, [&] { build_codes(ctx, p); });
+}
+
+int laq_plans_build_codes(laq_ctx* ctx, int32_t n_plans, laq_plan* const* plans) {
+  return guard(ctx, [&] {
+    if (n_plans < 0) fail(LAQ_ERR_SHAPE, "negative plan count");
+    if (build_codes_fused(ctx, plans, n_plans)) return;
+    for (int i = 0; i < n_plans; ++i) build_codes(ctx, plans[i]);
+  });
 }
 
 int laq_plan_scan(laq_ctx* ctx, laq_plan* p, int64_t* d_acc, int32_t accumulate) {

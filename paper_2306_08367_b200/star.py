@@ -243,6 +243,16 @@ class DeviceStar:
             pass
 
 
+def build_codes_batch(plans) -> None:
+    """Code tables of several plans (one step of queries) in one launch
+    (laq_plans_build_codes)."""
+    if not plans:
+        return
+    ctx = plans[0].ctx
+    arr = (C.c_void_p * len(plans))(*[p.h.value if hasattr(p.h, "value") else p.h for p in plans])
+    ctx.check(ctx.lib.laq_plans_build_codes(ctx.h, len(plans), arr))
+
+
 def upload_gen_star(g, ctx=None, row_range=None) -> DeviceStar:
     """Upload a gen.GenStar (or oracle RefStar-like object with .tables/.kinds/.links())."""
     links = g.links() if callable(getattr(g, "links", None)) else g.links
