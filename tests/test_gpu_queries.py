@@ -177,3 +177,23 @@ def test_scan_ranges_sum_to_whole(gpu_ctx):
         for k in range(3):
             acc = p.scan_range(cuts[k], cuts[k + 1] - cuts[k], acc=None if acc is None else acc, accumulate=k > 0)
         assert np.array_equal(acc.cpu().numpy(), whole.cpu().numpy()), qg["id"]
+
+
+def test_batched_code_tables_equal_per_plan(gpu_ctx):
+    """laq_plans_build_codes: one launch for a batch of plans (and the per-plan
+    fallback beyond 24 links) gives the same accumulators as per-plan builds."""
+    from paper_2306_08367_b200 import gen, query as Q, star
+    g = gen.gen_star("Ssb", 1, 42, narrow=True)
+    ds = star.upload_gen_star(g)
+    qs = [Q.spec_with_dial(Q.group_defs(gr)[qi], gr, d)
+          for (gr, qi), d in {(1, 0): 222, (2, 1): 199, (3, 0): 90, (4, 2): 20, (2, 0): 500, (4, 0): 50,
+                              (3, 2): 40, (4, 1): 30, (1, 2): 133}.items()]
+    want = []
+    for q in qs:
+        p = ds.prepare(q)
+        want.append(p.execute().cpu().numpy().copy())
+    for batch in (qs[:6], qs):  # <= 24 links: one launch; all nine: per-plan fallback
+        plans = [ds.prepare(q) for q in batch]
+        star.build_codes_batch(plans)
+        for p, w in zip(plans, want):
+            assert np.array_equal(p.scan().cpu().numpy(), w), p.q.id
