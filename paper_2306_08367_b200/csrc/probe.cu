@@ -423,11 +423,9 @@ struct laq_probe {
   DevMem<uint32_t> bits[kMaxLinks];
   int64_t pslot_l = 0;
   bool bound = false;
-  // two-pass chunk counts / offsets + scan temp storage
+  // chunk counts / offsets (scan_chunks_kernel)
   DevMem<int> chunk_counts;
   DevMem<int64_t> chunk_offsets;
-  DevMem<char> scan_tmp;
-  size_t scan_tmp_bytes = 0;
   int64_t chunk_cap = 0;
   // optimistic single pass: [0] chunks with a missing key (counted by the
   // direct pass, moved to [1] and cleared by the scan pass), [1] the decision
