@@ -105,11 +105,15 @@ __device__ bool parse_i64(const char* s, int len, int64_t* out) {
   if (neg) ++i;
   if (i >= len) return false;
   uint64_t v = 0;
-  const uint64_t lim = neg ? 9223372036854775808ull : 9223372036854775807ull;
+  // v * 10 + d <= lim  <=>  v < lim / 10, or v == lim / 10 and d <= lim % 10
+  // (lim / 10 = 922337203685477580; lim % 10 = 8 for -2^63, 7 for 2^63 - 1)
+  constexpr uint64_t kTenth = 922337203685477580ull;
+  const uint64_t last = neg ? 8u : 7u;
   for (; i < len; ++i) {
-    if (!is_digit(s[i])) return false;
-    const uint64_t d = static_cast<uint64_t>(s[i] - '0');
-    if (v > (lim - d) / 10) return false;  // out of range
+    const char ch = s[i];
+    if (!is_digit(ch)) return false;
+    const uint64_t d = static_cast<uint64_t>(ch - '0');
+    if (v > kTenth || (v == kTenth && d > last)) return false;  // out of range
     v = v * 10 + d;
   }
   *out = neg ? static_cast<int64_t>(0 - v) : static_cast<int64_t>(v);
