@@ -386,6 +386,13 @@ int laq_plan_build_codes(laq_ctx* ctx, laq_plan* plan);
 /* The code tables of a batch of plans (e.g. one step of queries) in one launch
  * (falls back to one launch per plan beyond 24 links in total). */
 int laq_plans_build_codes(laq_ctx* ctx, int32_t n_plans, laq_plan* const* plans);
+/* Scan a batch of 2-3 plans that read the same fact columns in the same roles
+ * (e.g. Q1.1-Q1.3) in ONE pass over the fact table: each column vector is
+ * loaded once and every query evaluates its own filters, probes and group bins
+ * into its own accumulator d_accs[q].  *h_shared = 1 when the batch qualified,
+ * 0 when it was scanned one plan at a time (same results either way). */
+int laq_plans_scan_shared(laq_ctx* ctx, int32_t n_plans, laq_plan* const* plans, int64_t* const* d_accs,
+                          int32_t accumulate, int32_t* h_shared);
 int laq_plan_scan(laq_ctx* ctx, laq_plan* plan, int64_t* d_acc, int32_t accumulate);
 /* Scan only fact rows [row0, row0 + rows) (row0 a multiple of 4) with the code
  * tables of the last build: lets a caller overlap the upload of later row

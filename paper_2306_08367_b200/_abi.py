@@ -96,6 +96,7 @@ _SIGS = {
     "laq_plan_execute": (C.c_int, [vp, vp, vp, i32]),
     "laq_plan_build_codes": (C.c_int, [vp, vp]),
     "laq_plans_build_codes": (C.c_int, [vp, i32, vp]),
+    "laq_plans_scan_shared": (C.c_int, [vp, i32, vp, vp, i32, i32p]),
     "laq_plan_scan": (C.c_int, [vp, vp, vp, i32]),
     "laq_plan_scan_range": (C.c_int, [vp, vp, i64, i64, vp, i32]),
     "laq_plan_bytes_per_row": (i64, [vp]),

@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "ssb_launch.cuh"
+#include "ssb_shared.cuh"
 
 namespace laq {
 namespace {
@@ -1119,6 +1120,95 @@ int laq_plan_scan(laq_ctx* ctx, laq_plan* p, int64_t* d_acc, int32_t accumulate)
     ScanArgs a = p->scan;
     a.acc = reinterpret_cast<unsigned long long*>(d_acc);
     launch_scan(ctx, a, p->nl, p->nf, p->mode, p->variant, p->vec, p->grid, p->smem);
+  });
+}
+
+// Shared scan of a batch of plans (ssb_shared.cu).  Every plan must be a
+// direct-kernel plan over the same int32 fact columns in the same roles (foreign
+// keys, fact filters, measure); each plan's links and filters are re-ordered to
+// the first plan's column order (the probe order changes, the result does not).
+// Returns false when the batch does not qualify (the caller scans one by one).
+static bool scan_shared(laq_ctx* ctx, int n, laq_plan* const* ps, int64_t* const* accs) {
+  using namespace scan;
+  if (n < 2 || n > kMaxShared || std::getenv("LAQ_NO_SHARED_SCAN")) return false;
+  const laq_plan* p0 = ps[0];
+  if (p0->variant != 4 || p0->fact_rows == 0) return false;
+  SharedScan M{};
+  int optin = 0;
+  LAQ_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+  const int64_t budget = static_cast<int64_t>(optin) - 2048;
+  int64_t off = 0;
+  int64_t flush = INT64_MAX;
+  int prefetch = 0;
+  for (int q = 0; q < n; ++q) {
+    const laq_plan* p = ps[q];
+    const ScanArgs& a = p->scan;
+    if (p->variant != 4 || p->nl != p0->nl || p->nf != p0->nf || p->mode != p0->mode || p->fact_rows != p0->fact_rows)
+      return false;
+    if (p->mode == 1 && !a.narrow_bins) return false;
+    if ((a.measure == nullptr) != (p0->scan.measure == nullptr)) return false;
+    if (a.measure && a.mc.p != p0->scan.mc.p) return false;
+    ScanArgs b = a;
+    // links: align to plan 0's fk columns
+    bool used[kMaxLinks] = {};
+    for (int j = 0; j < p0->nl; ++j) {
+      int k = -1;
+      for (int t = 0; t < p->nl && k < 0; ++t)
+        if (!used[t] && a.fkc[t].p == p0->scan.fkc[j].p) k = t;
+      if (k < 0) return false;
+      used[k] = true;
+      b.fk[j] = a.fk[k];
+      b.fkc[j] = a.fkc[k];
+      b.link[j] = a.link[k];
+    }
+    bool fused[kMaxFactFilters] = {};
+    for (int f = 0; f < p0->nf; ++f) {
+      int k = -1;
+      for (int t = 0; t < p->nf && k < 0; ++t)
+        if (!fused[t] && a.ffc[t].p == p0->scan.ffc[f].p) k = t;
+      if (k < 0) return false;
+      fused[k] = true;
+      b.ff[f] = a.ff[k];
+      b.ffc[f] = a.ffc[k];
+    }
+    // this query's staged tables, rebased after the previous queries'
+    const int64_t base = off;
+    for (int j = 0; j < p0->nl; ++j)
+      if (b.link[j].fmt != kFmtGlobal) b.link[j].smem_byte += static_cast<int>(base);
+    off += (a.smem_tab_elems + 15) & ~15;
+    b.acc = reinterpret_cast<unsigned long long*>(accs[q]);
+    M.q[q] = b;
+    flush = std::min<int64_t>(flush, std::max<int64_t>(1, a.flush_every));
+    prefetch = std::max(prefetch, a.prefetch);
+  }
+  for (int q = 0; q < n; ++q) {
+    M.bins_off[q] = off;
+    if (p0->mode == 1) off += 8 * ps[q]->G;
+  }
+  if (off > budget) return false;
+  M.flush_every = flush;
+  M.prefetch = prefetch;
+  launch_shared(ctx, M, n, p0->nl, p0->nf, p0->mode, static_cast<size_t>(off));
+  return true;
+}
+
+int laq_plans_scan_shared(laq_ctx* ctx, int32_t n_plans, laq_plan* const* plans, int64_t* const* d_accs,
+                          int32_t accumulate, int32_t* h_shared) {
+  return guard(ctx, [&] {
+    if (n_plans < 0) fail(LAQ_ERR_SHAPE, "negative plan count");
+    if (!accumulate)
+      for (int q = 0; q < n_plans; ++q)
+        LAQ_CUDA(cudaMemsetAsync(d_accs[q], 0, 2 * plans[q]->G * sizeof(int64_t), ctx->stream));
+    const bool shared = scan_shared(ctx, n_plans, plans, d_accs);
+    if (!shared)
+      for (int q = 0; q < n_plans; ++q) {
+        laq_plan* p = plans[q];
+        if (p->fact_rows == 0) continue;
+        ScanArgs a = p->scan;
+        a.acc = reinterpret_cast<unsigned long long*>(d_accs[q]);
+        launch_scan(ctx, a, p->nl, p->nf, p->mode, p->variant, p->vec, p->grid, p->smem);
+      }
+    if (h_shared) *h_shared = shared ? 1 : 0;
   });
 }
 

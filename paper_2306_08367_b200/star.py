@@ -253,6 +253,17 @@ def build_codes_batch(plans) -> None:
     ctx.check(ctx.lib.laq_plans_build_codes(ctx.h, len(plans), arr))
 
 
+def scan_shared(plans, accs, accumulate=False) -> bool:
+    """One pass over the fact table for a batch of 2-3 plans reading the same
+    columns (laq_plans_scan_shared); returns whether the batch was shared."""
+    ctx = plans[0].ctx
+    hp = (C.c_void_p * len(plans))(*[p.h.value for p in plans])
+    ha = (C.c_void_p * len(plans))(*[a.data_ptr() for a in accs])
+    shared = C.c_int32()
+    ctx.check(ctx.lib.laq_plans_scan_shared(ctx.h, len(plans), hp, ha, 1 if accumulate else 0, C.byref(shared)))
+    return bool(shared.value)
+
+
 def upload_gen_star(g, ctx=None, row_range=None) -> DeviceStar:
     """Upload a gen.GenStar (or oracle RefStar-like object with .tables/.kinds/.links())."""
     links = g.links() if callable(getattr(g, "links", None)) else g.links

@@ -9,6 +9,6 @@ python - <<'PY'
 import json
 d = json.load(open("gpurun_out/bench.json"))
 print("value %.3e  ms/step %.3f  frac %.3f  e2e %.3e" % (d["value"], d["ms_per_step"], d["roofline"]["frac"], d["e2e"]["value"]))
-print("per-query scan ms", d["config"]["per_query_scan_ms"])
+print("per-launch scan ms", d["config"]["per_launch_scan_ms"], d["config"]["shared_scan"])
 print("secondary", json.dumps(d["secondary"])[:600])
 PY

@@ -197,3 +197,29 @@ def test_batched_code_tables_equal_per_plan(gpu_ctx):
         star.build_codes_batch(plans)
         for p, w in zip(plans, want):
             assert np.array_equal(p.scan().cpu().numpy(), w), p.q.id
+
+
+def test_shared_scan_equals_individual_scans(gpu_ctx):
+    """laq_plans_scan_shared: Q1.1-Q1.3, Q2.1-Q2.3, Q3.x and Q4.x batches in one
+    pass over the fact table equal the queries scanned one by one; a batch
+    mixing column sets falls back to one-by-one scans with the same results."""
+    import torch
+    from paper_2306_08367_b200 import gen, query as Q, star
+    g = gen.gen_star("Ssb", 1, 42, narrow=True)
+    ds = star.upload_gen_star(g)
+    dials = {1: (222, 200, 133), 2: (500, 199, 516), 3: (90, 60, 40), 4: (50, 30, 20)}
+    batches = [[(gr, qi) for qi in range(3)] for gr in (1, 2, 3, 4)] + [[(2, 0), (2, 2)], [(1, 0), (2, 0)]]
+    for batch in batches:
+        qs = [Q.spec_with_dial(Q.group_defs(gr)[qi], gr, dials[gr][qi]) for gr, qi in batch]
+        plans = [ds.prepare(q) for q in qs]
+        want = [p.execute().cpu().numpy().copy() for p in plans]
+        star.build_codes_batch(plans)
+        accs = [torch.full_like(p.acc, 7) for p in plans]
+        shared = star.scan_shared(plans, accs)
+        torch.cuda.synchronize()
+        if len({gr for gr, _ in batch}) > 1:
+            assert not shared, batch  # different column sets: one by one
+        if batch[0][0] == 1 and len(batch) == 3:
+            assert shared  # Q1.x: same columns, small tables -> one pass
+        for a, w, q in zip(accs, want, qs):
+            assert np.array_equal(a.cpu().numpy(), w), (batch, q.id)
