@@ -513,9 +513,11 @@ def main():
 
 def ncu_traffic():
     """DRAM bytes (read + write) per scan launch from the committed ncu --set full
-    capture of the same six queries (profiles/<round>/scan_full_metrics.json)."""
+    capture of the bench's scan launches (profiles/<round>/shared_full_metrics.json:
+    the shared passes; else scan_full_metrics.json: per-query scans)."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "scan_full_metrics.json")))
+    files = (sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "shared_full_metrics.json")))
+             or sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "scan_full_metrics.json"))))
     if not files:
         return None
     rows = json.load(open(files[-1]))

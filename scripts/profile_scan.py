@@ -24,8 +24,12 @@ def main():
     for p in plans:
         p.build_codes()
     torch.cuda.synchronize()
-    for p in plans:
-        p.scan()
+    if os.environ.get("LAQ_PROFILE_SHARED") == "1":  # the bench's shared passes (one per query group)
+        star.scan_shared(plans[:3], [p.acc for p in plans[:3]])
+        star.scan_shared(plans[3:], [p.acc for p in plans[3:]])
+    else:
+        for p in plans:
+            p.scan()
     torch.cuda.synchronize()
     for p in plans:
         print(p.q.id, "pipe" if p.bytes_per_row else "", p.emit(p.acc.cpu().numpy())[:2].tolist())

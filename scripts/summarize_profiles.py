@@ -35,6 +35,7 @@ def raw(rep):
 
 lines = []
 for rep, title in (("scan_full.ncu-rep", "K4 scan (6 bench queries: Q1.1-Q1.3, Q2.1-Q2.3, SF=10)"),
+                   ("shared_full.ncu-rep", "K4 shared scans (the bench's passes: Q1.1-Q1.3 and Q2.1-Q2.3, SF=10)"),
                    ("predict_full.ncu-rep", "K2+K3 fused predict (1e8 fact rows, cfg1 dims)")):
     p = os.path.join(G, rep)
     if not os.path.exists(p):
