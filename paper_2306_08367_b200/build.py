@@ -69,7 +69,9 @@ def build_cuda(force=False, verbose=False):
 
 
 def build_oracle():
-    """Compile the reference (only where /root/reference exists: this container)."""
+    """Compile the parity checkers: oracle/ssb_oracle.c always, the reference
+    itself only where /root/reference exists (this container)."""
+    _run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "checker"])
     if os.path.isdir("/root/reference/proj/src"):
         _run(["make", "-s", "-j8", "-C", os.path.join(ROOT, "oracle")])
 

@@ -124,21 +124,31 @@ struct Star {
   bool narrow = false;
 };
 
+// Row window of the fact table a generator call keeps: all n values are drawn
+// (the engine stream must advance exactly as in the reference, one column
+// after the other), only rows [lo, hi) are stored.  The default keeps all.
+struct Window {
+  std::int64_t lo = 0, hi = INT64_MAX;
+};
+
 // Emit an integer column through a per-value generator.
 template <class F>
-void fill_int(Col& c, std::int64_t n, bool narrow, F&& f) {
+void fill_int(Col& c, std::int64_t n, bool narrow, F&& f, Window w = {}) {
+  const std::int64_t lo = std::min(w.lo, n), hi = std::max(lo, std::min(w.hi, n));
+  for (std::int64_t i = 0; i < lo; ++i) (void)f();
   if (narrow) {
-    c.i32.resize(static_cast<std::size_t>(n));
-    for (std::int64_t i = 0; i < n; ++i) c.i32[i] = static_cast<std::int32_t>(f());
+    c.i32.resize(static_cast<std::size_t>(hi - lo));
+    for (std::int64_t i = lo; i < hi; ++i) c.i32[i - lo] = static_cast<std::int32_t>(f());
   } else {
-    c.i64.resize(static_cast<std::size_t>(n));
-    for (std::int64_t i = 0; i < n; ++i) c.i64[i] = f();
+    c.i64.resize(static_cast<std::size_t>(hi - lo));
+    for (std::int64_t i = lo; i < hi; ++i) c.i64[i - lo] = f();
   }
+  for (std::int64_t i = hi; i < n; ++i) (void)f();
 }
 
-void uniform_col(Col& c, Rng& rng, std::int64_t n, std::int64_t lo, std::int64_t hi, bool narrow) {
+void uniform_col(Col& c, Rng& rng, std::int64_t n, std::int64_t lo, std::int64_t hi, bool narrow, Window w = {}) {
   const Rng::Bounded b(static_cast<std::uint64_t>(hi - lo));
-  fill_int(c, n, narrow, [&] { return lo + static_cast<std::int64_t>(rng.bounded(b)); });
+  fill_int(c, n, narrow, [&] { return lo + static_cast<std::int64_t>(rng.bounded(b)); }, w);
 }
 
 void iota_col(Col& c, std::int64_t n, bool narrow) {
@@ -147,12 +157,12 @@ void iota_col(Col& c, std::int64_t n, bool narrow) {
 }
 
 // benchgen.cpp:46-55
-void fk_col(Col& c, Rng& rng, std::int64_t n, std::int64_t dim_rows, double dangling, bool narrow) {
+void fk_col(Col& c, Rng& rng, std::int64_t n, std::int64_t dim_rows, double dangling, bool narrow, Window w = {}) {
   const Rng::Bounded b(static_cast<std::uint64_t>(dim_rows));
   fill_int(c, n, narrow, [&] {
     const bool miss = dangling > 0.0 && rng.unit() < dangling;
     return static_cast<std::int64_t>(rng.bounded(b)) + (miss ? dim_rows : 0);
-  });
+  }, w);
 }
 
 std::vector<std::int64_t> split_features(std::int64_t k, std::size_t parts) {  // benchgen.cpp:57-61
@@ -233,9 +243,13 @@ const char* laqgen_last_error() { return g_err.c_str(); }
 // fact_tag != NULL draws lineorder from derive_seed(seed, "lineorder/<tag>")
 // instead of "lineorder": an independent fact shard over the SAME dimension
 // tables (weak-scaling runs give every GPU its own SF-sized shard).
-int laqgen_star_create_tagged(int setting, std::int64_t sf, std::uint64_t seed, std::int64_t feature_width,
-                              double dangling, std::int64_t max_bytes, int narrow32, const char* fact_tag,
-                              laqgen_star** out) {
+// row_lo / row_hi: keep only lineorder rows [row_lo, row_hi) of the canonical
+// table (a contiguous row shard for multi-GPU runs: every rank draws the same
+// stream and stores its own rows, so the shards concatenate to exactly the
+// reference's table).  row_hi < 0 keeps everything.
+int laqgen_star_create_shard(int setting, std::int64_t sf, std::uint64_t seed, std::int64_t feature_width,
+                             double dangling, std::int64_t max_bytes, int narrow32, const char* fact_tag,
+                             std::int64_t row_lo, std::int64_t row_hi, laqgen_star** out) {
   try {
     if (sf < 1) { g_err = "scale factor must be >= 1"; return 12; }
     if (feature_width < 0) { g_err = "feature width must be >= 0"; return 12; }
@@ -254,6 +268,15 @@ int laqgen_star_create_tagged(int setting, std::int64_t sf, std::uint64_t seed, 
       g_err = "dataset needs " + std::to_string(cells * 8) + " bytes, cap is " + std::to_string(max_bytes);
       return 13;
     }
+    Window w;
+    if (row_hi >= 0) {
+      if (row_lo < 0 || row_lo > row_hi || row_hi > card.lineorder) {
+        g_err = "fact row window out of range";
+        return 12;
+      }
+      w.lo = row_lo;
+      w.hi = row_hi;
+    }
     const bool narrow = narrow32 != 0;
     auto s = std::make_unique<Star>();
     s->narrow = narrow;
@@ -269,21 +292,21 @@ int laqgen_star_create_tagged(int setting, std::int64_t sf, std::uint64_t seed, 
       Rng rng(derive_seed(seed, fact_tag ? std::string("lineorder/") + fact_tag : std::string("lineorder")));
       Tab& t = s->tables[0];
       t.name = "lineorder";
-      t.rows = card.lineorder;
+      t.rows = std::min(w.hi, card.lineorder) - std::min(w.lo, card.lineorder);
       t.cols.reserve(8);
       auto add = [&](const char* n, int kind) -> Col& {
         t.cols.push_back(Col{n, kind, {}, {}, {}});
         return t.cols.back();
       };
       const std::int64_t n = card.lineorder;
-      fk_col(add("lo_part", 0), rng, n, card.part, dangling, narrow);
-      fk_col(add("lo_supplier", 0), rng, n, card.supplier, dangling, narrow);
-      fk_col(add("lo_orderdate", 0), rng, n, card.date, dangling, narrow);
-      fk_col(add("lo_commitdate", 0), rng, n, card.date, dangling, narrow);
-      if (with_customer) fk_col(add("lo_customer", 0), rng, n, card.customer, dangling, narrow);
-      uniform_col(add("lo_quantity", 1), rng, n, 1, 51, narrow);
-      uniform_col(add("lo_discount", 1), rng, n, 0, 11, narrow);
-      uniform_col(add("lo_revenue", 1), rng, n, 100, 10000, narrow);
+      fk_col(add("lo_part", 0), rng, n, card.part, dangling, narrow, w);
+      fk_col(add("lo_supplier", 0), rng, n, card.supplier, dangling, narrow, w);
+      fk_col(add("lo_orderdate", 0), rng, n, card.date, dangling, narrow, w);
+      fk_col(add("lo_commitdate", 0), rng, n, card.date, dangling, narrow, w);
+      if (with_customer) fk_col(add("lo_customer", 0), rng, n, card.customer, dangling, narrow, w);
+      uniform_col(add("lo_quantity", 1), rng, n, 1, 51, narrow, w);
+      uniform_col(add("lo_discount", 1), rng, n, 0, 11, narrow, w);
+      uniform_col(add("lo_revenue", 1), rng, n, 100, 10000, narrow, w);
     }
     dims.join();
     *out = reinterpret_cast<laqgen_star*>(s.release());
@@ -292,6 +315,13 @@ int laqgen_star_create_tagged(int setting, std::int64_t sf, std::uint64_t seed, 
     g_err = e.what();
     return 1;
   }
+}
+
+int laqgen_star_create_tagged(int setting, std::int64_t sf, std::uint64_t seed, std::int64_t feature_width,
+                              double dangling, std::int64_t max_bytes, int narrow32, const char* fact_tag,
+                              laqgen_star** out) {
+  return laqgen_star_create_shard(setting, sf, seed, feature_width, dangling, max_bytes, narrow32, fact_tag, 0, -1,
+                                  out);
 }
 
 int laqgen_star_create(int setting, std::int64_t sf, std::uint64_t seed, std::int64_t feature_width,

@@ -4,7 +4,8 @@
 // groupby_sum_single = spmm(valued key_matrix(R), key->group matrix) then a
 // ones reduction.  The key->group matrix is built as sorted (key, group) runs
 // with multiplicities (csr_from_triplets sums duplicates); each R row probes
-// its key's run and adds v * multiplicity into its groups.
+// its key's run and emits v * multiplicity per group, and every group's terms
+// are summed in ascending R-row order (bit-identical to the reference).
 //
 // groupby_sum_multi = sort-unique over tuples + segmented sum in row order.
 // Tuples are ranked per column (distinct values -> dense ranks), packed into
@@ -63,18 +64,47 @@ __global__ void pair_code_kernel(const int64_t* __restrict__ ks, const int64_t* 
     code[i] = find_sorted(dk, nk, ks[i]) * G + find_sorted(dg, G, gs[i]);
 }
 
-__global__ void single_accumulate(const int64_t* __restrict__ kr, const double* __restrict__ vr, int64_t nr,
-                                  const int64_t* __restrict__ dk, int64_t nk, const int64_t* __restrict__ key_run_off,
-                                  const int64_t* __restrict__ pair_codes, const int64_t* __restrict__ pair_cnt,
-                                  int64_t G, double* sums) {
+// groupby_sum_single, pass 1: how many (group, value) terms each R row adds
+// (its key's number of distinct groups; 0 for a zero value or a key absent from S).
+__global__ void single_count(const int64_t* __restrict__ kr, const double* __restrict__ vr, int64_t nr,
+                             const int64_t* __restrict__ dk, int64_t nk, const int64_t* __restrict__ key_run_off,
+                             int64_t* __restrict__ cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nr; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c = 0;
+    if (vr[i] != 0.0) {  // key_matrix skips zero values (laqops.cpp:188-190)
+      const int64_t kp = find_sorted(dk, nk, kr[i]);
+      if (kp >= 0) c = key_run_off[kp + 1] - key_run_off[kp];
+    }
+    cnt[i] = c;
+  }
+}
+
+// Pass 2: per_row = spmm(valued key_matrix(R), key->group) entries in R-row
+// order: term = v * multiplicity (0.0 + v*m in the reference's accumulator,
+// matrix.cpp:107-113, which is exact), tagged with its group.
+__global__ void single_terms(const int64_t* __restrict__ kr, const double* __restrict__ vr, int64_t nr,
+                             const int64_t* __restrict__ dk, int64_t nk, const int64_t* __restrict__ key_run_off,
+                             const int64_t* __restrict__ pair_codes, const int64_t* __restrict__ pair_cnt, int64_t G,
+                             const int64_t* __restrict__ row_off, int64_t* __restrict__ term_group,
+                             double* __restrict__ term_val, int64_t* __restrict__ term_idx) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nr; i += (int64_t)gridDim.x * blockDim.x) {
     const double v = vr[i];
-    if (v == 0.0) continue;  // key_matrix skips zero values (laqops.cpp:188-190)
+    if (v == 0.0) continue;
     const int64_t kp = find_sorted(dk, nk, kr[i]);
     if (kp < 0) continue;
-    for (int64_t t = key_run_off[kp]; t < key_run_off[kp + 1]; ++t)
-      atomicAdd(sums + pair_codes[t] % G, __dmul_rn(v, static_cast<double>(pair_cnt[t])));
+    int64_t o = row_off[i];
+    for (int64_t t = key_run_off[kp]; t < key_run_off[kp + 1]; ++t, ++o) {
+      term_group[o] = pair_codes[t] % G;
+      term_val[o] = __dmul_rn(v, static_cast<double>(pair_cnt[t]));
+      term_idx[o] = o;
+    }
   }
+}
+
+__global__ void scatter_sums(const int64_t* __restrict__ seg_group, const double* __restrict__ seg_sum, int64_t n_seg,
+                             double* __restrict__ sums) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_seg; s += (int64_t)gridDim.x * blockDim.x)
+    sums[seg_group[s]] = seg_sum[s];
 }
 
 __global__ void key_of_pair(const int64_t* __restrict__ codes, int64_t n, int64_t G, int64_t* out) {
@@ -176,9 +206,34 @@ int laq_groupby_sum_single(laq_ctx* ctx, const int64_t* kr, const double* vr, in
     LAQ_CUDA(cudaMemcpyAsync(key_off.get() + NK, &ctx->h_pinned[8], sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
     LAQ_CUDA(cudaMemsetAsync(out_sums, 0, G * sizeof(double), ctx->stream));
     if (nr) {
-      single_accumulate<<<grid_for(nr, 256, g), 256, 0, ctx->stream>>>(kr, vr, nr, dkeys.get(), NK, key_off.get(),
-                                                                       uniq.get(), cnt.get(), G, out_sums);
+      // The ones reduction sums per_row's entries in ascending R-row order
+      // (laqops.cpp:404-405): terms are laid out in row order, stably sorted
+      // by group, and each group's run is summed sequentially (segsum_kernel).
+      DevBuf<int64_t> rcnt(ctx, nr), roff(ctx, nr);
+      single_count<<<grid_for(nr, 256, g), 256, 0, ctx->stream>>>(kr, vr, nr, dkeys.get(), NK, key_off.get(),
+                                                                  rcnt.get());
       launched(ctx);
+      int64_t nt = 0;
+      exclusive_scan_i64(ctx, rcnt.get(), roff.get(), nr, &nt);
+      if (nt > 0) {
+        DevBuf<int64_t> tg(ctx, nt), ti(ctx, nt), sg(ctx, nt), si(ctx, nt), ug(ctx, nt), uc(ctx, nt), so(ctx, nt + 1);
+        DevBuf<double> tv(ctx, nt), ss(ctx, nt);
+        single_terms<<<grid_for(nr, 256, g), 256, 0, ctx->stream>>>(kr, vr, nr, dkeys.get(), NK, key_off.get(),
+                                                                    uniq.get(), cnt.get(), G, roff.get(), tg.get(),
+                                                                    tv.get(), ti.get());
+        launched(ctx);
+        sort_pairs(ctx, tg.get(), sg.get(), ti.get(), si.get(), nt);  // stable: row order kept per group
+        const int64_t ng = run_length(ctx, sg.get(), nt, ug.get(), uc.get());
+        int64_t tot = 0;
+        exclusive_scan_i64(ctx, uc.get(), so.get(), ng, &tot);
+        ctx->h_pinned[8] = tot;
+        LAQ_CUDA(cudaMemcpyAsync(so.get() + ng, &ctx->h_pinned[8], sizeof(int64_t), cudaMemcpyHostToDevice,
+                                 ctx->stream));
+        segsum_kernel<<<grid_for(ng, 128, g), 128, 0, ctx->stream>>>(so.get(), ng, si.get(), tv.get(), ss.get());
+        launched(ctx);
+        scatter_sums<<<grid_for(ng, 256, g), 256, 0, ctx->stream>>>(ug.get(), ss.get(), ng, out_sums);
+        launched(ctx);
+      }
     }
     LAQ_CUDA(cudaMemcpyAsync(out_groups, groups.get(), G * sizeof(int64_t), cudaMemcpyDeviceToDevice, ctx->stream));
     sync(ctx);

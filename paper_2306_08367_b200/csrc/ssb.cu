@@ -475,10 +475,13 @@ void lay_out_scan(laq_ctx* ctx, laq_plan* p, const std::vector<const int32_t*>& 
   const int64_t budget = static_cast<int64_t>(optin) - 2048;  // static smem + mbarriers
   const int nc = p->nl + p->nf + (a.measure ? 1 : 0);
   const int64_t stage_bytes = static_cast<int64_t>(nc) * scan::kTile * 4;
-  // 32-bit bins are exact when a tile's largest possible sum fits 32 bits; the
-  // kernel spills them to the 64-bit accumulator every flush_every tiles.
+  // 32-bit bins are exact when the largest sum one CTA can add between two
+  // spills fits 32 bits.  The widest step of any scan kernel is the direct
+  // kernel's 1024 threads x 4 rows = 4096 rows, so vmax < 2^20 keeps even a
+  // flush_every of 1 exact (4096 * vmax < 2^32); wider measures take 64-bit bins.
   const int64_t vmax = a.measure ? std::max<int64_t>(measure_max, 1) : 1;
-  const bool narrow = a.measure == nullptr || (measure_min >= 0 && vmax < (int64_t{1} << 21));
+  const bool narrow = a.measure == nullptr ||
+                      (measure_min >= 0 && vmax * int64_t{scan::kDirectThreads} * 4 < (int64_t{1} << 32));
   const int64_t bin_bytes = p->mode == 1 ? (narrow ? 8 : 16) * p->G : 0;
   const int64_t tab_budget = budget - bin_bytes - 4 * stage_bytes;
 
@@ -499,7 +502,9 @@ void lay_out_scan(laq_ctx* ctx, laq_plan* p, const std::vector<const int32_t*>& 
     std::vector<int> fmt(nl, scan::kFmtGlobal);
     for (int j = 0; j < nl; ++j) {
       const auto& lc = p->links[j];
-      const int64_t slots = probes[j]->size;
+      // lc.slots = max(probe size, 1): an empty dimension still gets a one-slot
+      // (all-fail) compact table, which codes_kernel writes.
+      const int64_t slots = lc.slots;
       if (lc.args.n_groups == 0) fmt[j] = scan::kFmtBit, need[j] = ((slots + 31) / 32) * 4;
       else if (lc.max_code <= 254) fmt[j] = scan::kFmtU8, need[j] = slots;
       else if (lc.max_code <= 32767) fmt[j] = scan::kFmtS16, need[j] = 2 * slots;
@@ -519,7 +524,7 @@ void lay_out_scan(laq_ctx* ctx, laq_plan* p, const std::vector<const int32_t*>& 
     // upgrades never evict another link's table.
     for (int j : by) {
       if (!staged[j] || fmt[j] != scan::kFmtBit) continue;
-      const int64_t u8 = (probes[j]->size + 15) & ~int64_t{15};
+      const int64_t u8 = (p->links[j].slots + 15) & ~int64_t{15};
       if (u8 - need[j] <= room) {
         room -= u8 - need[j];
         fmt[j] = scan::kFmtU8;
@@ -1133,6 +1138,9 @@ static bool scan_shared(laq_ctx* ctx, int n, laq_plan* const* ps, int64_t* const
   if (n < 2 || n > kMaxShared || std::getenv("LAQ_NO_SHARED_SCAN")) return false;
   const laq_plan* p0 = ps[0];
   if (p0->variant != 4 || p0->fact_rows == 0) return false;
+  // launch_shared instantiates 1..4 links and 0..2 fact filters; other shapes
+  // take the one-plan-at-a-time path (same results).
+  if (p0->nl < 1 || p0->nl > 4 || p0->nf > 2) return false;
   SharedScan M{};
   int optin = 0;
   LAQ_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));

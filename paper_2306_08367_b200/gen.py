@@ -30,6 +30,8 @@ def lib():
                                          C.c_int, C.POINTER(C.c_void_p)]
         L.laqgen_star_create_tagged.argtypes = [C.c_int, C.c_int64, C.c_uint64, C.c_int64, C.c_double, C.c_int64,
                                                 C.c_int, C.c_char_p, C.POINTER(C.c_void_p)]
+        L.laqgen_star_create_shard.argtypes = [C.c_int, C.c_int64, C.c_uint64, C.c_int64, C.c_double, C.c_int64,
+                                               C.c_int, C.c_char_p, C.c_int64, C.c_int64, C.POINTER(C.c_void_p)]
         L.laqgen_star_destroy.argtypes = [C.c_void_p]
         L.laqgen_n_tables.argtypes = [C.c_void_p]
         L.laqgen_table_name.restype = C.c_char_p
@@ -98,12 +100,16 @@ class GenStar:
 
 
 def gen_star(setting="Ssb", sf=1, seed=42, feature_width=0, dangling=0.0, max_bytes=0, narrow=False,
-             fact_tag=None) -> GenStar:
+             fact_tag=None, row_range=None) -> GenStar:
     """gen_star (benchgen.cpp:190-193).  fact_tag: draw the fact table from an
-    independent stream over the same dimensions (per-GPU weak-scaling shards)."""
+    independent stream over the same dimensions.  row_range=(lo, hi): keep only
+    lineorder rows [lo, hi) of the canonical table (a row shard: the full
+    stream is drawn, only the shard is stored)."""
     h = C.c_void_p()
-    rc = lib().laqgen_star_create_tagged(SETTINGS[setting], sf, seed, feature_width, dangling, max_bytes,
-                                         1 if narrow else 0, fact_tag.encode() if fact_tag else None, C.byref(h))
+    lo, hi = row_range if row_range is not None else (0, -1)
+    rc = lib().laqgen_star_create_shard(SETTINGS[setting], sf, seed, feature_width, dangling, max_bytes,
+                                        1 if narrow else 0, fact_tag.encode() if fact_tag else None, lo, hi,
+                                        C.byref(h))
     errors.raise_for(rc, lib().laqgen_last_error().decode())
     return GenStar(h.value, narrow)
 

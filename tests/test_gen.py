@@ -61,3 +61,21 @@ def test_capacity_guard():
         gen.gen_star("Ssb", 100, 42, max_bytes=1 << 20)
     with pytest.raises(errors.GenError):
         gen.gen_star("S2", 0, 42)
+
+
+def test_row_shards_concatenate_to_the_canonical_table():
+    """Strong row sharding: every rank draws the canonical stream
+    and keeps rows [lo, hi); the shards concatenate to the full table."""
+    gen = _gen()
+    from paper_2306_08367_b200 import dist, errors
+    full = gen.gen_star("S1", 2, 7, narrow=True)
+    n = len(full.fact["lo_part"])
+    for world in (1, 3, 8):
+        parts = [gen.gen_star("S1", 2, 7, narrow=True, row_range=dist.shard_range(n, r, world)) for r in range(world)]
+        for c, a in full.fact.items():
+            assert np.array_equal(np.concatenate([p.fact[c] for p in parts]), a), (world, c)
+        for t in ("part", "supplier", "date"):
+            for c, a in full.tables[t].items():
+                assert np.array_equal(parts[-1].tables[t][c], a)
+    with pytest.raises(errors.GenError):
+        gen.gen_star("S1", 2, 7, row_range=(5, n + 1))

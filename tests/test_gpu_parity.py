@@ -1,9 +1,8 @@
 """GPU parity: every C-ABI operator vs the reference's golden vectors and the
 pinned oracle.  Bar: bit-exact for keys / indices / integer aggregates, and
-bit-exact for the fp64 fused-prediction paths too (same association order);
-groupby_sum_single uses device atomics, so its float sums are checked at the
-north_star tolerance (1e-5 relative) unless the inputs are exactly
-representable (then exact)."""
+bit-exact for the fp64 fused-prediction paths too (same association order),
+and for groupby_sum_single's fp64 sums (each group's terms summed in
+ascending R-row order, laqops.cpp:404-405)."""
 import numpy as np
 import pytest
 
@@ -123,7 +122,7 @@ def test_groupby(lib):
     e = OPS["groupby_single_example"]
     g, s = ops.groupby_sum_single(ia(e["kr"]), fa(e["vr"]), ia(e["ks"]), ia(e["gs"]))
     assert g.tolist() == [0, 1, 2] and s.tolist() == [1000.0, 10010.0, 100.0]
-    for c in OPS["groupby_single"]:  # quarter-integer values: exact in any order
+    for c in OPS["groupby_single"]:
         g, s = ops.groupby_sum_single(ia(c["kr"]), fa(c["vr"]), ia(c["ks"]), ia(c["gs"]))
         assert g.tolist() == c["groups"] and np.array_equal(s, fa(c["sums"]))
     for c in OPS["groupby_multi"]:  # row-order segmented sums: bit-exact
@@ -137,7 +136,9 @@ def test_groupby(lib):
     g, s = ops.groupby_sum_single(kr, vr, ks, gs)
     wg, ws = O.groupby_sum_single(kr, vr, ks, gs)
     assert np.array_equal(g, wg)
-    np.testing.assert_allclose(s, ws, rtol=1e-5, atol=1e-9)  # north_star float tolerance
+    assert np.array_equal(s, ws)  # R-row-ordered sums: bit-identical, run to run too
+    g2, s2 = ops.groupby_sum_single(kr, vr, ks, gs)
+    assert np.array_equal(s2, s)
 
 
 def _star(c):
