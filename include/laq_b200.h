@@ -66,6 +66,27 @@ int64_t laq_ctx_launch_count(const laq_ctx* ctx);
 /* Library build string (arch, version). */
 const char* laq_version(void);
 
+/* ---- row-sharded multi-GPU ---------------------------------
+ * The reference is single-process (proj/README.md:115); these entry points are
+ * the B200 build's own.  One process per GPU, each owning a contiguous row
+ * shard of the fact table (dimension tables replicated).  Once a context has a
+ * communicator, laq_run_query and laq_measure_selectivity sum their per-group
+ * (count, sum) accumulators across the ranks before emitting, so every rank
+ * returns the whole-table result; laq_allreduce_acc does the same for the
+ * prepared-plan path (laq_plan_execute on each shard, then all-reduce, then
+ * laq_plan_emit).  Integer accumulators: the merge is exact and order-free. */
+/* NCCL (loaded at run time from libnccl.so.2): rank 0 creates the id, the
+ * caller distributes its 128 bytes, every rank attaches. */
+int laq_nccl_unique_id(uint8_t h_id[128]);
+int laq_ctx_attach_nccl(laq_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t h_id[128]);
+/* Or any host-side transport: fn sums h_buf[0..count) in place across the
+ * ranks (called with the context's stream synchronised).  NULL detaches. */
+typedef int (*laq_allreduce_host_fn)(int64_t* h_buf, int64_t count, void* user);
+int laq_ctx_set_allreduce_host(laq_ctx* ctx, int32_t nranks, int32_t rank, laq_allreduce_host_fn fn, void* user);
+int laq_ctx_comm_info(const laq_ctx* ctx, int32_t* h_nranks, int32_t* h_rank);
+/* Sum d_acc[0..count) (int64, device) across the ranks on the context stream. */
+int laq_allreduce_acc(laq_ctx* ctx, int64_t* d_acc, int64_t count);
+
 /* ---- key encoding (laqops.hpp:54-78) ----------------------------------- */
 
 /* build_key_domain (laqops.cpp:142-155): ascending distinct union of keys_r and
@@ -274,6 +295,74 @@ int laq_groupby_sum_multi(laq_ctx* ctx, int32_t n_cols, const int64_t* const* d_
                           const double* d_vals, int64_t n, int64_t* d_out_keys, double* d_out_sums,
                           int64_t capacity, int64_t* h_n_groups);
 
+/* sort_rows (laqops.cpp:457-478): stable lexicographic sort of the rows of a
+ * row-major fp64 rows x cols matrix on h_key_cols (h_desc[k] != 0: descending),
+ * ties in the original row order, -0.0 == 0.0.  LAQ_ERR_INDEX on a bad key
+ * column. Synchronises. */
+int laq_sort_rows(laq_ctx* ctx, const double* d_t, int64_t rows, int64_t cols, const int64_t* h_key_cols,
+                  const int32_t* h_desc, int32_t n_keys, double* d_out);
+
+/* ---- sparse formats and SpGEMM (matrix.hpp:44-100) ------------------------ */
+
+/* check_canonical(SparseCoo) (matrix.cpp:243-255): in bounds, sorted by
+ * (row, col), no duplicates; LAQ_ERR_GENERIC with the reference's message for
+ * the first offending entry. Synchronises. */
+int laq_coo_check(laq_ctx* ctx, const int64_t* d_row_idx, const int64_t* d_col_idx, int64_t nnz, int64_t rows,
+                  int64_t cols);
+/* csr_from_coo (matrix.cpp:210-221): validates like laq_coo_check, then
+ * d_row_ptr (rows + 1); col_idx / values are the COO's unchanged. */
+int laq_csr_from_coo(laq_ctx* ctx, const int64_t* d_row_idx, const int64_t* d_col_idx, int64_t nnz, int64_t rows,
+                     int64_t cols, int64_t* d_row_ptr);
+/* coo_from_csr (matrix.cpp:198-208): the row index of every stored entry. */
+int laq_coo_from_csr(laq_ctx* ctx, const int64_t* d_row_ptr, int64_t rows, int64_t nnz, int64_t* d_row_idx);
+/* spmm (matrix.cpp:81-123): C = A B for canonical CSR operands, Gustavson
+ * semantics bit for bit: every (i, j) sums its products a(i,k) b(k,j) from 0.0
+ * in A-row then B-row order, exact zeros dropped, columns ascending.
+ * d_c_row_ptr has a_rows + 1 entries; if *h_nnz > capacity returns
+ * LAQ_ERR_CAPACITY (nothing written to d_c_col_idx / d_c_values).
+ * LAQ_ERR_SHAPE when a_cols != b_rows. Synchronises. */
+int laq_spmm(laq_ctx* ctx, const int64_t* d_a_row_ptr, const int64_t* d_a_col_idx, const double* d_a_values,
+             int64_t a_rows, int64_t a_cols, const int64_t* d_b_row_ptr, const int64_t* d_b_col_idx,
+             const double* d_b_values, int64_t b_rows, int64_t b_cols, int64_t* d_c_row_ptr, int64_t* d_c_col_idx,
+             double* d_c_values, int64_t capacity, int64_t* h_nnz);
+
+/* ---- selection (laqops.hpp:37-52; predicate.hpp:15-103) ------------------- */
+
+/* A typed Predicate (predicate.hpp:15-57): integer constants (ilo/ihi/iset) or
+ * float constants (flo/fhi/fset); sets are host arrays (any order). */
+typedef struct {
+  int32_t kind;     /* laq_pred_kind */
+  int32_t is_float;
+  int64_t ilo, ihi;
+  double flo, fhi;
+  const int64_t* iset;
+  const double* fset;
+  int64_t set_len;
+} laq_pred;
+/* build_selection_mask (laqops.cpp:65-79): d_mask[i] = pred.matches(col[i])
+ * (1/0), or AND-ed into d_mask when and_into != 0 (mask_and).  d_col is int64
+ * (col_is_float = 0) or double.  LAQ_ERR_TYPE on a typed mismatch (only for a
+ * non-empty column, as the reference throws from matches()). Synchronises. */
+int laq_selection_mask(laq_ctx* ctx, const void* d_col, int32_t col_is_float, int64_t n, const laq_pred* pred,
+                       uint8_t* d_mask, int32_t and_into);
+/* mask_and (laqops.cpp:87-93). */
+int laq_mask_and(laq_ctx* ctx, const uint8_t* d_a, const uint8_t* d_b, int64_t n, uint8_t* d_out);
+/* apply_mask's row selection (laqops.cpp:95-121): ascending positions of the
+ * set mask entries into d_idx (capacity n; NULL to count only). Synchronises. */
+int laq_mask_indices(laq_ctx* ctx, const uint8_t* d_mask, int64_t n, int64_t* d_idx, int64_t* h_count);
+/* Row gather d_dst[r] = d_src[d_idx[r]] (d_idx NULL: identity) over rows of
+ * row_elems elements: apply_mask for columns / DenseMat rows, the exact
+ * one-hot spmm_dense(I, to_matrix(col)) of run_query_laq (cli.cpp:96-101) and
+ * column_to_ints (cli.cpp:65-69).  src_kind 0 int32, 1 int64, 2 double;
+ * out_kind 1 int64 (copy; integer sources), 2 double ((double) v), 3 int64
+ * llround((double) v). */
+int laq_gather(laq_ctx* ctx, const void* d_src, int32_t src_kind, int64_t row_elems, const int64_t* d_idx, int64_t n,
+               void* d_dst, int32_t out_kind);
+/* dense_matmul(ones(1 x n), v) (cli.cpp:103-107): the sequential fp64 sum in
+ * row order (integral inputs whose partial sums stay below 2^53 are summed in
+ * parallel, exactly). Synchronises. */
+int laq_sum_f64(laq_ctx* ctx, const double* d_v, int64_t n, double* h_out);
+
 /* ---- ingest: the reference's CSV table format parsed on the device
  *      (load_csv storage.cpp:112-150; load_dataset cli.cpp:483-513) ---- */
 
@@ -420,7 +509,7 @@ int laq_run_query(laq_ctx* ctx, const laq_star* star, const laq_query_desc* q, d
 int laq_measure_selectivity(laq_ctx* ctx, const laq_star* star, const laq_query_desc* q,
                             double* h_out);
 
-/* ---- fusion cost model (fusion.hpp:56-76; fusion.cpp:259-302) ----------- */
+/* ---- fusion cost model (fusion.hpp:57-76; fusion.cpp:181-224) ----------- */
 int laq_speedup_ratio_linear(int64_t i, int64_t k, int64_t l, const int64_t* dim_rows,
                              int32_t n_dims, double* h_out);
 int laq_speedup_ratio_tree(int64_t i, int64_t k, int64_t l, int64_t p, const int64_t* dim_rows,

@@ -245,6 +245,20 @@ def gen_queries(star: RefStar, group: int, targets=()):
     return dials, real
 
 
+def cfg1_inputs(n_fact=1_000_000, dim_rows=10_000, k=16, l=1, seed=42):
+    """cfg1 inputs from the reference's own Rng / gen_linear (ref_cfg1_inputs)."""
+    fk = np.zeros(n_fact, np.int64)
+    pk = np.zeros(dim_rows, np.int64)
+    feats = np.zeros((dim_rows, k), np.float64)
+    W = np.zeros((k, l), np.float64)
+    L = lib()
+    L.ref_cfg1_inputs.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.c_void_p, C.c_void_p,
+                                  C.c_void_p, C.c_void_p]
+    _check(L.ref_cfg1_inputs(n_fact, dim_rows, k, l, seed, fk.ctypes.data, pk.ctypes.data, feats.ctypes.data,
+                             W.ctypes.data))
+    return fk, pk, feats, W
+
+
 def checksum_rows(m: np.ndarray) -> int:
     m = np.ascontiguousarray(m, dtype=np.float64)
     return int(lib().ref_checksum_rows(_pf(m), m.shape[0], m.shape[1] if m.ndim == 2 else 1))

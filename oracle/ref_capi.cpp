@@ -592,6 +592,26 @@ int ref_dense_matmul(const double* a, int64_t m, int64_t k, const double* b, int
 // multiway_star_join -> csr_from_coo -> prefuse_linear -> apply_fused_linear.
 // One dim per link, dim features B_j (r_j x k_j) placed contiguously.
 // seconds[0..3] = join, csr, prefuse, apply.
+// cfg1 inputs drawn with the REFERENCE's own Rng (rng.hpp) and
+// gen_linear (benchgen.cpp:512-518), for bench.py's reference arm: fk =
+// Rng(derive_seed(seed, "lineorder")).range(0, dim_rows) x n; pk = iota; k
+// unit() feature columns drawn column by column from derive_seed(seed, "dim")
+// (as make_dim draws features, benchgen.cpp:96-99), stored row-major; W =
+// gen_linear(k, l, 7) (row-major k x l).
+int ref_cfg1_inputs(int64_t n, int64_t dim_rows, int64_t k, int64_t l, uint64_t seed, int64_t* fk, int64_t* pk,
+                    double* feats, double* w) {
+  return guard([&] {
+    Rng rf(derive_seed(seed, "lineorder"));
+    for (int64_t i = 0; i < n; ++i) fk[i] = rf.range(0, dim_rows);
+    for (int64_t i = 0; i < dim_rows; ++i) pk[i] = i;
+    Rng rd(derive_seed(seed, "dim"));
+    for (int64_t c = 0; c < k; ++c)
+      for (int64_t r = 0; r < dim_rows; ++r) feats[r * k + c] = rd.unit();
+    const ml::LinearOperator op = bench::gen_linear(k, l, 7);
+    std::copy(op.mat.data().begin(), op.mat.data().end(), w);
+  });
+}
+
 int ref_fused_pipeline(int n_links, const int64_t* const* fks, int64_t n, const int64_t* const* pks,
                        const int64_t* pk_rows, const double* const* feats, const int64_t* kj,
                        const double* L, int64_t l, double* out_y, int64_t* nnz, double* seconds) {

@@ -29,6 +29,11 @@ class FilterDesc(C.Structure):
                 ("lo", i64), ("hi", i64), ("set", i64p), ("set_len", i64)]
 
 
+class PredDesc(C.Structure):
+    _fields_ = [("kind", i32), ("is_float", i32), ("ilo", i64), ("ihi", i64), ("flo", C.c_double),
+                ("fhi", C.c_double), ("iset", i64p), ("fset", f64p), ("set_len", i64)]
+
+
 class LinkDesc(C.Structure):
     _fields_ = [("fact_fk", C.c_char_p), ("dim_name", C.c_char_p), ("dim_pk", C.c_char_p)]
 
@@ -52,6 +57,11 @@ _SIGS = {
     "laq_ctx_last_error": (C.c_char_p, [vp]),
     "laq_ctx_launch_count": (i64, [vp]),
     "laq_version": (C.c_char_p, []),
+    "laq_nccl_unique_id": (C.c_int, [vp]),
+    "laq_ctx_attach_nccl": (C.c_int, [vp, i32, i32, vp]),
+    "laq_ctx_set_allreduce_host": (C.c_int, [vp, i32, i32, vp, vp]),
+    "laq_ctx_comm_info": (C.c_int, [vp, i32p, i32p]),
+    "laq_allreduce_acc": (C.c_int, [vp, vp, i64]),
     "laq_build_key_domain": (C.c_int, [vp, vp, i64, vp, i64, vp, i64p]),
     "laq_update_key_domain": (C.c_int, [vp, vp, i64, vp, i64, vp, i64p]),
     "laq_key_positions": (C.c_int, [vp, vp, i64, vp, i64, vp]),
@@ -82,6 +92,16 @@ _SIGS = {
     "laq_apply_fused_tree": (C.c_int, [vp, i32, vp, i64, vp, i64, f64p, i64p, vp, i64p, i32p]),
     "laq_groupby_sum_single": (C.c_int, [vp, vp, vp, i64, vp, vp, i64, vp, vp, i64p]),
     "laq_groupby_sum_multi": (C.c_int, [vp, i32, vp, vp, i64, vp, vp, i64, i64p]),
+    "laq_sort_rows": (C.c_int, [vp, vp, i64, i64, i64p, i32p, i32, vp]),
+    "laq_coo_check": (C.c_int, [vp, vp, vp, i64, i64, i64]),
+    "laq_csr_from_coo": (C.c_int, [vp, vp, vp, i64, i64, i64, vp]),
+    "laq_coo_from_csr": (C.c_int, [vp, vp, i64, i64, vp]),
+    "laq_spmm": (C.c_int, [vp, vp, vp, vp, i64, i64, vp, vp, vp, i64, i64, vp, vp, vp, i64, i64p]),
+    "laq_selection_mask": (C.c_int, [vp, vp, i32, i64, vp, vp, i32]),
+    "laq_mask_and": (C.c_int, [vp, vp, vp, i64, vp]),
+    "laq_mask_indices": (C.c_int, [vp, vp, i64, vp, i64p]),
+    "laq_gather": (C.c_int, [vp, vp, i32, i64, vp, i64, vp, i32]),
+    "laq_sum_f64": (C.c_int, [vp, vp, i64, f64p]),
     "laq_star_create": (C.c_int, [vp, C.POINTER(vp)]),
     "laq_star_destroy": (C.c_int, [vp]),
     "laq_star_add_table": (C.c_int, [vp, C.c_char_p, i32, i64, i32, vp, i32p, i32, vp]),
@@ -129,6 +149,10 @@ def lib():
             fn.argtypes = args
         _lib = L
     return _lib
+
+
+# laq_allreduce_host_fn: int (*)(int64_t* h_buf, int64_t count, void* user)
+ALLREDUCE_HOST_FN = C.CFUNCTYPE(C.c_int, i64p, i64, vp)
 
 
 def ptr_array(ptrs):

@@ -64,7 +64,7 @@ def build_cuda(force=False, verbose=False):
         from concurrent.futures import ThreadPoolExecutor
         with ThreadPoolExecutor(max_workers=max(1, os.cpu_count() or 1)) as ex:
             list(ex.map(_run, jobs))
-    _run([NVCC, *ARCH, "-shared", *objs, "-o", out, "-lcudart"])
+    _run([NVCC, *ARCH, "-shared", *objs, "-o", out, "-lcudart", "-ldl"])
     return out
 
 

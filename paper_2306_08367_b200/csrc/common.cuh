@@ -41,6 +41,14 @@ struct laq_ctx {
   int64_t* h_pinned = nullptr;
   // Device flag words (error flags, counters) reused by synchronous calls.
   int64_t* d_flags = nullptr;
+  // Row-sharded multi-GPU (comm.cu): an NCCL communicator over the
+  // ranks that each hold one fact shard, or a host all-reduce hook supplied by
+  // the caller (e.g. torch.distributed / MPI).  nranks == 1: single GPU.
+  void* nccl = nullptr;  // ncclComm_t
+  int32_t nranks = 1;
+  int32_t rank = 0;
+  laq_allreduce_host_fn hook = nullptr;
+  void* hook_user = nullptr;
 };
 
 namespace laq {
@@ -134,5 +142,9 @@ double absmax_f64(laq_ctx* ctx, const double* d, int64_t n);
 // Exclusive scan of int64 counts (in place allowed); returns total (synchronises
 // only when h_total != nullptr).
 void exclusive_scan_i64(laq_ctx* ctx, const int64_t* d_in, int64_t* d_out, int64_t n, int64_t* h_total);
+// Sum d_buf (count int64, on ctx->stream) across the context's ranks: NCCL when
+// a communicator is attached, else the host hook, else nothing (comm.cu).
+void allreduce_i64(laq_ctx* ctx, int64_t* d_buf, int64_t count);
+inline bool sharded(const laq_ctx* ctx) { return ctx->nranks > 1 || ctx->hook != nullptr; }
 
 }  // namespace laq

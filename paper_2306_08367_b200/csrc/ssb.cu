@@ -1308,6 +1308,7 @@ int laq_run_query(laq_ctx* ctx, const laq_star* s, const laq_query_desc* q, doub
     DevBuf<int64_t> acc(ctx, 2 * G);
     const int rc2 = laq_plan_execute(ctx, p, acc.get(), 0);
     if (rc2) fail(rc2, ctx->err);
+    allreduce_i64(ctx, acc.get(), 2 * G);  // row-sharded: whole-table groups on every rank
     std::vector<int64_t> h(2 * G);
     LAQ_CUDA(cudaMemcpyAsync(h.data(), acc.get(), 2 * G * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
     sync(ctx);
@@ -1331,9 +1332,19 @@ int laq_measure_selectivity(laq_ctx* ctx, const laq_star* s, const laq_query_des
     // prepare already built the code tables (pass fractions): scan only.
     const int rc2 = laq_plan_scan(ctx, p, ctx->d_flags + 32, 0);
     if (rc2) fail(rc2, ctx->err);
+    int64_t rows = p->fact_rows;
+    if (sharded(ctx)) {  // whole-table survivors / whole-table rows
+      ctx->h_pinned[1] = p->fact_rows;
+      LAQ_CUDA(cudaMemcpyAsync(ctx->d_flags + 33, ctx->h_pinned + 1, sizeof(int64_t), cudaMemcpyHostToDevice,
+                               ctx->stream));
+      allreduce_i64(ctx, ctx->d_flags + 32, 2);
+      LAQ_CUDA(cudaMemcpyAsync(ctx->h_pinned + 1, ctx->d_flags + 33, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+    }
     LAQ_CUDA(cudaMemcpyAsync(ctx->h_pinned, ctx->d_flags + 32, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
     sync(ctx);
-    *out = p->fact_rows == 0 ? 0.0 : static_cast<double>(ctx->h_pinned[0]) / static_cast<double>(p->fact_rows);
+    if (sharded(ctx)) rows = ctx->h_pinned[1];
+    *out = rows == 0 ? 0.0 : static_cast<double>(ctx->h_pinned[0]) / static_cast<double>(rows);
   });
   laq_plan_destroy(p);
   return rc;

@@ -149,6 +149,7 @@ int laq_ctx_destroy(laq_ctx* ctx) {
   if (!ctx) return LAQ_OK;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  laq_ctx_set_allreduce_host(ctx, 1, 0, nullptr, nullptr);  // releases an NCCL communicator
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
   if (ctx->d_flags) cudaFree(ctx->d_flags);
   delete ctx;
@@ -167,7 +168,7 @@ int laq_ctx_synchronize(laq_ctx* ctx) {
 const char* laq_ctx_last_error(const laq_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
 int64_t laq_ctx_launch_count(const laq_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
-// ---- cost model: fusion.cpp:259-302, verbatim formulas ----------------------
+// ---- cost model: fusion.cpp:181-224, verbatim formulas ----------------------
 static int cost_check(int64_t i, int64_t k, int64_t l, int64_t p, const int64_t* dims, int32_t n) {
   if (i <= 0 || k <= 0 || l <= 0 || p <= 0) return LAQ_ERR_DOMAIN;
   if (n <= 0) return LAQ_ERR_DOMAIN;
@@ -177,7 +178,7 @@ static int cost_check(int64_t i, int64_t k, int64_t l, int64_t p, const int64_t*
 }
 
 int laq_speedup_ratio_linear(int64_t i, int64_t k, int64_t l, const int64_t* dims, int32_t n, double* out) {
-  // CostInputs::tree_features is validated too (fusion.cpp:268); linear callers pass k.
+  // CostInputs::tree_features is validated too (fusion.cpp:189-197); linear callers pass k.
   const int rc = cost_check(i, k, l, k, dims, n);
   if (rc) return rc;
   double sum_r = 0;

@@ -41,6 +41,40 @@ class Context:
     def sync(self):
         self.check(self.lib.laq_ctx_synchronize(self.h))
 
+    # ---- row-sharded multi-GPU (laq_ctx_attach_nccl / laq_ctx_set_allreduce_host)
+    def attach_nccl(self, nranks: int, rank: int, uid: bytes):
+        """Attach an NCCL communicator (uid: 128 bytes from nccl_unique_id() on rank 0)."""
+        buf = (C.c_uint8 * 128).from_buffer_copy(bytes(uid))
+        self.check(self.lib.laq_ctx_attach_nccl(self.h, nranks, rank, buf))
+
+    def set_allreduce_host(self, nranks: int, rank: int, fn):
+        """fn(np.ndarray int64) sums the array in place across ranks (any host transport)."""
+        if fn is None:
+            self._hook = None
+            self.check(self.lib.laq_ctx_set_allreduce_host(self.h, 1, 0, None, None))
+            return
+
+        def tramp(buf, count, _user):
+            try:
+                fn(np.ctypeslib.as_array(buf, shape=(count,)))
+                return 0
+            except Exception:  # noqa: BLE001 - reported as a C status
+                return 1
+        self._hook = _abi.ALLREDUCE_HOST_FN(tramp)  # keep the thunk alive
+        self.check(self.lib.laq_ctx_set_allreduce_host(self.h, nranks, rank, self._hook, None))
+
+    @property
+    def comm(self) -> tuple[int, int]:
+        n, r = C.c_int32(), C.c_int32()
+        self.check(self.lib.laq_ctx_comm_info(self.h, C.byref(n), C.byref(r)))
+        return n.value, r.value
+
+    def allreduce_acc(self, acc: torch.Tensor):
+        """Sum an int64 device accumulator across the attached ranks (in place)."""
+        assert acc.dtype == torch.int64 and acc.is_cuda and acc.is_contiguous()
+        self.check(self.lib.laq_allreduce_acc(self.h, C.c_void_p(acc.data_ptr()), acc.numel()))
+        return acc
+
     @property
     def launches(self) -> int:
         return int(self.lib.laq_ctx_launch_count(self.h))
@@ -55,6 +89,14 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    rc = _abi.lib().laq_nccl_unique_id(buf)
+    if rc != 0:
+        errors.raise_for(rc, "laq_nccl_unique_id failed")
+    return bytes(buf)
 
 
 def context(device: int = 0) -> Context:

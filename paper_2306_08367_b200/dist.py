@@ -4,7 +4,11 @@ Fact rows are independent: rank r owns the contiguous row range
 shard_range(n, r, world); dimensions are replicated.  Query accumulators
 (int64 [G][count, sum]) are summed across ranks with one all-reduce; fused
 predictions stay row-sharded and their global order is the rank order.
-torch.distributed is the transport (NCCL on GPUs, gloo in the CPU tests).
+The product's own transport is the C-ABI communicator (laq_ctx_attach_nccl:
+NCCL loaded inside liblaq_b200.so, all-reduce enqueued on the context stream);
+attach() sets it up from an initialised torch.distributed group.  With a gloo
+group (CPU tests, several ranks sharing one GPU) the context gets a host
+all-reduce hook over that group instead.
 """
 from __future__ import annotations
 
@@ -16,6 +20,27 @@ def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
     if world < 1 or not 0 <= rank < world:
         raise ValueError("bad rank/world")
     return n * rank // world, n * (rank + 1) // world
+
+
+def attach(ctx, group=None):
+    """Give a device.Context the ranks of an initialised torch.distributed group:
+    NCCL inside the C-ABI when the group's backend is nccl, else a host
+    all-reduce hook over the group (gloo)."""
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    if world == 1:
+        return ctx
+    if dist.get_backend(group) == "nccl":
+        from .device import nccl_unique_id
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        ctx.attach_nccl(world, rank, obj[0])
+    else:
+        def hook(buf):
+            t = torch.from_numpy(buf)  # shares memory with the C buffer
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        ctx.set_allreduce_host(world, rank, hook)
+    return ctx
 
 
 def allreduce_acc(acc: torch.Tensor, group=None) -> torch.Tensor:
