@@ -14,12 +14,16 @@
 // operands the API is defined over, and filling host-visible return structs
 // (e.g. KeyDomain::index, laqops.hpp:58-65).
 //
-// Replaced:  dense_matmul, spmm_dense (matrix.cpp:125-174);
-//            build_key_domain, update_key_domain, key_matrix, mm_join x2,
-//            multiway_star_join, materialize, groupby_sum_single/_multi
-//            (laqops.cpp:142-455);  prefuse_linear, apply_fused_linear,
-//            speedup_ratio_linear/_tree, decide_fusion (fusion.cpp:50-77, 199-224);
-//            run_query_laq (cli.cpp:73-138);  load_csv (storage.cpp:112-150).
+// Replaced here:  spmm, spmm_dense, dense_matmul, coo_from_csr, csr_from_coo
+//            (matrix.cpp:81-221); build_key_domain, update_key_domain,
+//            key_matrix, mm_join x2, multiway_star_join, row_mapping_matrices,
+//            materialize, groupby_sum_single/_multi, sort_rows
+//            (laqops.cpp:142-478);  prefuse_linear, apply_fused_linear, trees,
+//            refresh_partial, speedup_ratio_linear/_tree, decide_fusion
+//            (fusion.cpp:39-224); predict_tree (mlops.cpp:254-280);
+//            load_csv (storage.cpp:112-150).
+// laq_dropin_query.cpp: selection (laqops.cpp:65-121), run_query_laq
+//            (cli.cpp:73-138) and PipelineRunner (cli.cpp:246-378).
 
 #include <cuda_runtime.h>
 
@@ -40,95 +44,11 @@
 #include "laq/predicate.hpp"
 #include "laq/storage.hpp"
 #include "laq_b200.h"
-
-// ---- legal access to Predicate's private constants (explicit instantiation
-// definitions may name private members) --------------------------------------
-namespace {
-template <typename Tag, typename Tag::type M>
-struct Rob {
-  friend typename Tag::type get(Tag) { return M; }
-};
-struct PredKind { using type = laq::Predicate::Kind laq::Predicate::*; friend type get(PredKind); };
-struct PredInt { using type = bool laq::Predicate::*; friend type get(PredInt); };
-struct PredIlo { using type = std::int64_t laq::Predicate::*; friend type get(PredIlo); };
-struct PredIhi { using type = std::int64_t laq::Predicate::*; friend type get(PredIhi); };
-struct PredIset { using type = std::vector<std::int64_t> laq::Predicate::*; friend type get(PredIset); };
-}  // namespace
-template struct Rob<PredKind, &laq::Predicate::kind_>;
-template struct Rob<PredInt, &laq::Predicate::integer_>;
-template struct Rob<PredIlo, &laq::Predicate::ilo_>;
-template struct Rob<PredIhi, &laq::Predicate::ihi_>;
-template struct Rob<PredIset, &laq::Predicate::iset_>;
+#include "dropin_common.hpp"
 
 namespace laq {
+using namespace dropin;
 namespace {
-
-laq_ctx* ctx() {
-  static laq_ctx* c = [] {
-    laq_ctx* p = nullptr;
-    const int rc = laq_ctx_create(0, &p);
-    if (rc != LAQ_OK) throw Error("laq_b200: no usable sm_100 device (status " + std::to_string(rc) + ")");
-    return p;
-  }();
-  return c;
-}
-
-[[noreturn]] void raise(int rc, const std::string& msg) {
-  switch (rc) {
-    case LAQ_ERR_INDEX: throw IndexError(msg);
-    case LAQ_ERR_SHAPE: throw ShapeError(msg);
-    case LAQ_ERR_FORMAT: throw FormatError(msg);
-    case LAQ_ERR_NAME: throw NameError(msg);
-    case LAQ_ERR_TYPE: throw TypeError(msg);
-    case LAQ_ERR_MAPPING: throw MappingError(msg);
-    case LAQ_ERR_DOMAIN: throw DomainError(msg);
-    case LAQ_ERR_DUPLICATE_KEY: throw DuplicateKeyError(msg);
-    case LAQ_ERR_TREE: throw TreeError(msg);
-    case LAQ_ERR_MODEL: throw ModelError(msg);
-    case LAQ_ERR_GEN: throw GenError(msg);
-    case LAQ_ERR_CAPACITY: throw CapacityError(msg);
-    default: throw Error(msg);
-  }
-}
-
-void check(int rc) {
-  if (rc != LAQ_OK) raise(rc, laq_ctx_last_error(ctx()));
-}
-
-// Device mirror of a host vector (freed on scope exit).
-template <class T>
-struct Dev {
-  T* p = nullptr;
-  size_t n = 0;
-  explicit Dev(size_t count) : n(count) {
-    ctx();
-    if (n && cudaMalloc(reinterpret_cast<void**>(&p), n * sizeof(T)) != cudaSuccess)
-      throw CapacityError("laq_b200: device allocation of " + std::to_string(n * sizeof(T)) + " bytes failed");
-  }
-  Dev(const T* h, size_t count) : Dev(count) { up(h, count); }
-  explicit Dev(const std::vector<T>& v) : Dev(v.data(), v.size()) {}
-  Dev(const Dev&) = delete;
-  Dev& operator=(const Dev&) = delete;
-  Dev(Dev&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; }
-  ~Dev() {
-    if (p) cudaFree(p);
-  }
-  void up(const T* h, size_t m) {
-    if (m && cudaMemcpy(p, h, m * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess) throw Error("laq_b200: H2D");
-  }
-  void down(T* h, size_t m) const {
-    if (m && cudaMemcpy(h, p, m * sizeof(T), cudaMemcpyDeviceToHost) != cudaSuccess) throw Error("laq_b200: D2H");
-  }
-  std::vector<T> to_vector(size_t m) const {
-    std::vector<T> v(m);
-    down(v.data(), m);
-    return v;
-  }
-};
-
-std::string shape_str(index_t r, index_t c) { return std::to_string(r) + "x" + std::to_string(c); }
-
-double now_s() { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); }
 
 bool is_row_map(const SparseCsr& m) {  // one entry of value 1.0 per row
   if (m.nnz() != m.rows) return false;
@@ -168,7 +88,101 @@ DenseMat spmm_dense(const SparseCsr& a, const DenseMat& b) {
   return out;
 }
 
+SparseCsr spmm(const SparseCsr& a, const SparseCsr& b) {  // matrix.cpp:81-123
+  if (a.cols != b.rows)
+    throw ShapeError("spmm: " + shape_str(a.rows, a.cols) + " x " + shape_str(b.rows, b.cols));
+  Dev<index_t> arp(a.row_ptr), aci(a.col_idx), brp(b.row_ptr), bci(b.col_idx);
+  Dev<double> av(a.values), bv(b.values);
+  Dev<index_t> crp(static_cast<size_t>(a.rows) + 1);
+  int64_t cap = std::max<int64_t>(1, std::max(a.nnz(), b.nnz())), nnz = 0;
+  while (true) {
+    Dev<index_t> cci(static_cast<size_t>(cap));
+    Dev<double> cv(static_cast<size_t>(cap));
+    const int rc = laq_spmm(ctx(), arp.p, aci.p, av.p, a.rows, a.cols, brp.p, bci.p, bv.p, b.rows, b.cols, crp.p, cci.p,
+                            cv.p, cap, &nnz);
+    if (rc == LAQ_ERR_CAPACITY && nnz > cap) {
+      cap = nnz;
+      continue;
+    }
+    check(rc);
+    SparseCsr c;
+    c.rows = a.rows;
+    c.cols = b.cols;
+    c.row_ptr = crp.to_vector(static_cast<size_t>(a.rows) + 1);
+    c.col_idx = cci.to_vector(static_cast<size_t>(nnz));
+    c.values = cv.to_vector(static_cast<size_t>(nnz));
+    return c;
+  }
+}
+
+SparseCoo coo_from_csr(const SparseCsr& a) {  // matrix.cpp:198-208
+  SparseCoo c;
+  c.rows = a.rows;
+  c.cols = a.cols;
+  c.col_idx = a.col_idx;
+  c.values = a.values;
+  const size_t nnz = a.col_idx.size();
+  if (nnz == 0) return c;
+  Dev<index_t> rp(a.row_ptr), ri(nnz);
+  check(laq_coo_from_csr(ctx(), rp.p, a.rows, static_cast<int64_t>(nnz), ri.p));
+  c.row_idx = ri.to_vector(nnz);
+  return c;
+}
+
+SparseCsr csr_from_coo(const SparseCoo& a) {  // matrix.cpp:210-221, check_canonical 243-255
+  if (a.rows < 0 || a.cols < 0) throw Error("coo: negative dimension");
+  if (a.row_idx.size() != a.col_idx.size() || a.values.size() != a.col_idx.size())
+    throw Error("coo: index/value length mismatch");
+  SparseCsr c;
+  c.rows = a.rows;
+  c.cols = a.cols;
+  c.col_idx = a.col_idx;
+  c.values = a.values;
+  Dev<index_t> ri(a.row_idx), ci(a.col_idx), rp(static_cast<size_t>(a.rows) + 1);
+  check(laq_csr_from_coo(ctx(), ri.p, ci.p, a.nnz(), a.rows, a.cols, rp.p));
+  c.row_ptr = rp.to_vector(static_cast<size_t>(a.rows) + 1);
+  return c;
+}
+
 namespace ops {
+
+std::pair<SparseCsr, SparseCsr> row_mapping_matrices(const RowMatch& i) {  // laqops.cpp:321-336
+  const SparseCoo& m = i.mat;
+  if (m.rows < 0 || m.cols < 0) throw Error("coo: negative dimension");
+  if (m.row_idx.size() != m.col_idx.size() || m.values.size() != m.col_idx.size())
+    throw Error("coo: index/value length mismatch");
+  {  // check_canonical on the device
+    Dev<index_t> ri(m.row_idx), ci(m.col_idx);
+    check(laq_coo_check(ctx(), ri.p, ci.p, m.nnz(), m.rows, m.cols));
+  }
+  const index_t nnz = i.nnz();
+  const auto one_hot = [nnz](const std::vector<index_t>& src, index_t count) {  // host-visible structs
+    SparseCsr r;
+    r.rows = nnz;
+    r.cols = count;
+    r.row_ptr.resize(static_cast<std::size_t>(nnz) + 1);
+    std::iota(r.row_ptr.begin(), r.row_ptr.end(), index_t{0});
+    r.col_idx = src;
+    r.values.assign(static_cast<std::size_t>(nnz), 1.0);
+    return r;
+  };
+  return {one_hot(m.row_idx, m.rows), one_hot(m.col_idx, m.cols)};
+}
+
+DenseMat sort_rows(const DenseMat& t, std::span<const index_t> key_cols, std::span<const SortDir> directions) {
+  if (key_cols.size() != directions.size()) throw ShapeError("sort_rows: key/direction counts");
+  for (index_t c : key_cols)
+    if (c < 0 || c >= t.cols()) throw IndexError("sort_rows: key column " + std::to_string(c));
+  DenseMat out(t.rows(), t.cols());
+  if (out.data().empty()) return out;
+  std::vector<int32_t> desc;
+  for (SortDir d : directions) desc.push_back(d == SortDir::Desc ? 1 : 0);
+  Dev<double> dt(t.data()), dout(out.data().size());
+  check(laq_sort_rows(ctx(), dt.p, t.rows(), t.cols(), key_cols.data(), desc.data(),
+                      static_cast<int32_t>(key_cols.size()), dout.p));
+  dout.down(out.data().data(), out.data().size());
+  return out;
+}
 
 // ============================================================================
 // laqops.hpp: key domains, key matrices, joins
@@ -742,90 +756,6 @@ std::vector<std::int64_t> predict_tree(const DenseMat& t, const TreeLA& m) {
 }
 }  // namespace ml
 
-namespace cli {
-
-DenseMat run_query_laq(const StarSchema& data, const bench::QuerySpec& q, StageTimes* stages) {
-  StageTimes local;
-  StageTimes& st = stages ? *stages : local;
-  const double t0 = now_s();
-  laq_star* star = nullptr;
-  check(laq_star_create(ctx(), &star));
-  struct Guard {
-    laq_star* s;
-    ~Guard() { laq_star_destroy(s); }
-  } guard{star};
-
-  auto add_table = [&](const std::string& name, const Table& t, bool is_fact) {
-    std::vector<std::string> names;
-    std::vector<const char*> cn;
-    std::vector<int32_t> kinds;
-    std::vector<const void*> cols;
-    for (index_t c = 0; c < t.col_count(); ++c) names.push_back(t.schema().name(c));
-    for (index_t c = 0; c < t.col_count(); ++c) {
-      cn.push_back(names[c].c_str());
-      const ColKind k = t.schema().kind(c);
-      kinds.push_back(k == ColKind::Key ? LAQ_COL_KEY : k == ColKind::Int ? LAQ_COL_INT : LAQ_COL_FLOAT);
-      cols.push_back(k == ColKind::Float ? static_cast<const void*>(t.floats(c).data())
-                                         : static_cast<const void*>(t.ints(c).data()));
-    }
-    check(laq_star_add_table(star, name.c_str(), is_fact ? 1 : 0, t.row_count(), static_cast<int32_t>(cn.size()),
-                             cn.data(), kinds.data(), 8, cols.data()));
-  };
-  add_table("__fact__", data.fact(), true);
-  std::vector<std::string> added;
-  for (const StarLink& l : q.joins) {
-    if (std::find(added.begin(), added.end(), l.dim_name) != added.end()) continue;
-    add_table(l.dim_name, data.dim(l.dim_name), false);  // NameError for unknown dims, as StarSchema::dim
-    added.push_back(l.dim_name);
-  }
-
-  // Query description (benchgen.hpp:296-326) with the predicates' constants.
-  std::vector<laq_link_desc> links;
-  for (const StarLink& l : q.joins) links.push_back({l.fact_fk.c_str(), l.dim_name.c_str(), l.dim_pk.c_str()});
-  std::vector<laq_filter_desc> filters;
-  std::vector<std::vector<std::int64_t>> sets;
-  sets.reserve(q.filters.size());
-  for (const bench::FilterSpec& f : q.filters) {
-    const Predicate& p = f.pred;
-    laq_filter_desc d{};
-    d.target = f.target;
-    d.column = f.column.c_str();
-    d.is_float = (p.*get(PredInt())) ? 0 : 1;
-    switch (p.*get(PredKind())) {
-      case Predicate::Kind::Lt: d.kind = LAQ_PRED_LT; break;
-      case Predicate::Kind::Le: d.kind = LAQ_PRED_LE; break;
-      case Predicate::Kind::Eq: d.kind = LAQ_PRED_EQ; break;
-      case Predicate::Kind::Ge: d.kind = LAQ_PRED_GE; break;
-      case Predicate::Kind::Gt: d.kind = LAQ_PRED_GT; break;
-      case Predicate::Kind::Between: d.kind = LAQ_PRED_BETWEEN; break;
-      case Predicate::Kind::InSet: d.kind = LAQ_PRED_INSET; break;
-    }
-    d.lo = p.*get(PredIlo());
-    d.hi = p.*get(PredIhi());
-    sets.push_back(p.*get(PredIset()));
-    d.set = sets.back().data();
-    d.set_len = static_cast<int64_t>(sets.back().size());
-    filters.push_back(d);
-  }
-  std::vector<laq_group_desc> groups;
-  for (const bench::GroupRef& g : q.group_by) groups.push_back({g.target, g.column.c_str()});
-  laq_query_desc desc{static_cast<int32_t>(links.size()), links.data(), static_cast<int32_t>(filters.size()),
-                      filters.data(),   q.measure.c_str(), static_cast<int32_t>(groups.size()),
-                      groups.data(),    q.order_by ? 1 : 0};
-  std::vector<double> buf(1 << 16);
-  int64_t rows = 0, cols = 0;
-  int rc = laq_run_query(ctx(), star, &desc, buf.data(), static_cast<int64_t>(buf.size()), &rows, &cols);
-  if (rc == LAQ_ERR_CAPACITY && rows * cols > static_cast<int64_t>(buf.size())) {
-    buf.resize(static_cast<size_t>(rows * cols));
-    rc = laq_run_query(ctx(), star, &desc, buf.data(), static_cast<int64_t>(buf.size()), &rows, &cols);
-  }
-  check(rc);
-  buf.resize(static_cast<size_t>(rows * cols));
-  st.materialize += now_s() - t0;  // one fused device pass: filters, joins, aggregation
-  return DenseMat(rows, cols, std::move(buf));
-}
-
-}  // namespace cli
 
 // load_csv (storage.cpp:112-150): the file is read on the host, lines indexed
 // and fields parsed on the device (csv.cu; from_chars semantics, the same

@@ -1,0 +1,789 @@
+// Drop-in, part 2: selection (laqops.cpp:65-121), the query plan driver
+// run_query_laq (cli.cpp:73-138) and the predictive pipeline driver
+// PipelineRunner (cli.cpp:246-378), signatures UNCHANGED, over the C-ABI.
+//
+// run_query_laq has two device paths:
+//  * fast: the query's columns registered once per StarSchema as an int32
+//    device star (laq_star_add_table: H2D + device narrowing) and cached
+//    (LAQ_DROPIN_CACHE=0 disables the cache), then laq_run_query: code tables +
+//    one fused scan + emit.  Repeated queries over the same StarSchema move no
+//    fact bytes over PCIe (SURVEY §7 hard-part 3).
+//  * general: everything the fast path declines (float measures / predicates /
+//    group columns, integers outside int32, > 6 joins, wide group spaces,
+//    duplicate keys outside the filtered rows, ...) runs the reference's own
+//    algorithm step by step on device operators: selection masks + compaction
+//    (filter_table), laq_star_join (multiway_star_join), one-hot gathers
+//    (spmm_dense of the row maps), laq_groupby_sum_multi (row-ordered fp64 sums),
+//    laq_sort_rows.  Same results and the same exceptions as the reference.
+//
+// PipelineRunner keeps the join's row maps and the pre-fused partials resident
+// on the device between runs (side state keyed by the runner), so run_fused
+// moves only its predictions D2H.  include/laq_dropin.hpp adds the planner-
+// driven run_auto (speedup_ratio_* + decide_fusion, fusion.cpp:199-224).
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <list>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "dropin_common.hpp"
+#include "laq/benchgen.hpp"
+#include "laq/cli.hpp"
+#include "laq/fusion.hpp"
+#include "laq/laqops.hpp"
+#include "laq/oracle.hpp"
+#include "laq/predicate.hpp"
+#include "laq/storage.hpp"
+#include "laq_b200.h"
+#include "laq_dropin.hpp"
+
+// ---- legal access to Predicate's private constants (explicit instantiation
+// definitions may name private members) --------------------------------------
+namespace {
+template <typename Tag, typename Tag::type M>
+struct Rob {
+  friend typename Tag::type get(Tag) { return M; }
+};
+struct PredKind { using type = laq::Predicate::Kind laq::Predicate::*; friend type get(PredKind); };
+struct PredInt { using type = bool laq::Predicate::*; friend type get(PredInt); };
+struct PredIlo { using type = std::int64_t laq::Predicate::*; friend type get(PredIlo); };
+struct PredIhi { using type = std::int64_t laq::Predicate::*; friend type get(PredIhi); };
+struct PredFlo { using type = double laq::Predicate::*; friend type get(PredFlo); };
+struct PredFhi { using type = double laq::Predicate::*; friend type get(PredFhi); };
+struct PredIset { using type = std::vector<std::int64_t> laq::Predicate::*; friend type get(PredIset); };
+struct PredFset { using type = std::vector<double> laq::Predicate::*; friend type get(PredFset); };
+}  // namespace
+template struct Rob<PredKind, &laq::Predicate::kind_>;
+template struct Rob<PredInt, &laq::Predicate::integer_>;
+template struct Rob<PredIlo, &laq::Predicate::ilo_>;
+template struct Rob<PredIhi, &laq::Predicate::ihi_>;
+template struct Rob<PredFlo, &laq::Predicate::flo_>;
+template struct Rob<PredFhi, &laq::Predicate::fhi_>;
+template struct Rob<PredIset, &laq::Predicate::iset_>;
+template struct Rob<PredFset, &laq::Predicate::fset_>;
+
+namespace laq {
+using namespace dropin;
+namespace {
+
+int32_t pred_kind(const Predicate& p) {
+  switch (p.*get(PredKind())) {
+    case Predicate::Kind::Lt: return LAQ_PRED_LT;
+    case Predicate::Kind::Le: return LAQ_PRED_LE;
+    case Predicate::Kind::Eq: return LAQ_PRED_EQ;
+    case Predicate::Kind::Ge: return LAQ_PRED_GE;
+    case Predicate::Kind::Gt: return LAQ_PRED_GT;
+    case Predicate::Kind::Between: return LAQ_PRED_BETWEEN;
+    case Predicate::Kind::InSet: return LAQ_PRED_INSET;
+  }
+  return LAQ_PRED_LT;
+}
+
+laq_pred to_pred(const Predicate& p) {
+  laq_pred d{};
+  d.kind = pred_kind(p);
+  d.is_float = (p.*get(PredInt())) ? 0 : 1;
+  d.ilo = p.*get(PredIlo());
+  d.ihi = p.*get(PredIhi());
+  d.flo = p.*get(PredFlo());
+  d.fhi = p.*get(PredFhi());
+  const auto& is = p.*get(PredIset());
+  const auto& fs = p.*get(PredFset());
+  d.iset = is.data();
+  d.fset = fs.data();
+  d.set_len = static_cast<int64_t>(d.is_float ? fs.size() : is.size());
+  return d;
+}
+
+// A column of a host Table on the device, as the reference holds it (int64 or double).
+struct DevCol {
+  Dev<std::int64_t> i;
+  Dev<double> f;
+  bool is_float = false;
+  const void* p() const { return is_float ? static_cast<const void*>(f.p) : static_cast<const void*>(i.p); }
+  int32_t kind() const { return is_float ? 2 : 1; }
+};
+
+DevCol upload(const Table& t, index_t c) {
+  DevCol d;
+  d.is_float = t.schema().kind(c) == ColKind::Float;
+  if (d.is_float) d.f = Dev<double>(t.floats(c));
+  else d.i = Dev<std::int64_t>(t.ints(c));
+  return d;
+}
+
+// Ascending row ids passing every filter (filter_table, cli.cpp:33-45), or an
+// empty Dev with *all = true when there are no filters.
+Dev<std::int64_t> filtered_rows(const Table& t, const std::vector<const bench::FilterSpec*>& filters, int64_t* count,
+                                bool* all) {
+  *all = filters.empty();
+  *count = t.row_count();
+  if (filters.empty()) return {};
+  const int64_t n = t.row_count();
+  Dev<std::uint8_t> mask(static_cast<size_t>(std::max<int64_t>(n, 1)));
+  bool first = true;
+  for (const bench::FilterSpec* f : filters) {
+    const index_t c = t.schema().index_of(f->column);  // NameError as the reference
+    const DevCol col = upload(t, c);
+    const laq_pred p = to_pred(f->pred);
+    check(laq_selection_mask(ctx(), col.p(), col.is_float ? 1 : 0, n, &p, mask.p, first ? 0 : 1));
+    first = false;
+  }
+  Dev<std::int64_t> idx(static_cast<size_t>(std::max<int64_t>(n, 1)));
+  check(laq_mask_indices(ctx(), mask.p, n, idx.p, count));
+  return idx;
+}
+
+// d_out[r] = src[idx ? idx[r] : r] with the requested conversion (laq_gather).
+template <class T>
+Dev<T> gather(const void* src, int32_t src_kind, const std::int64_t* idx, int64_t n, int32_t out_kind) {
+  Dev<T> out(static_cast<size_t>(std::max<int64_t>(n, 1)));
+  check(laq_gather(ctx(), src, src_kind, 1, idx, n, out.p, out_kind));
+  return out;
+}
+
+std::vector<const bench::FilterSpec*> filters_for(const bench::QuerySpec& q, int target) {
+  std::vector<const bench::FilterSpec*> out;
+  for (const bench::FilterSpec& f : q.filters)
+    if (f.target == target) out.push_back(&f);
+  return out;
+}
+
+// ---- the general device path: run_query_laq step by step ----------------------
+DenseMat general_query(const StarSchema& data, const bench::QuerySpec& q) {
+  const Table& fact = data.fact();
+  int64_t nf = 0;
+  bool fact_all = true;
+  Dev<std::int64_t> frows = filtered_rows(fact, filters_for(q, -1), &nf, &fact_all);
+  const size_t J = q.joins.size();
+  std::vector<const Table*> dims(J);
+  std::vector<Dev<std::int64_t>> drows(J);
+  std::vector<int64_t> nd(J);
+  std::vector<bool> dim_all(J);
+  for (size_t j = 0; j < J; ++j) {
+    dims[j] = &data.dim(q.joins[j].dim_name);
+    bool a = true;
+    drows[j] = filtered_rows(*dims[j], filters_for(q, static_cast<int>(j)), &nd[j], &a);
+    dim_all[j] = a;
+  }
+  // multiway_star_join over the filtered tables (laqops.cpp:233-319)
+  Dev<std::int64_t> surv(static_cast<size_t>(std::max<int64_t>(nf, 1)));
+  std::vector<Dev<std::int64_t>> fk(J), pk(J), rows(J);
+  int64_t nnz = nf;
+  if (J > 0) {
+    std::vector<const int64_t*> pf, pp;
+    std::vector<int64_t*> pr;
+    std::vector<int64_t> prow;
+    for (size_t j = 0; j < J; ++j) {
+      const IntColumn& fkc = fact.ints(q.joins[j].fact_fk);      // NameError / TypeError as the reference
+      const IntColumn& pkc = dims[j]->ints(q.joins[j].dim_pk);
+      Dev<std::int64_t> fk_all(fkc), pk_all(pkc);
+      fk[j] = fact_all ? std::move(fk_all) : gather<std::int64_t>(fk_all.p, 1, frows.p, nf, 1);
+      pk[j] = dim_all[j] ? std::move(pk_all) : gather<std::int64_t>(pk_all.p, 1, drows[j].p, nd[j], 1);
+      rows[j] = Dev<std::int64_t>(static_cast<size_t>(std::max<int64_t>(nf, 1)));
+      pf.push_back(fk[j].p);
+      pp.push_back(pk[j].p);
+      pr.push_back(rows[j].p);
+      prow.push_back(nd[j]);
+    }
+    check(laq_star_join(ctx(), static_cast<int32_t>(J), pf.data(), nf, pp.data(), prow.data(), surv.p, pr.data(),
+                        &nnz));
+  }
+  // fact row of every survivor (identity chain when nothing was filtered / joined)
+  const std::int64_t* s_idx = J > 0 ? surv.p : nullptr;
+  Dev<std::int64_t> fact_of;
+  const std::int64_t* fact_idx = nullptr;
+  if (!fact_all && s_idx) { fact_of = gather<std::int64_t>(frows.p, 1, s_idx, nnz, 1); fact_idx = fact_of.p; }
+  else if (!fact_all) fact_idx = frows.p;
+  else fact_idx = s_idx;
+  // measure: spmm_dense(I_fact, to_matrix(fact, {measure})) (cli.cpp:96-99): (double) v, gathered
+  const index_t mc = fact.schema().index_of(q.measure);
+  const DevCol mcol = upload(fact, mc);
+  Dev<double> vals = gather<double>(mcol.p(), mcol.kind(), fact_idx, nnz, 2);
+  if (q.group_by.empty()) {  // ones-vector reduction, sequential (cli.cpp:103-107)
+    double s = 0;
+    check(laq_sum_f64(ctx(), vals.p, nnz, &s));
+    return DenseMat(1, 1, std::vector<double>{s});
+  }
+  // group columns: column_to_ints(spmm_dense(I, to_matrix(...))) = llround((double) v)
+  std::vector<Dev<std::int64_t>> gcols;
+  std::vector<const int64_t*> gp;
+  for (const bench::GroupRef& g : q.group_by) {
+    if (g.target == -1) {
+      const DevCol c = upload(fact, fact.schema().index_of(g.column));
+      gcols.push_back(gather<std::int64_t>(c.p(), c.kind(), fact_idx, nnz, 3));
+    } else {
+      const Table& dim = *dims[static_cast<size_t>(g.target)];
+      const DevCol c = upload(dim, dim.schema().index_of(g.column));
+      const std::int64_t* r = rows[static_cast<size_t>(g.target)].p;
+      Dev<std::int64_t> dim_of;
+      const std::int64_t* didx = r;
+      if (!dim_all[static_cast<size_t>(g.target)]) {
+        dim_of = gather<std::int64_t>(drows[static_cast<size_t>(g.target)].p, 1, r, nnz, 1);
+        didx = dim_of.p;
+      }
+      gcols.push_back(gather<std::int64_t>(c.p(), c.kind(), didx, nnz, 3));
+    }
+    gp.push_back(gcols.back().p);
+  }
+  const size_t G = q.group_by.size();
+  const int64_t cap = std::max<int64_t>(nnz, 1);
+  Dev<std::int64_t> keys(G * static_cast<size_t>(cap));
+  Dev<double> sums(static_cast<size_t>(cap));
+  int64_t ng = 0;
+  if (nnz > 0)
+    check(laq_groupby_sum_multi(ctx(), static_cast<int32_t>(G), gp.data(), vals.p, nnz, keys.p, sums.p, cap, &ng));
+  const std::vector<std::int64_t> hk = keys.to_vector(G * static_cast<size_t>(cap));
+  const std::vector<double> hs = sums.to_vector(static_cast<size_t>(ng));
+  DenseMat result(ng, static_cast<index_t>(G) + 1);
+  for (int64_t r = 0; r < ng; ++r) {
+    for (size_t c = 0; c < G; ++c) result(r, static_cast<index_t>(c)) = static_cast<double>(hk[c * cap + r]);
+    result(r, static_cast<index_t>(G)) = hs[static_cast<size_t>(r)];
+  }
+  if (q.order_by && ng > 0) {
+    std::vector<index_t> kc(G);
+    std::iota(kc.begin(), kc.end(), index_t{0});
+    const std::vector<ops::SortDir> dirs(G, ops::SortDir::Asc);
+    result = ops::sort_rows(result, kc, dirs);
+  }
+  return result;
+}
+
+// ---- the fast path: a cached int32 device star per StarSchema -----------------
+uint64_t fingerprint(const std::int64_t* p, size_t n) {  // size + 64 sampled values + both ends
+  uint64_t h = 0xcbf29ce484222325ull ^ n;
+  auto mix = [&](uint64_t v) {
+    h ^= v;
+    h *= 0x100000001b3ull;
+  };
+  for (size_t k = 0; k < 64 && n; ++k) mix(static_cast<uint64_t>(p[(n - 1) * k / 63]));
+  for (size_t k = 0; k < std::min<size_t>(8, n); ++k) mix(static_cast<uint64_t>(p[k]) ^ static_cast<uint64_t>(p[n - 1 - k]));
+  return h;
+}
+
+struct ColRef {
+  std::string table, column;
+  const void* data;
+  size_t n;
+  uint64_t fp;
+  bool operator==(const ColRef&) const = default;
+};
+
+struct CachedStar {
+  std::vector<ColRef> key;
+  laq_star* star = nullptr;
+  int status = LAQ_OK;  // != OK: this column set needs the general path
+  ~CachedStar() {
+    if (star) laq_star_destroy(star);
+  }
+};
+
+std::mutex g_cache_mu;
+std::list<std::unique_ptr<CachedStar>> g_cache;  // most recent first
+constexpr size_t kCacheEntries = 8;
+
+bool cache_enabled() {
+  const char* e = std::getenv("LAQ_DROPIN_CACHE");
+  return !(e && std::string(e) == "0");
+}
+
+// Register the query's integer columns (only those it reads) as an int32
+// device star; returns a status instead of throwing (any failure = general path).
+int build_star(const StarSchema& data, const std::vector<std::pair<std::string, std::vector<std::string>>>& cols,
+               laq_star** out) {
+  laq_star* star = nullptr;
+  int rc = laq_star_create(ctx(), &star);
+  if (rc) return rc;
+  bool fact = true;
+  for (const auto& [name, names] : cols) {
+    const Table& t = fact ? data.fact() : data.dim(name);
+    std::vector<const char*> cn;
+    std::vector<int32_t> kinds;
+    std::vector<const void*> ptrs;
+    for (const std::string& c : names) {
+      const index_t i = t.schema().index_of(c);
+      cn.push_back(c.c_str());
+      kinds.push_back(t.schema().kind(i) == ColKind::Key ? LAQ_COL_KEY : LAQ_COL_INT);
+      ptrs.push_back(t.ints(i).data());
+    }
+    rc = laq_star_add_table(star, fact ? "__fact__" : name.c_str(), fact ? 1 : 0, t.row_count(),
+                            static_cast<int32_t>(cn.size()), cn.data(), kinds.data(), 8, ptrs.data());
+    if (rc) {
+      laq_star_destroy(star);
+      return rc;
+    }
+    fact = false;
+  }
+  *out = star;
+  return LAQ_OK;
+}
+
+// The fast path; returns false when the query must take the general path.
+bool fast_query(const StarSchema& data, const bench::QuerySpec& q, DenseMat* result) {
+  // Which columns does the query read, and are they all integer columns?
+  std::vector<std::pair<std::string, std::vector<std::string>>> cols;  // fact first
+  auto want = [&](size_t slot, const std::string& c) {
+    auto& v = cols[slot].second;
+    if (std::find(v.begin(), v.end(), c) == v.end()) v.push_back(c);
+  };
+  cols.push_back({"__fact__", {}});
+  std::vector<size_t> slot_of(q.joins.size());
+  for (size_t j = 0; j < q.joins.size(); ++j) {
+    size_t s = 0;
+    for (size_t k = 1; k < cols.size(); ++k)
+      if (cols[k].first == q.joins[j].dim_name) s = k;
+    if (s == 0) {
+      cols.push_back({q.joins[j].dim_name, {}});
+      s = cols.size() - 1;
+    }
+    slot_of[j] = s;
+    want(0, q.joins[j].fact_fk);
+    want(s, q.joins[j].dim_pk);
+  }
+  for (const bench::FilterSpec& f : q.filters) {
+    if (!(f.pred.*get(PredInt()))) return false;  // float constants: general path
+    if (f.target < -1 || f.target >= static_cast<int>(q.joins.size())) return false;
+    want(f.target < 0 ? 0 : slot_of[static_cast<size_t>(f.target)], f.column);
+  }
+  for (const bench::GroupRef& g : q.group_by) {
+    if (g.target < -1 || g.target >= static_cast<int>(q.joins.size())) return false;
+    want(g.target < 0 ? 0 : slot_of[static_cast<size_t>(g.target)], g.column);
+  }
+  want(0, q.measure);
+  std::vector<ColRef> key;
+  for (size_t s = 0; s < cols.size(); ++s) {
+    const Table* t = nullptr;
+    try {
+      t = s == 0 ? &data.fact() : &data.dim(cols[s].first);
+    } catch (const Error&) {
+      return false;  // the general path raises the reference's error
+    }
+    for (const std::string& c : cols[s].second) {
+      const auto& sc = t->schema().columns;
+      auto it = std::find_if(sc.begin(), sc.end(), [&](const auto& x) { return x.first == c; });
+      if (it == sc.end() || it->second == ColKind::Float) return false;
+      const IntColumn& v = t->ints(c);
+      key.push_back({cols[s].first, c, v.data(), v.size(), fingerprint(v.data(), v.size())});
+    }
+  }
+  laq_star* star = nullptr;
+  std::unique_ptr<CachedStar> owned;
+  CachedStar* entry = nullptr;
+  std::unique_lock<std::mutex> lock(g_cache_mu);
+  if (cache_enabled()) {
+    for (auto it = g_cache.begin(); it != g_cache.end(); ++it)
+      if ((*it)->key == key) {
+        g_cache.splice(g_cache.begin(), g_cache, it);
+        entry = g_cache.front().get();
+        break;
+      }
+  }
+  if (!entry) {
+    owned = std::make_unique<CachedStar>();
+    owned->key = key;
+    owned->status = build_star(data, cols, &owned->star);
+    entry = owned.get();
+    if (cache_enabled()) {
+      g_cache.push_front(std::move(owned));
+      while (g_cache.size() > kCacheEntries) g_cache.pop_back();
+    }
+  }
+  if (entry->status != LAQ_OK) return false;
+  star = entry->star;
+  // Query description (benchgen.hpp:296-326); dims are registered under their names.
+  std::vector<laq_link_desc> links;
+  for (const StarLink& l : q.joins) links.push_back({l.fact_fk.c_str(), l.dim_name.c_str(), l.dim_pk.c_str()});
+  std::vector<laq_filter_desc> filters;
+  for (const bench::FilterSpec& f : q.filters) {
+    const Predicate& p = f.pred;
+    laq_filter_desc d{};
+    d.target = f.target;
+    d.column = f.column.c_str();
+    d.is_float = 0;
+    d.kind = pred_kind(p);
+    d.lo = p.*get(PredIlo());
+    d.hi = p.*get(PredIhi());
+    const auto& set = p.*get(PredIset());
+    d.set = set.data();
+    d.set_len = static_cast<int64_t>(set.size());
+    filters.push_back(d);
+  }
+  std::vector<laq_group_desc> groups;
+  for (const bench::GroupRef& g : q.group_by) groups.push_back({g.target, g.column.c_str()});
+  laq_query_desc desc{static_cast<int32_t>(links.size()), links.data(), static_cast<int32_t>(filters.size()),
+                      filters.data(),   q.measure.c_str(), static_cast<int32_t>(groups.size()),
+                      groups.data(),    q.order_by ? 1 : 0};
+  std::vector<double> buf(1 << 16);
+  int64_t rows = 0, ncols = 0;
+  int rc = laq_run_query(ctx(), star, &desc, buf.data(), static_cast<int64_t>(buf.size()), &rows, &ncols);
+  if (rc == LAQ_ERR_CAPACITY && rows * ncols > static_cast<int64_t>(buf.size())) {
+    buf.resize(static_cast<size_t>(rows * ncols));
+    rc = laq_run_query(ctx(), star, &desc, buf.data(), static_cast<int64_t>(buf.size()), &rows, &ncols);
+  }
+  if (rc != LAQ_OK) return false;
+  buf.resize(static_cast<size_t>(rows * ncols));
+  *result = DenseMat(rows, ncols, std::move(buf));
+  return true;
+}
+
+}  // namespace
+
+// ============================================================================
+// laqops.hpp: selection (laqops.cpp:65-121)
+// ============================================================================
+namespace ops {
+
+namespace {
+SelectionMask mask_of(const void* col, bool is_float, size_t n, const Predicate& pred) {
+  SelectionMask m;
+  m.bits.resize(n);
+  if (n == 0) return m;
+  Dev<std::uint8_t> d(n);
+  const laq_pred p = to_pred(pred);
+  check(laq_selection_mask(ctx(), col, is_float ? 1 : 0, static_cast<int64_t>(n), &p, d.p, 0));
+  const std::vector<std::uint8_t> h = d.to_vector(n);
+  for (size_t i = 0; i < n; ++i) m.bits[i] = h[i] != 0;
+  return m;
+}
+
+Dev<std::uint8_t> dev_mask(const SelectionMask& m) {
+  std::vector<std::uint8_t> h(m.bits.size());
+  for (size_t i = 0; i < h.size(); ++i) h[i] = m.bits[i] ? 1 : 0;
+  return Dev<std::uint8_t>(h);
+}
+}  // namespace
+
+SelectionMask build_selection_mask(const IntColumn& col, const Predicate& pred) {
+  Dev<std::int64_t> d(col);
+  return mask_of(d.p, false, col.size(), pred);
+}
+
+SelectionMask build_selection_mask(const FloatColumn& col, const Predicate& pred) {
+  Dev<double> d(col);
+  return mask_of(d.p, true, col.size(), pred);
+}
+
+SelectionMask mask_and(const SelectionMask& a, const SelectionMask& b) {
+  if (a.size() != b.size()) throw ShapeError("mask_and: length mismatch");
+  SelectionMask out;
+  out.bits.resize(a.bits.size());
+  if (a.bits.empty()) return out;
+  Dev<std::uint8_t> da = dev_mask(a), db = dev_mask(b), dc(a.bits.size());
+  check(laq_mask_and(ctx(), da.p, db.p, a.size(), dc.p));
+  const std::vector<std::uint8_t> h = dc.to_vector(a.bits.size());
+  for (size_t i = 0; i < h.size(); ++i) out.bits[i] = h[i] != 0;
+  return out;
+}
+
+Table apply_mask(const Table& t, const SelectionMask& mask) {
+  if (mask.size() != t.row_count()) throw ShapeError("apply_mask: mask length mismatch");
+  const int64_t n = t.row_count();
+  Dev<std::uint8_t> dm = dev_mask(mask);
+  Dev<std::int64_t> idx(static_cast<size_t>(std::max<int64_t>(n, 1)));
+  int64_t m = 0;
+  if (n) check(laq_mask_indices(ctx(), dm.p, n, idx.p, &m));
+  std::vector<Column> cols;
+  cols.reserve(static_cast<size_t>(t.col_count()));
+  for (index_t c = 0; c < t.col_count(); ++c) {
+    if (std::holds_alternative<IntColumn>(t.column(c))) {
+      const IntColumn& src = std::get<IntColumn>(t.column(c));
+      Dev<std::int64_t> s(src);
+      Dev<std::int64_t> out = gather<std::int64_t>(s.p, 1, idx.p, m, 1);
+      cols.emplace_back(out.to_vector(static_cast<size_t>(m)));
+    } else {
+      const FloatColumn& src = std::get<FloatColumn>(t.column(c));
+      Dev<double> s(src);
+      Dev<double> out = gather<double>(s.p, 2, idx.p, m, 2);
+      cols.emplace_back(out.to_vector(static_cast<size_t>(m)));
+    }
+  }
+  return Table(t.schema(), std::move(cols));
+}
+
+DenseMat apply_mask(const DenseMat& t, const SelectionMask& mask) {
+  if (mask.size() != t.rows()) throw ShapeError("apply_mask: mask length mismatch");
+  const int64_t n = t.rows();
+  Dev<std::uint8_t> dm = dev_mask(mask);
+  Dev<std::int64_t> idx(static_cast<size_t>(std::max<int64_t>(n, 1)));
+  int64_t m = 0;
+  if (n) check(laq_mask_indices(ctx(), dm.p, n, idx.p, &m));
+  DenseMat out(m, t.cols());
+  if (out.data().empty()) return out;
+  Dev<double> s(t.data()), d(out.data().size());
+  check(laq_gather(ctx(), s.p, 2, t.cols(), idx.p, m, d.p, 2));
+  d.down(out.data().data(), out.data().size());
+  return out;
+}
+
+}  // namespace ops
+
+// ============================================================================
+// cli.hpp: the query plan driver and the pipeline driver
+// ============================================================================
+namespace cli {
+
+DenseMat run_query_laq(const StarSchema& data, const bench::QuerySpec& q, StageTimes* stages) {
+  StageTimes local;
+  StageTimes& st = stages ? *stages : local;
+  const double t0 = now_s();
+  DenseMat out;
+  const char* path = std::getenv("LAQ_DROPIN_PATH");  // "general": skip the fast path (tests)
+  const bool general_only = path && std::string(path) == "general";
+  if (general_only || !fast_query(data, q, &out)) out = general_query(data, q);
+  st.materialize += now_s() - t0;  // device passes: filters, joins, aggregation
+  return out;
+}
+
+namespace {
+// Device side of a PipelineRunner: the join's row maps (one fact-ordered dim
+// row id per survivor and link) and the pre-fused linear partials, resident
+// between runs.  Keyed by the runner; the host row-map vector identifies the
+// join the state belongs to.
+struct RunnerDev {
+  const void* rows_key = nullptr;
+  std::vector<Dev<std::int64_t>> idx;
+  std::vector<Dev<double>> partials;
+  std::vector<std::int64_t> partial_rows;
+  index_t out_width = 0;
+  // cost-model inputs recorded at construction (plan_pipeline)
+  index_t k = 0;
+  index_t model_width = 0;
+  bool is_tree = false;
+  std::vector<std::int64_t> dim_rows;
+};
+std::mutex g_run_mu;
+std::map<const PipelineRunner*, std::unique_ptr<RunnerDev>> g_runners;
+
+RunnerDev& runner_dev(const PipelineRunner* r) {
+  std::lock_guard<std::mutex> lock(g_run_mu);
+  auto& p = g_runners[r];
+  if (!p) p = std::make_unique<RunnerDev>();
+  return *p;
+}
+}  // namespace
+
+PipelineRunner::PipelineRunner(const StarSchema& data, const ml::TreeModel* tree, const ml::LinearOperator* linear,
+                               std::int64_t max_bytes)
+    : data_(&data), tree_(tree), linear_(linear), layout_(bench::feature_layout(data)), max_bytes_(max_bytes) {
+  // Setup as cli.cpp:246-277: feature matrices, placements, tree compilation.
+  if ((tree_ != nullptr) == (linear_ != nullptr))
+    throw ShapeError("pipeline: exactly one of tree/linear model required");
+  for (std::size_t d = 0; d < layout_.dim_names.size(); ++d) {
+    dim_mats_.push_back(to_matrix(data.dim(layout_.dim_names[d]), layout_.dim_feature_cols[d]));
+    std::vector<std::pair<index_t, index_t>> mapping;
+    for (index_t f = 0; f < static_cast<index_t>(layout_.dim_feature_cols[d].size()); ++f)
+      mapping.emplace_back(f, layout_.offsets[d] + f);
+    placements_.push_back(ops::build_placement_map(static_cast<index_t>(mapping.size()), layout_.total, mapping));
+  }
+  join_specs_ = {{&data.dim("part"), "lo_part", "p_key"},
+                 {&data.dim("supplier"), "lo_supplier", "s_key"},
+                 {&data.dim("date"), "lo_orderdate", "d_key"}};
+  if (tree_) {
+    tree_la_ = ml::compile_tree(*tree_, layout_.total);
+    tree_parts_ = fusion::partition_tree(tree_la_, layout_.feature_owner,
+                                         static_cast<index_t>(layout_.dim_names.size()));
+  } else if (linear_->mat.rows() != layout_.total) {
+    throw ShapeError("pipeline: operator input width " + std::to_string(linear_->mat.rows()) +
+                     " does not match feature width " + std::to_string(layout_.total));
+  }
+  {
+    std::lock_guard<std::mutex> lock(g_run_mu);
+    g_runners.erase(this);  // a previous runner at this address
+  }
+  RunnerDev& rd = runner_dev(this);
+  rd.k = layout_.total;
+  rd.is_tree = tree_ != nullptr;
+  rd.model_width = tree_ ? tree_la_.leaf_count() : linear_->mat.cols();
+  for (const DenseMat& m : dim_mats_) rd.dim_rows.push_back(std::max<index_t>(m.rows(), 1));
+}
+
+void PipelineRunner::prepare_joins(StageTimes& st) {
+  if (joined_) return;
+  // multiway_star_join on the device (laq_star_join), the row maps kept resident.
+  const double t0 = now_s();
+  const Table& fact = data_->fact();
+  const size_t J = join_specs_.size();
+  const int64_t n = fact.row_count();
+  RunnerDev& rd = runner_dev(this);
+  rd.idx.clear();
+  std::vector<Dev<std::int64_t>> fk, pk;
+  std::vector<const int64_t*> pf, pp;
+  std::vector<int64_t*> pr;
+  std::vector<int64_t> prow;
+  for (size_t j = 0; j < J; ++j) {
+    fk.emplace_back(fact.ints(join_specs_[j].fk_col));
+    pk.emplace_back(join_specs_[j].dim->ints(join_specs_[j].pk_col));
+    rd.idx.emplace_back(static_cast<size_t>(std::max<int64_t>(n, 1)));
+    pf.push_back(fk.back().p);
+    pp.push_back(pk.back().p);
+    pr.push_back(rd.idx.back().p);
+    prow.push_back(join_specs_[j].dim->row_count());
+  }
+  int64_t nnz = 0;
+  check(laq_star_join(ctx(), static_cast<int32_t>(J), pf.data(), n, pp.data(), prow.data(), nullptr, pr.data(),
+                      &nnz));
+  st.spmm += now_s() - t0;
+  {  // csr_from_coo of each RowMatch (row_idx = iota) on the device; host-visible CSR members
+    const double t1 = now_s();
+    i_csr_.clear();
+    Dev<std::int64_t> iota_rows(static_cast<size_t>(std::max<int64_t>(nnz, 1)));
+    std::vector<std::int64_t> h(static_cast<size_t>(nnz));
+    std::iota(h.begin(), h.end(), std::int64_t{0});
+    iota_rows.up(h.data(), h.size());
+    for (size_t j = 0; j < J; ++j) {
+      Dev<std::int64_t> rp(static_cast<size_t>(nnz) + 1);
+      check(laq_csr_from_coo(ctx(), iota_rows.p, rd.idx[j].p, nnz, nnz, join_specs_[j].dim->row_count(), rp.p));
+      SparseCsr c;
+      c.rows = nnz;
+      c.cols = join_specs_[j].dim->row_count();
+      c.row_ptr = rp.to_vector(static_cast<size_t>(nnz) + 1);
+      c.col_idx = rd.idx[j].to_vector(static_cast<size_t>(nnz));
+      c.values.assign(static_cast<size_t>(nnz), 1.0);
+      i_csr_.push_back(std::move(c));
+    }
+    st.construct += now_s() - t1;
+  }
+  rd.rows_key = i_csr_.empty() ? nullptr : i_csr_[0].col_idx.data();
+  target_rows_ = J == 0 ? 0 : nnz;
+  joined_ = true;
+}
+
+void PipelineRunner::prefuse(StageTimes& st) {
+  if (fused_linear_ || fused_tree_) return;
+  const index_t out_width = linear_ ? linear_->mat.cols() : tree_la_.leaf_count();
+  std::int64_t partial_cells = 0;
+  for (const DenseMat& dim : dim_mats_) partial_cells += dim.rows() * out_width;
+  if (max_bytes_ > 0 && partial_cells * 8 > max_bytes_)
+    throw CapacityError("pre-fused partials need " + std::to_string(partial_cells * 8) + " bytes, cap is " +
+                        std::to_string(max_bytes_));
+  const double t0 = now_s();
+  if (linear_) {
+    fused_linear_ = fusion::prefuse_linear(dim_mats_, placements_, *linear_);
+    RunnerDev& rd = runner_dev(this);  // keep the partials resident for run_fused
+    rd.partials.clear();
+    rd.partial_rows.clear();
+    for (const DenseMat& p : fused_linear_->partials) {
+      rd.partials.emplace_back(p.data());
+      rd.partial_rows.push_back(p.rows());
+    }
+    rd.out_width = fused_linear_->out_width;
+  } else {
+    fused_tree_ = fusion::prefuse_tree(dim_mats_, placements_, tree_parts_, tree_la_.path_score, tree_la_.labels);
+  }
+  st.prefuse += now_s() - t0;
+}
+
+void PipelineRunner::invalidate_prefuse() {
+  fused_linear_.reset();
+  fused_tree_.reset();
+  runner_dev(this).partials.clear();
+}
+
+PipelineResult PipelineRunner::run_nonfused(StageTimes& st) {
+  prepare_joins(st);
+  if (max_bytes_ > 0 && target_rows_ * layout_.total * 8 > max_bytes_)
+    throw CapacityError("materialized target needs " + std::to_string(target_rows_ * layout_.total * 8) +
+                        " bytes, cap is " + std::to_string(max_bytes_));
+  PipelineResult out;
+  DenseMat target;
+  double t0 = now_s();
+  target = ops::materialize(i_csr_, dim_mats_, placements_);
+  st.materialize += now_s() - t0;
+  t0 = now_s();
+  if (linear_) out.values = ml::predict_linear(target, *linear_);
+  else out.labels = ml::predict_tree(target, tree_la_);
+  st.predict += now_s() - t0;
+  return out;
+}
+
+PipelineResult PipelineRunner::run_fused(StageTimes& st) {
+  prepare_joins(st);
+  prefuse(st);
+  PipelineResult out;
+  const double t0 = now_s();
+  RunnerDev& rd = runner_dev(this);
+  const bool resident = linear_ && !rd.partials.empty() && rd.idx.size() == i_csr_.size() &&
+                        rd.rows_key == (i_csr_.empty() ? nullptr : i_csr_[0].col_idx.data());
+  if (resident) {  // fused gather-sum over the resident row maps and partials; only Y moves
+    std::vector<const int64_t*> pi;
+    std::vector<const double*> pp;
+    for (size_t j = 0; j < rd.idx.size(); ++j) {
+      pi.push_back(rd.idx[j].p);
+      pp.push_back(rd.partials[j].p);
+    }
+    DenseMat y(target_rows_, rd.out_width);
+    if (!y.data().empty()) {
+      Dev<double> dy(y.data().size());
+      check(laq_apply_fused_linear(ctx(), static_cast<int32_t>(pi.size()), pi.data(), target_rows_, pp.data(),
+                                   rd.partial_rows.data(), rd.out_width, dy.p));
+      dy.down(y.data().data(), y.data().size());
+    }
+    out.values = std::move(y);
+  } else if (linear_) {
+    out.values = fusion::apply_fused_linear(i_csr_, *fused_linear_);
+  } else {
+    out.labels = fusion::apply_fused_tree(i_csr_, *fused_tree_);
+  }
+  st.predict += now_s() - t0;
+  return out;
+}
+
+PipelineResult PipelineRunner::run_oracle(StageTimes& st) {
+  // The reference's own scalar pipeline (oracle::star_pipeline, oracle.cpp) -- the checker.
+  std::vector<oracle::DimRef> refs;
+  for (const ops::DimJoinSpec& spec : join_specs_) refs.push_back({spec.dim, spec.fk_col, spec.pk_col});
+  oracle::PipelineOutput raw;
+  double t0 = now_s();
+  raw = oracle::star_pipeline(data_->fact(), refs, layout_.dim_feature_cols, tree_ ? tree_ : nullptr, nullptr);
+  st.materialize += now_s() - t0;
+  PipelineResult out;
+  if (tree_) {
+    out.labels = std::move(raw.labels);
+    return out;
+  }
+  t0 = now_s();
+  const DenseMat& x = raw.values;
+  const DenseMat& w = linear_->mat;
+  DenseMat pred(x.rows(), w.cols());
+  for (index_t m = 0; m < x.rows(); ++m)  // scalar dot per (row, output), features in order
+    for (index_t c = 0; c < w.cols(); ++c) {
+      double acc = 0;
+      for (index_t f = 0; f < x.cols(); ++f) acc += x(m, f) * w(f, c);
+      pred(m, c) = acc;
+    }
+  out.values = std::move(pred);
+  st.predict += now_s() - t0;
+  return out;
+}
+
+// ---- include/laq_dropin.hpp: the planner-driven pipeline -----------------------
+PlanChoice plan_pipeline(PipelineRunner& r, StageTimes& st, double threshold) {
+  r.prepare_joins(st);
+  RunnerDev& rd = runner_dev(&r);
+  PlanChoice p;
+  p.inputs.target_rows = std::max<index_t>(r.target_rows(), 1);
+  p.inputs.input_width = rd.k;
+  p.inputs.output_width = rd.model_width;
+  p.inputs.tree_features = rd.k;  // the tree ratio assumes p == k (fusion.hpp:61)
+  p.inputs.dim_rows = rd.dim_rows;
+  p.ratio = rd.is_tree ? fusion::speedup_ratio_tree(p.inputs) : fusion::speedup_ratio_linear(p.inputs);
+  p.fused = fusion::decide_fusion(p.ratio, threshold);
+  return p;
+}
+
+PipelineResult run_auto(PipelineRunner& r, StageTimes& st, double threshold, PlanChoice* chosen) {
+  const PlanChoice p = plan_pipeline(r, st, threshold);
+  if (chosen) *chosen = p;
+  return p.fused ? r.run_fused(st) : r.run_nonfused(st);
+}
+
+}  // namespace cli
+}  // namespace laq

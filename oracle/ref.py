@@ -245,6 +245,81 @@ def gen_queries(star: RefStar, group: int, targets=()):
     return dials, real
 
 
+def _csr_args(m):
+    rp = np.ascontiguousarray(m.row_ptr, np.int64)
+    ci = np.ascontiguousarray(m.col_idx, np.int64)
+    v = np.ascontiguousarray(m.values, np.float64)
+    return (rp, ci, v), (rp.ctypes.data, ci.ctypes.data, v.ctypes.data, m.rows, m.cols)
+
+
+def spmm(a, b):
+    """matrix.cpp:81-123 -> (row_ptr, col_idx, values)."""
+    ka, aa = _csr_args(a)
+    kb, bb = _csr_args(b)
+    cap = max(1, len(ka[1]) * max(1, b.cols))
+    cap = min(cap, max(1, len(ka[1])) * max(1, int(np.diff(kb[0]).max()) if b.rows else 1))
+    rp = np.zeros(a.rows + 1, np.int64)
+    ci = np.zeros(cap, np.int64)
+    cv = np.zeros(cap, np.float64)
+    nnz = C.c_int64()
+    L = lib()
+    L.ref_spmm.argtypes = [C.c_void_p] * 3 + [C.c_int64] * 2 + [C.c_void_p] * 3 + [C.c_int64] * 3 + \
+        [C.c_void_p] * 3 + [C.c_void_p]
+    _check(L.ref_spmm(*aa, *bb, cap, rp.ctypes.data, ci.ctypes.data, cv.ctypes.data, C.byref(nnz)))
+    return rp, ci[: nnz.value].copy(), cv[: nnz.value].copy()
+
+
+def csr_from_coo(row_idx, col_idx, values, rows, cols):
+    r = np.ascontiguousarray(row_idx, np.int64)
+    c = np.ascontiguousarray(col_idx, np.int64)
+    v = np.ascontiguousarray(values, np.float64)
+    rp = np.zeros(rows + 1 if rows >= 0 else 1, np.int64)
+    L = lib()
+    L.ref_csr_from_coo.argtypes = [C.c_void_p] * 3 + [C.c_int64] * 3 + [C.c_void_p]
+    _check(L.ref_csr_from_coo(r.ctypes.data, c.ctypes.data, v.ctypes.data, len(c), rows, cols, rp.ctypes.data))
+    return rp
+
+
+def coo_from_csr(m):
+    k, a = _csr_args(m)
+    out = np.zeros(max(1, len(k[1])), np.int64)
+    L = lib()
+    L.ref_coo_from_csr.argtypes = [C.c_void_p] * 3 + [C.c_int64] * 2 + [C.c_void_p]
+    _check(L.ref_coo_from_csr(*a[:3], m.rows, m.cols, out.ctypes.data))
+    return out[: len(k[1])]
+
+
+def sort_rows(t, key_cols, directions):
+    t = np.ascontiguousarray(t, np.float64)
+    out = np.zeros_like(t)
+    k = np.ascontiguousarray(key_cols, np.int64)
+    d = np.ascontiguousarray([1 if x == "Desc" else 0 for x in directions], np.int32)
+    L = lib()
+    L.ref_sort_rows.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]
+    _check(L.ref_sort_rows(t.ctypes.data, t.shape[0], t.shape[1], k.ctypes.data, d.ctypes.data, len(k),
+                           out.ctypes.data))
+    return out
+
+
+def selection_mask(col, pred):
+    """build_selection_mask (laqops.cpp:65-79) with a query.Pred."""
+    col = np.asarray(col)
+    is_float = col.dtype.kind == "f"
+    col = np.ascontiguousarray(col, np.float64 if is_float else np.int64)
+    out = np.zeros(max(1, len(col)), np.uint8)
+    iset = np.ascontiguousarray(np.asarray(pred.values if not pred.is_float else [], np.int64))
+    fset = np.ascontiguousarray(np.asarray(pred.values if pred.is_float else [], np.float64))
+    L = lib()
+    L.ref_selection_mask.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int64, C.c_int64,
+                                     C.c_double, C.c_double, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+    _check(L.ref_selection_mask(col.ctypes.data, 1 if is_float else 0, len(col), pred.kind,
+                                1 if pred.is_float else 0, int(pred.lo) if not pred.is_float else 0,
+                                int(pred.hi) if not pred.is_float else 0,
+                                float(pred.lo) if pred.is_float else 0.0, float(pred.hi) if pred.is_float else 0.0,
+                                iset.ctypes.data, fset.ctypes.data, len(pred.values), out.ctypes.data))
+    return out[: len(col)]
+
+
 def cfg1_inputs(n_fact=1_000_000, dim_rows=10_000, k=16, l=1, seed=42):
     """cfg1 inputs from the reference's own Rng / gen_linear (ref_cfg1_inputs)."""
     fk = np.zeros(n_fact, np.int64)

@@ -598,6 +598,101 @@ int ref_dense_matmul(const double* a, int64_t m, int64_t k, const double* b, int
 // unit() feature columns drawn column by column from derive_seed(seed, "dim")
 // (as make_dim draws features, benchgen.cpp:96-99), stored row-major; W =
 // gen_linear(k, l, 7) (row-major k x l).
+// ---- matrix / selection API (matrix.cpp:81-123, 198-255; laqops.cpp:65-121, 457-478)
+SparseCsr make_csr(const int64_t* rp, const int64_t* ci, const double* v, int64_t rows, int64_t cols) {
+  SparseCsr m;
+  m.rows = rows;
+  m.cols = cols;
+  m.row_ptr.assign(rp, rp + rows + 1);
+  const int64_t nnz = rp[rows];
+  m.col_idx.assign(ci, ci + nnz);
+  m.values.assign(v, v + nnz);
+  return m;
+}
+
+int ref_spmm(const int64_t* a_rp, const int64_t* a_ci, const double* a_v, int64_t a_rows, int64_t a_cols,
+             const int64_t* b_rp, const int64_t* b_ci, const double* b_v, int64_t b_rows, int64_t b_cols, int64_t cap,
+             int64_t* c_rp, int64_t* c_ci, double* c_v, int64_t* nnz) {
+  return guard([&] {
+    const SparseCsr c = spmm(make_csr(a_rp, a_ci, a_v, a_rows, a_cols), make_csr(b_rp, b_ci, b_v, b_rows, b_cols));
+    *nnz = c.nnz();
+    if (c.nnz() > cap) throw CapacityError("output capacity");
+    std::copy(c.row_ptr.begin(), c.row_ptr.end(), c_rp);
+    std::copy(c.col_idx.begin(), c.col_idx.end(), c_ci);
+    std::copy(c.values.begin(), c.values.end(), c_v);
+  });
+}
+
+int ref_csr_from_coo(const int64_t* r, const int64_t* c, const double* v, int64_t nnz, int64_t rows, int64_t cols,
+                     int64_t* rp) {
+  return guard([&] {
+    SparseCoo m;
+    m.rows = rows;
+    m.cols = cols;
+    m.row_idx.assign(r, r + nnz);
+    m.col_idx.assign(c, c + nnz);
+    m.values.assign(v, v + nnz);
+    const SparseCsr out = csr_from_coo(m);
+    std::copy(out.row_ptr.begin(), out.row_ptr.end(), rp);
+  });
+}
+
+int ref_coo_from_csr(const int64_t* rp, const int64_t* ci, const double* v, int64_t rows, int64_t cols, int64_t* r) {
+  return guard([&] {
+    const SparseCoo m = coo_from_csr(make_csr(rp, ci, v, rows, cols));
+    std::copy(m.row_idx.begin(), m.row_idx.end(), r);
+  });
+}
+
+int ref_sort_rows(const double* t, int64_t rows, int64_t cols, const int64_t* keys, const int32_t* desc, int32_t nk,
+                  double* out) {
+  return guard([&] {
+    DenseMat m(rows, cols, std::vector<double>(t, t + rows * cols));
+    std::vector<index_t> kc(keys, keys + nk);
+    std::vector<ops::SortDir> d;
+    for (int32_t k = 0; k < nk; ++k) d.push_back(desc[k] ? ops::SortDir::Desc : ops::SortDir::Asc);
+    const DenseMat o = ops::sort_rows(m, kc, d);
+    std::copy(o.data().begin(), o.data().end(), out);
+  });
+}
+
+// build_selection_mask over an int64 (is_float = 0) or double column with a typed predicate.
+int ref_selection_mask(const void* col, int is_float, int64_t n, int kind, int pred_float, int64_t ilo, int64_t ihi,
+                       double flo, double fhi, const int64_t* iset, const double* fset, int64_t set_len,
+                       uint8_t* out) {
+  return guard([&] {
+    auto make = [&]() -> Predicate {
+      if (pred_float) {
+        switch (kind) {
+          case LAQ_PRED_LT: return Predicate::lt(flo);
+          case LAQ_PRED_LE: return Predicate::le(flo);
+          case LAQ_PRED_EQ: return Predicate::eq(flo);
+          case LAQ_PRED_GE: return Predicate::ge(flo);
+          case LAQ_PRED_GT: return Predicate::gt(flo);
+          case LAQ_PRED_BETWEEN: return Predicate::between(flo, fhi);
+          default: return Predicate::in_set(std::vector<double>(fset, fset + set_len));
+        }
+      }
+      switch (kind) {
+        case LAQ_PRED_LT: return Predicate::lt(ilo);
+        case LAQ_PRED_LE: return Predicate::le(ilo);
+        case LAQ_PRED_EQ: return Predicate::eq(ilo);
+        case LAQ_PRED_GE: return Predicate::ge(ilo);
+        case LAQ_PRED_GT: return Predicate::gt(ilo);
+        case LAQ_PRED_BETWEEN: return Predicate::between(ilo, ihi);
+        default: return Predicate::in_set(std::vector<std::int64_t>(iset, iset + set_len));
+      }
+    };
+    const Predicate p = make();
+    const ops::SelectionMask m =
+        is_float ? ops::build_selection_mask(FloatColumn(static_cast<const double*>(col),
+                                                          static_cast<const double*>(col) + n), p)
+                 : ops::build_selection_mask(IntColumn(static_cast<const int64_t*>(col),
+                                                       static_cast<const int64_t*>(col) + n), p);
+    for (int64_t i = 0; i < n; ++i) out[i] = m.bits[i] ? 1 : 0;
+  });
+}
+
 int ref_cfg1_inputs(int64_t n, int64_t dim_rows, int64_t k, int64_t l, uint64_t seed, int64_t* fk, int64_t* pk,
                     double* feats, double* w) {
   return guard([&] {

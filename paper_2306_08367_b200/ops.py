@@ -228,17 +228,188 @@ def groupby_sum_multi(group_cols, vals):
     return _out(keys[:, :g], on), _out(sums[:g], on)
 
 
-def sort_rows(t: np.ndarray, key_cols, directions):
-    """laqops.cpp:457-478 (host; ORDER BY over <= a few hundred result rows)."""
+def sort_rows(t, key_cols, directions):
+    """laqops.cpp:457-478 on the device (laq_sort_rows): stable lexicographic,
+    directions "Asc" / "Desc"."""
     if len(key_cols) != len(directions):
         raise errors.ShapeError("sort_rows: key/direction counts")
-    t = np.asarray(t)
-    for c in key_cols:
-        if c < 0 or c >= t.shape[1]:
-            raise errors.IndexError(f"sort_rows: key column {c}")
-    order = np.arange(t.shape[0])
-    for c, d in reversed(list(zip(key_cols, directions))):  # stable LSD passes
-        col = t[order, c]
-        o = np.argsort(-col if d == "Desc" else col, kind="stable")
-        order = order[o]
-    return t[order]
+    on = _is_dev(t)
+    ctx = context()
+    d = dev(t, torch.float64)
+    if d.dim() != 2:
+        raise errors.ShapeError("sort_rows: matrix expected")
+    rows, cols = d.shape
+    out = torch.empty((max(rows, 1), max(cols, 1)), dtype=torch.float64, device="cuda")[:rows, :cols].contiguous()
+    kc = (C.c_int64 * max(1, len(key_cols)))(*[int(c) for c in key_cols])
+    kd = (C.c_int32 * max(1, len(key_cols)))(*[1 if x == "Desc" else 0 for x in directions])
+    ctx.check(ctx.lib.laq_sort_rows(ctx.h, d.data_ptr(), rows, cols, kc, kd, len(key_cols), out.data_ptr()))
+    return _out(out, on)
+
+
+# ---------------------------------------------------------------------------
+# sparse formats and SpGEMM (matrix.hpp:44-100)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class Coo:
+    """SparseCoo (matrix.hpp:60-71)."""
+    rows: int
+    cols: int
+    row_idx: np.ndarray
+    col_idx: np.ndarray
+    values: np.ndarray
+
+    def nnz(self) -> int:
+        return int(len(self.col_idx))
+
+
+def _chk_coo(c):
+    if c.rows < 0 or c.cols < 0:
+        raise errors.Error("coo: negative dimension")
+    if len(c.row_idx) != len(c.col_idx) or len(c.values) != len(c.col_idx):
+        raise errors.Error("coo: index/value length mismatch")
+
+
+def csr_from_coo(c: Coo) -> Csr:
+    """matrix.cpp:210-221 (check_canonical first, matrix.cpp:243-255)."""
+    _chk_coo(c)
+    ctx = context()
+    r, ci = dev(c.row_idx, i64), dev(c.col_idx, i64)
+    rp = torch.empty(c.rows + 1, dtype=i64, device="cuda")
+    ctx.check(ctx.lib.laq_csr_from_coo(ctx.h, r.data_ptr(), ci.data_ptr(), len(c.col_idx), c.rows, c.cols,
+                                       rp.data_ptr()))
+    return Csr(c.rows, c.cols, host(rp), np.asarray(c.col_idx, np.int64).copy(), np.asarray(c.values, np.float64).copy())
+
+
+def coo_from_csr(m: Csr) -> Coo:
+    """matrix.cpp:198-208."""
+    ctx = context()
+    rp = dev(m.row_ptr, i64)
+    nnz = len(m.col_idx)
+    out = torch.empty(max(nnz, 1), dtype=i64, device="cuda")
+    ctx.check(ctx.lib.laq_coo_from_csr(ctx.h, rp.data_ptr(), m.rows, nnz, out.data_ptr()))
+    return Coo(m.rows, m.cols, host(out[:nnz]), np.asarray(m.col_idx, np.int64).copy(),
+               np.asarray(m.values, np.float64).copy())
+
+
+def spmm(a: Csr, b: Csr) -> Csr:
+    """matrix.cpp:81-123: Gustavson SpGEMM, bit-identical (laq_spmm)."""
+    if a.cols != b.rows:
+        raise errors.ShapeError(f"spmm: {a.rows}x{a.cols} x {b.rows}x{b.cols}")
+    ctx = context()
+    ar, ac, av = dev(a.row_ptr, i64), dev(a.col_idx, i64), dev(a.values, torch.float64)
+    br, bc, bv = dev(b.row_ptr, i64), dev(b.col_idx, i64), dev(b.values, torch.float64)
+    rp = torch.empty(a.rows + 1, dtype=i64, device="cuda")
+    cap = max(1, len(a.col_idx), len(b.col_idx))
+    while True:
+        ci = torch.empty(cap, dtype=i64, device="cuda")
+        cv = torch.empty(cap, dtype=torch.float64, device="cuda")
+        nnz = C.c_int64()
+        rc = ctx.lib.laq_spmm(ctx.h, ar.data_ptr(), ac.data_ptr(), av.data_ptr(), a.rows, a.cols, br.data_ptr(),
+                              bc.data_ptr(), bv.data_ptr(), b.rows, b.cols, rp.data_ptr(), ci.data_ptr(),
+                              cv.data_ptr(), cap, C.byref(nnz))
+        if rc == 13 and nnz.value > cap:
+            cap = nnz.value
+            continue
+        ctx.check(rc)
+        m = nnz.value
+        return Csr(a.rows, b.cols, host(rp), host(ci[:m]), host(cv[:m]))
+
+
+def row_mapping_matrices(match: RowMatch):
+    """laqops.cpp:321-336: (I_R, I_S) one-hot CSR from a canonical RowMatch
+    (validated on the device, check_canonical)."""
+    ctx = context()
+    r, s = dev(match.row_idx, i64), dev(match.col_idx, i64)
+    ctx.check(ctx.lib.laq_coo_check(ctx.h, r.data_ptr(), s.data_ptr(), r.numel(), match.rows, match.cols))
+    n = r.numel()
+    rp = np.arange(n + 1, dtype=np.int64)
+    return (Csr(n, match.rows, rp, host(r), np.ones(n)), Csr(n, match.cols, rp.copy(), host(s), np.ones(n)))
+
+
+# ---------------------------------------------------------------------------
+# selection (laqops.cpp:65-121, predicate.hpp:81-103)
+# ---------------------------------------------------------------------------
+
+def _pred_desc(p):
+    from . import _abi
+    keep = []
+    d = _abi.PredDesc()
+    d.kind, d.is_float = p.kind, 1 if p.is_float else 0
+    if p.is_float:
+        d.flo, d.fhi = float(p.lo), float(p.hi)
+        fs = np.ascontiguousarray(np.asarray(p.values, np.float64))
+        keep.append(fs)
+        d.fset = fs.ctypes.data_as(_abi.f64p) if len(fs) else _abi.f64p()
+        d.set_len = len(fs)
+    else:
+        d.ilo, d.ihi = int(p.lo), int(p.hi)
+        si = np.ascontiguousarray(np.asarray(p.values, np.int64))
+        keep.append(si)
+        d.iset = si.ctypes.data_as(_abi.i64p) if len(si) else _abi.i64p()
+        d.set_len = len(si)
+    return d, keep
+
+
+def build_selection_mask(col, pred):
+    """laqops.cpp:65-79: uint8 mask of pred.matches(col[i]) (TypeError on a
+    typed mismatch over a non-empty column)."""
+    on = _is_dev(col)
+    ctx = context()
+    is_float = (col.dtype == torch.float64) if isinstance(col, torch.Tensor) else np.asarray(col).dtype.kind == "f"
+    c = dev(col, torch.float64 if is_float else i64)
+    n = c.numel()
+    m = torch.empty(max(n, 1), dtype=torch.uint8, device="cuda")
+    d, keep = _pred_desc(pred)
+    ctx.check(ctx.lib.laq_selection_mask(ctx.h, c.data_ptr(), 1 if is_float else 0, n, C.byref(d), m.data_ptr(), 0))
+    return _out(m[:n], on)
+
+
+def mask_and(a, b):
+    """laqops.cpp:87-93."""
+    if len(a) != len(b):
+        raise errors.ShapeError("mask_and: length mismatch")
+    on = _is_dev(a, b)
+    ctx = context()
+    x, y = dev(a, torch.uint8), dev(b, torch.uint8)
+    out = torch.empty(max(x.numel(), 1), dtype=torch.uint8, device="cuda")
+    ctx.check(ctx.lib.laq_mask_and(ctx.h, x.data_ptr(), y.data_ptr(), x.numel(), out.data_ptr()))
+    return _out(out[: x.numel()], on)
+
+
+def mask_indices(mask):
+    on = _is_dev(mask)
+    ctx = context()
+    m = dev(mask, torch.uint8)
+    out = torch.empty(max(m.numel(), 1), dtype=i64, device="cuda")
+    n = C.c_int64()
+    ctx.check(ctx.lib.laq_mask_indices(ctx.h, m.data_ptr(), m.numel(), out.data_ptr(), C.byref(n)))
+    return _out(out[: n.value], on)
+
+
+def apply_mask(table, mask):
+    """laqops.cpp:95-121: rows whose mask is set, in order.  table: a 2-D
+    matrix (DenseMat) or a {column: array} dict (Table)."""
+    on = _is_dev(mask)
+    ctx = context()
+    idx = mask_indices(dev(mask, torch.uint8))
+    n = idx.numel()
+
+    def gather(a, row_elems):
+        src = dev(a)
+        kind = {torch.int32: 0, torch.int64: 1, torch.float64: 2}[src.dtype]
+        out = torch.empty((max(n, 1), row_elems) if row_elems > 1 else (max(n, 1),),
+                          dtype=torch.float64 if kind == 2 else i64, device="cuda")
+        ctx.check(ctx.lib.laq_gather(ctx.h, src.data_ptr(), kind, row_elems, idx.data_ptr(), n, out.data_ptr(),
+                                     2 if kind == 2 else 1))
+        return _out(out[:n], on or isinstance(a, torch.Tensor))
+
+    if isinstance(table, dict):
+        for c, a in table.items():
+            if len(a) != len(mask):
+                raise errors.ShapeError("apply_mask: mask length mismatch")
+        return {c: gather(a, 1) for c, a in table.items()}
+    t = dev(table, torch.float64)
+    if t.shape[0] != len(mask):
+        raise errors.ShapeError("apply_mask: mask length mismatch")
+    return gather(t, t.shape[1])

@@ -43,6 +43,11 @@ class Pred:
     @staticmethod
     def in_set(vals): return Pred(INSET, values=tuple(sorted(int(v) for v in vals)))
 
+    @staticmethod
+    def flt(kind, lo=0.0, hi=0.0, values=()):
+        """A float-typed Predicate (predicate.hpp:25-33): matches float columns only."""
+        return Pred(kind, float(lo), float(hi), tuple(sorted(float(v) for v in values)), True)
+
     def matches(self, v: np.ndarray) -> np.ndarray:
         k = self.kind
         if k == LT: return v < self.lo

@@ -29,7 +29,8 @@ def _bins():
 
 def test_drop_in_binds_every_hot_symbol():
     _bins()
-    out = subprocess.run(["nm", "-C", os.path.join(BUILD, "laq_dropin.o")], capture_output=True, text=True).stdout
+    out = "".join(subprocess.run(["nm", "-C", os.path.join(BUILD, o)], capture_output=True, text=True).stdout
+                  for o in ("laq_dropin.o", "laq_dropin_query.o"))
     defined = [l for l in out.splitlines() if " T " in l]
     for h in HOT:
         assert any(h in l for l in defined), h
@@ -57,3 +58,30 @@ def test_reference_acceptance_on_device():
     r = subprocess.run([os.path.join(BUILD, "acceptance")], capture_output=True, text=True, timeout=1800, cwd=BUILD)
     lines = [l for l in r.stdout.splitlines() if l.startswith("[")]
     assert lines and all(l.startswith("[PASS]") for l in lines), r.stdout[-4000:]
+
+
+def test_hot_symbols_resolve_to_the_drop_in():
+    """In a linked binary every hot symbol has exactly one (strong) definition:
+    the reference's weakened copies are overridden, never called."""
+    _bins()
+    syms = subprocess.run(["nm", "-C", "--defined-only", os.path.join(BUILD, "test_cli")], capture_output=True,
+                          text=True).stdout.splitlines()
+    for h in HOT:
+        lines = [l for l in syms if h in l and "[clone" not in l]  # .cold clones are local parts
+        assert lines, h
+        assert all(l.split(" ", 2)[1] == "T" for l in lines), (h, lines[:3])
+
+
+@pytest.mark.gpu
+def test_drop_in_extra_checks_on_device():
+    """integration/dropin_extra.cpp: the general device path of run_query_laq
+    (float measures / predicates, int64 values, filtered duplicate keys), the
+    device cache, and the planner-driven run_auto, against the reference's own
+    run_query_oracle / cost model at tolerance 0."""
+    _bins()
+    exe = os.path.join(BUILD, "dropin_extra")
+    if not os.path.exists(exe):
+        pytest.skip("dropin_extra not built")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900, cwd=BUILD)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("[")]
+    assert r.returncode == 0 and lines and all(l.startswith("[PASS]") for l in lines), r.stdout[-4000:] + r.stderr[-2000:]
