@@ -266,7 +266,7 @@ int laq_apply_fused_linear_f32(laq_ctx* ctx, int32_t n_parts, const int32_t* con
  * placement value (NULL = all 1).  Bit-identical to the
  * reference.  predict_tree's scores (mlops.cpp:254-268) are the same call on T
  * with every node.  d_out rows x l.  p <= 2048 nodes.  Synchronises.
- * laq_apply_fused_tree: apply_fused_tree (fusion.cpp:146-168) /
+ * laq_apply_fused_tree: apply_fused_tree (fusion.cpp:138-159) /
  * predict_tree's decode (mlops.cpp:269-280): scores = ((P_0[i_0] + P_1[i_1]) +
  * ...), label = labels[c] of the unique leaf with scores[c] == path_score[c].
  * d_idx NULL (or d_idx[j] NULL) = identity rows.  LAQ_ERR_MODEL for the first

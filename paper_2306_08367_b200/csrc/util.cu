@@ -204,8 +204,8 @@ int laq_speedup_ratio_tree(int64_t i, int64_t k, int64_t l, int64_t p, const int
 }
 
 int laq_decide_fusion(double ratio, double threshold, int32_t* out) {
-  if (!std::isfinite(ratio)) return LAQ_ERR_DOMAIN;  // fusion.cpp:300
-  *out = ratio > threshold ? 1 : 0;                   // strict, fusion.cpp:301
+  if (!std::isfinite(ratio)) return LAQ_ERR_DOMAIN;  // fusion.cpp:222
+  *out = ratio > threshold ? 1 : 0;                   // strict, fusion.cpp:223
   return LAQ_OK;
 }
 

@@ -395,21 +395,21 @@ def apply_mask(table, mask):
     idx = mask_indices(dev(mask, torch.uint8))
     n = idx.numel()
 
-    def gather(a, row_elems):
+    def gather(a, row_elems, a_dev):
         src = dev(a)
         kind = {torch.int32: 0, torch.int64: 1, torch.float64: 2}[src.dtype]
         out = torch.empty((max(n, 1), row_elems) if row_elems > 1 else (max(n, 1),),
                           dtype=torch.float64 if kind == 2 else i64, device="cuda")
         ctx.check(ctx.lib.laq_gather(ctx.h, src.data_ptr(), kind, row_elems, idx.data_ptr(), n, out.data_ptr(),
                                      2 if kind == 2 else 1))
-        return _out(out[:n], on or isinstance(a, torch.Tensor))
+        return _out(out[:n], on or a_dev)
 
     if isinstance(table, dict):
         for c, a in table.items():
             if len(a) != len(mask):
                 raise errors.ShapeError("apply_mask: mask length mismatch")
-        return {c: gather(a, 1) for c, a in table.items()}
+        return {c: gather(a, 1, isinstance(a, torch.Tensor)) for c, a in table.items()}
     t = dev(table, torch.float64)
     if t.shape[0] != len(mask):
         raise errors.ShapeError("apply_mask: mask length mismatch")
-    return gather(t, t.shape[1])
+    return gather(t, t.shape[1], isinstance(table, torch.Tensor))
