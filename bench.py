@@ -323,16 +323,18 @@ def main():
     plans = [ds.prepare(q) for q in queries]
     sizes = [2 * p.n_groups for p in plans]
     offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
-    # Shared scans: queries of a group reading the same fact columns in the same
-    # roles share one pass when their code tables fit shared memory together
-    # (laq_plans_scan_shared; falls back to one scan per query otherwise).
+    # Batched scans: each query group (the same fact columns, different dials)
+    # is ONE pass with one dictionary-encoded probe per dimension link for the
+    # whole group (laq_batch_*, csrc/ssb_batch.cuh); a group the fused pass
+    # cannot take is scanned query by query with the same results.
     groups = []
     for qi, q in enumerate(queries):
-        if groups and queries[groups[-1][0]].group == q.group and len(groups[-1]) < 3:
+        if groups and queries[groups[-1][0]].group == q.group and len(groups[-1]) < 4:
             groups[-1].append(qi)
         else:
             groups.append([qi])
-    shared_flags = [False] * len(groups)
+    batches = [star.Batch([plans[qi] for qi in grp]) for grp in groups]
+    shared_flags = [b.fused for b in batches]
     ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in groups]
           for _ in range(args.steps)]
     accs = [torch.zeros(int(offs[-1]), dtype=torch.int64, device="cuda") for _ in range(2)]
@@ -344,15 +346,11 @@ def main():
     def launch(k, i=None):
         b = k & 1
         accs[b].zero_()
-        star.build_codes_batch(plans)  # every query's code tables: one launch
         for gi, grp in enumerate(groups):
+            batches[gi].build()  # the group's code tables (dimension filters) + link dictionaries
             if i is not None:
                 ev[i][gi][0].record(stream)
-            if len(grp) > 1:
-                shared_flags[gi] = star.scan_shared([plans[qi] for qi in grp],
-                                                    [accs[b][offs[qi]: offs[qi + 1]] for qi in grp], accumulate=True)
-            else:
-                plans[grp[0]].scan(accs[b][offs[grp[0]]: offs[grp[0] + 1]], accumulate=True)
+            batches[gi].scan([accs[b][offs[qi]: offs[qi + 1]] for qi in grp], accumulate=True)
             if i is not None:
                 ev[i][gi][1].record(stream)
         ctx.allreduce_acc(accs[b])  # C-ABI: ncclAllReduce on the context stream (no-op at N=1)
@@ -395,8 +393,7 @@ def main():
     # ---- roofline of the scan kernel (the dominant kernel), rank 0's shard ----
     scan_ms = np.array([[ev[i][gi][0].elapsed_time(ev[i][gi][1]) for gi in range(len(groups))]
                         for i in range(args.steps)]).mean(axis=0)
-    bytes_per_launch = np.array([plans[grp[0]].bytes_per_row * n_local * (1 if shared_flags[gi] else len(grp))
-                                 for gi, grp in enumerate(groups)], dtype=np.float64)
+    bytes_per_launch = np.array([batches[gi].bytes_per_row * n_local for gi in range(len(groups))], dtype=np.float64)
     achieved = float(bytes_per_launch.sum() / (scan_ms.sum() / 1e3) / 1e9)
     pk, pk_src = peaks()
     peak = float(pk["hbm_gbs"])
@@ -459,9 +456,11 @@ def main():
             "config": W.config(),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "traffic_source": traffic_src,
-                         "kernel": "scan_direct_kernel / scan_shared_kernel (K4, csrc/ssb_scan.cuh, ssb_shared.cu)",
+                         "kernel": "scan_batch_kernel (K4 batched: one pass per query group, csrc/ssb_batch.cu)",
                          "algorithmic_bytes_per_launch": [int(b) for b in bytes_per_launch],
-                         "unit_bytes": "touched fact columns x 4 B per row (Q3.x 12-16 B, Q4.x 20 B; SURVEY §8d)",
+                         "unit_bytes": "the union of the group's touched fact columns x 4 B per row, read once per group (Q3.x: "
+                                       "lo_supplier, lo_orderdate, lo_revenue = 12 B; Q4.x: + lo_part, lo_commitdate "
+                                       "= 20 B; SURVEY §8d)",
                          "peak_source": pk_src + " hbm_gbs (copy bandwidth, burst)",
                          "frac_vs_nominal_7700": achieved / 7700.0},
             "cpu_baseline": cpu,
@@ -474,7 +473,8 @@ def main():
                        "dials_retuned_on_device_match": dials_match, "check_s": round(check_s, 2)},
             "details": {"per_query_scan_ms": dict(zip(["+".join(W.qnames[qi] for qi in grp) for grp in groups],
                                                       per_launch)),
-                        "shared_scan": [bool(f) for f in shared_flags],
+                        "batched_scan": [bool(f) for f in shared_flags],
+                        "batch_not_fused_why": [b.why for b in batches if not b.fused],
                         "result_rows": [int(r.shape[0]) for r in results],
                         "lineorder_rows_per_gpu": n_local,
                         "parallelism": f"row-sharded x{world}, int64 accumulators all-reduced by the C-ABI's "

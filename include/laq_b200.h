@@ -483,6 +483,26 @@ int laq_plans_build_codes(laq_ctx* ctx, int32_t n_plans, laq_plan* const* plans)
 int laq_plans_scan_shared(laq_ctx* ctx, int32_t n_plans, laq_plan* const* plans, int64_t* const* d_accs,
                           int32_t accumulate, int32_t* h_shared);
 int laq_plan_scan(laq_ctx* ctx, laq_plan* plan, int64_t* d_acc, int32_t accumulate);
+/* Batched scan: a batch of 1..4 prepared plans over the same fact table run
+ * as ONE pass (scan_batch_kernel, csrc/ssb_batch.cuh) with one probe per row
+ * per dimension link for the whole batch: each link's per-query codes are
+ * dictionary-encoded on the device (laq_batch_build), staged in shared
+ * memory, and decoded into every query's group id at once.  A batch the
+ * fused pass cannot take (InSet / packed fact columns, > 4096 groups, > 6
+ * links ...) is scanned plan by plan with identical results; *h_fused and
+ * laq_batch_info say which.  Each plan keeps its own accumulator
+ * (laq_plan_emit).  The reference runs the same queries one run_query_laq
+ * (cli.cpp:73-138) at a time; the results are those of each query alone.
+ * The batch borrows the plans: destroy it before them. */
+typedef struct laq_batch laq_batch;
+int laq_batch_prepare(laq_ctx* ctx, int32_t n_plans, laq_plan* const* plans, laq_batch** out, int32_t* h_fused);
+/* Every plan's code tables (one launch) + the link dictionaries (3 launches). */
+int laq_batch_build(laq_ctx* ctx, laq_batch* batch);
+/* d_accs[q]: plan q's [2*G] int64 (count, sum) accumulator. */
+int laq_batch_scan(laq_ctx* ctx, laq_batch* batch, int64_t* const* d_accs, int32_t accumulate);
+int laq_batch_info(const laq_batch* batch, int32_t* fused, int64_t* bytes_per_row, int32_t* n_links, char* why,
+                   size_t why_cap);
+int laq_batch_destroy(laq_batch* batch);
 /* Scan only fact rows [row0, row0 + rows) (row0 a multiple of 4) with the code
  * tables of the last build: lets a caller overlap the upload of later row
  * chunks with the scan of earlier ones (accumulate = 1 after the first chunk). */

@@ -15,6 +15,7 @@
 
 #include "laq/benchgen.hpp"
 #include "laq/cli.hpp"
+#include "laq/oracle.hpp"
 #include "laq/report.hpp"
 #include "laq_dropin.hpp"
 
@@ -33,9 +34,12 @@ static bool same(const DenseMat& a, const DenseMat& b, std::string* why) {
   return r.ok;
 }
 
+static DenseMat oracle_float_measure(const StarSchema& s, const bench::QuerySpec& q);
+
 static void check_query(const StarSchema& s, const bench::QuerySpec& q, const std::string& name) {
   std::string why;
-  const DenseMat want = cli::run_query_oracle(s, q);
+  const bool float_measure = s.fact().schema().kind(s.fact().schema().index_of(q.measure)) == ColKind::Float;
+  const DenseMat want = float_measure ? oracle_float_measure(s, q) : cli::run_query_oracle(s, q);
   setenv("LAQ_DROPIN_PATH", "", 1);
   const DenseMat fast = cli::run_query_laq(s, q);
   setenv("LAQ_DROPIN_PATH", "general", 1);
@@ -45,6 +49,67 @@ static void check_query(const StarSchema& s, const bench::QuerySpec& q, const st
   report(name + " (default path)", ok, why);
   ok = same(gen, want, &why);
   report(name + " (general device path)", ok, why);
+}
+
+// Expected result for a FLOAT measure.  The reference's scalar oracle reads the
+// measure with Table::ints (cli.cpp:194-196), so it cannot check these; the
+// reference's run_query_laq reads it through to_matrix (cli.cpp:96-99), i.e.
+// as doubles, summed per group in ascending fact-row order (groupby_sum_multi,
+// laqops.cpp:415-455; the plain sum is dense_matmul's sequential loop).  Same
+// scalar filter + oracle::star_join + oracle::hash_aggregate as the oracle,
+// with the measure read as doubles.
+static DenseMat oracle_float_measure(const StarSchema& s, const bench::QuerySpec& q) {
+  auto filter = [&](const Table& t, int target) {
+    std::vector<char> keep(static_cast<size_t>(t.row_count()), 1);
+    for (const bench::FilterSpec& f : q.filters) {
+      if (f.target != target) continue;
+      const index_t c = t.schema().index_of(f.column);
+      for (index_t r = 0; r < t.row_count(); ++r)
+        if (keep[r]) keep[r] = t.schema().kind(c) == ColKind::Float ? f.pred.matches(t.floats(c)[r])
+                                                                     : f.pred.matches(t.ints(c)[r]);
+    }
+    std::vector<Column> cols;
+    for (index_t c = 0; c < t.col_count(); ++c) {
+      if (std::holds_alternative<IntColumn>(t.column(c))) {
+        IntColumn d;
+        for (size_t r = 0; r < keep.size(); ++r) if (keep[r]) d.push_back(t.ints(c)[r]);
+        cols.emplace_back(std::move(d));
+      } else {
+        FloatColumn d;
+        for (size_t r = 0; r < keep.size(); ++r) if (keep[r]) d.push_back(t.floats(c)[r]);
+        cols.emplace_back(std::move(d));
+      }
+    }
+    return Table(t.schema(), std::move(cols));
+  };
+  const Table fact = filter(s.fact(), -1);
+  std::vector<Table> dims;
+  for (size_t j = 0; j < q.joins.size(); ++j) dims.push_back(filter(s.dim(q.joins[j].dim_name), static_cast<int>(j)));
+  std::vector<oracle::DimRef> refs;
+  for (size_t j = 0; j < q.joins.size(); ++j) refs.push_back({&dims[j], q.joins[j].fact_fk, q.joins[j].dim_pk});
+  const oracle::StarMatch m = oracle::star_join(fact, refs);
+  const FloatColumn& mv = fact.floats(q.measure);
+  std::vector<double> vals;
+  for (index_t r : m.fact_rows) vals.push_back(mv[r]);
+  if (q.group_by.empty()) {
+    double sum = 0;
+    for (double v : vals) sum += v;
+    return DenseMat(1, 1, {sum});
+  }
+  std::vector<IntColumn> gcols;
+  for (const bench::GroupRef& g : q.group_by) {
+    IntColumn col;
+    const IntColumn& src = g.target < 0 ? fact.ints(g.column) : dims[g.target].ints(g.column);
+    for (size_t i = 0; i < m.fact_rows.size(); ++i) col.push_back(src[g.target < 0 ? m.fact_rows[i] : m.dim_rows[g.target][i]]);
+    gcols.push_back(std::move(col));
+  }
+  const auto agg = oracle::hash_aggregate(gcols, vals);
+  DenseMat out(static_cast<index_t>(agg.size()), static_cast<index_t>(q.group_by.size()) + 1);
+  for (size_t r = 0; r < agg.size(); ++r) {
+    for (size_t c = 0; c < agg[r].keys.size(); ++c) out(static_cast<index_t>(r), static_cast<index_t>(c)) = static_cast<double>(agg[r].keys[c]);
+    out(static_cast<index_t>(r), static_cast<index_t>(q.group_by.size())) = agg[r].sum;
+  }
+  return out;
 }
 
 // A star with extra fact columns: a float measure and 64-bit integers.

@@ -118,6 +118,11 @@ _SIGS = {
     "laq_plans_build_codes": (C.c_int, [vp, i32, vp]),
     "laq_plans_scan_shared": (C.c_int, [vp, i32, vp, vp, i32, i32p]),
     "laq_plan_scan": (C.c_int, [vp, vp, vp, i32]),
+    "laq_batch_prepare": (C.c_int, [vp, i32, vp, C.POINTER(vp), i32p]),
+    "laq_batch_build": (C.c_int, [vp, vp]),
+    "laq_batch_scan": (C.c_int, [vp, vp, vp, i32]),
+    "laq_batch_info": (C.c_int, [vp, i32p, i64p, i32p, C.c_char_p, C.c_size_t]),
+    "laq_batch_destroy": (C.c_int, [vp]),
     "laq_plan_scan_range": (C.c_int, [vp, vp, i64, i64, vp, i32]),
     "laq_plan_bytes_per_row": (i64, [vp]),
     "laq_plan_scanned_links": (i32, [vp]),

@@ -31,6 +31,7 @@
 
 #include "ssb_launch.cuh"
 #include "ssb_shared.cuh"
+#include "ssb_batch.cuh"
 
 namespace laq {
 namespace {
@@ -1348,6 +1349,398 @@ int laq_measure_selectivity(laq_ctx* ctx, const laq_star* s, const laq_query_des
   });
   laq_plan_destroy(p);
   return rc;
+}
+
+}  // extern "C"
+
+// ---- batched scan (ssb_batch.cuh): a batch of plans, one pass, one probe per link ----
+
+struct laq_batch {
+  laq_ctx* ctx = nullptr;
+  std::vector<laq_plan*> plans;
+  bool fused = false;
+  std::string why;  // why the batch is scanned plan by plan (empty when fused)
+  int nl = 0, nf = 0, mode = 0;
+  scan::BatchScan B{};
+  scan::DictArgs D{};
+  DevMem<unsigned long long> hkeys;  // every link's hash table, one allocation
+  DevMem<int32_t> hid;
+  size_t hkey_count = 0;
+  std::vector<DevMem<uint8_t>> ids;
+  std::vector<DevMem<uint32_t>> bm;
+  std::vector<DevMem<unsigned long long>> dec;
+  DevMem<int> counts;  // [kBatchMaxLinks] tuple ids per link, [kBatchMaxLinks] overflow
+  size_t smem = 0;
+  int grid = 1;
+  int64_t bytes_per_row = 0;
+  std::vector<int> n_dec;
+};
+
+namespace laq {
+namespace {
+
+int ceil_log2(int64_t v) {
+  int b = 0;
+  while ((int64_t{1} << b) < v) ++b;
+  return b;
+}
+
+// (Re)allocate the dictionary of every link: hash tables sized for `cap`
+// tuples per link, id tables of width idw[j], decode tables of cap[j] entries.
+void batch_alloc_dict(laq_batch* b, const std::vector<int64_t>& cap, const std::vector<int>& idw,
+                      const std::vector<char>& want_bm) {
+  scan::DictArgs& D = b->D;
+  size_t total = 0;
+  std::vector<int> hb(b->nl);
+  for (int j = 0; j < b->nl; ++j) {
+    hb[j] = std::max(6, ceil_log2(2 * cap[j]));
+    total += size_t{1} << hb[j];
+  }
+  b->hkeys = DevMem<unsigned long long>(total);
+  b->hid = DevMem<int32_t>(total);
+  b->hkey_count = total;
+  b->ids.clear();
+  b->bm.clear();
+  b->dec.clear();
+  size_t off = 0;
+  for (int j = 0; j < b->nl; ++j) {
+    scan::DictLink& L = D.l[j];
+    L.hkeys = b->hkeys.get() + off;
+    L.hid = b->hid.get() + off;
+    L.hbits = hb[j];
+    off += size_t{1} << hb[j];
+    L.idw = idw[j];
+    b->ids.emplace_back(static_cast<size_t>(((L.slots * idw[j]) + 15) & ~int64_t{15}));
+    L.ids = b->ids.back().get();
+    b->dec.emplace_back(static_cast<size_t>((cap[j] + 1) & ~int64_t{1}));  // 16-byte multiple
+    L.dec = b->dec.back().get();
+    L.dec_cap = static_cast<int>(cap[j]);
+    if (want_bm[j]) {
+      b->bm.emplace_back(static_cast<size_t>((((L.slots + 31) / 32) + 3) & ~int64_t{3}));
+      L.bm = b->bm.back().get();
+    } else {
+      b->bm.emplace_back();
+      L.bm = nullptr;
+    }
+  }
+}
+
+void batch_build(laq_ctx* ctx, laq_batch* b, bool dict) {
+  const int n = static_cast<int>(b->plans.size());
+  if (!build_codes_fused(ctx, b->plans.data(), n))
+    for (auto* p : b->plans) build_codes(ctx, p);
+  if (!dict) return;
+  LAQ_CUDA(cudaMemsetAsync(b->hkeys.get(), 0xFF, b->hkey_count * sizeof(unsigned long long), ctx->stream));
+  LAQ_CUDA(cudaMemsetAsync(b->counts.get(), 0, 2 * scan::kBatchMaxLinks * sizeof(int), ctx->stream));
+  scan::launch_dict_build(ctx, b->D);
+}
+
+// Decide whether a batch runs fused and lay it out; b->why says why not.
+void batch_prepare(laq_ctx* ctx, laq_batch* b) {
+  using namespace scan;
+  const int nq = static_cast<int>(b->plans.size());
+  auto reject = [&](const std::string& why) {
+    b->fused = false;
+    b->why = why;
+  };
+  if (std::getenv("LAQ_NO_BATCH_SCAN")) return reject("LAQ_NO_BATCH_SCAN");
+  if (nq < 1 || nq > kBatchMaxQ) return reject("batch of 1..4 plans");
+  const laq_plan* p0 = b->plans[0];
+  if (p0->fact_rows == 0) return reject("empty fact table");
+  int mode = 0;
+  for (const laq_plan* p : b->plans) {
+    const ScanArgs& a = p->scan;
+    if (p->variant != 4) return reject("a plan is not on the direct int32 scan");
+    if (p->fact_rows != p0->fact_rows) return reject("plans over different fact tables");
+    if (p->mode > 1 || (p->mode == 1 && !a.narrow_bins)) return reject("wide group bins");
+    if (p->G > kLaneFail) return reject("more than 4096 groups");
+    if ((a.measure == nullptr) != (p0->scan.measure == nullptr) || (a.measure && a.mc.p != p0->scan.mc.p))
+      return reject("different measures");
+    if (a.measure && a.mc.w != 4) return reject("packed measure");
+    mode = std::max(mode, p->mode);
+  }
+  // Union of links (keyed by the fact FK column) and of fact filter columns.
+  struct U {
+    const void* col;
+    Col c;
+    uint32_t base, size;
+    int64_t slots;
+    const int32_t* code[kBatchMaxQ];
+  };
+  std::vector<U> links;
+  std::vector<std::pair<const void*, Col>> fcols;
+  int32_t flo[kBatchMaxFilters][kBatchMaxQ], fhi[kBatchMaxFilters][kBatchMaxQ];
+  uint32_t reject_mask = 0;
+  for (int f = 0; f < kBatchMaxFilters; ++f)
+    for (int q = 0; q < kBatchMaxQ; ++q) flo[f][q] = INT32_MIN, fhi[f][q] = INT32_MAX;
+  for (int q = 0; q < nq; ++q) {
+    const laq_plan* p = b->plans[q];
+    const ScanArgs& a = p->scan;
+    for (int t = 0; t < p->nl; ++t) {
+      const LinkProbe& lp = a.link[t];
+      if (lp.kind != PROBE_DIRECT || a.fkc[t].w != 4) return reject("non-direct link or packed key column");
+      int u = -1;
+      for (size_t k = 0; k < links.size(); ++k)
+        if (links[k].col == a.fkc[t].p) u = static_cast<int>(k);
+      if (u < 0) {
+        if (links.size() == static_cast<size_t>(kBatchMaxLinks)) return reject("more than 6 distinct links");
+        U x{a.fkc[t].p, a.fkc[t], static_cast<uint32_t>(lp.base), static_cast<uint32_t>(lp.size),
+            std::max<int64_t>(lp.size, 1), {}};
+        links.push_back(x);
+        u = static_cast<int>(links.size()) - 1;
+      }
+      U& x = links[u];
+      if (x.base != static_cast<uint32_t>(lp.base) || x.size != static_cast<uint32_t>(lp.size))
+        return reject("one FK column probed into different dimensions");
+      if (x.code[q]) return reject("a plan joins one FK column twice");
+      x.code[q] = lp.code;
+    }
+    for (int f = 0; f < p->nf; ++f) {
+      const FactFilter& ff = a.ff[f];
+      if (ff.inset || a.ffc[f].w != 4) return reject("InSet or packed fact filter");
+      int u = -1;
+      for (size_t k = 0; k < fcols.size(); ++k)
+        if (fcols[k].first == a.ffc[f].p) u = static_cast<int>(k);
+      if (u < 0) {
+        if (fcols.size() == 2) return reject("more than 2 fact filter columns");
+        fcols.emplace_back(a.ffc[f].p, a.ffc[f]);
+        u = static_cast<int>(fcols.size()) - 1;
+      }
+      if (ff.lo > ff.hi) reject_mask |= 1u << q;  // an empty interval: the query matches no row
+      flo[u][q] = std::max(flo[u][q], ff.lo);
+      fhi[u][q] = std::min(fhi[u][q], ff.hi);
+      if (flo[u][q] > fhi[u][q]) reject_mask |= 1u << q;
+    }
+  }
+  if (links.empty()) return reject("no links");
+  b->nl = static_cast<int>(links.size());
+  b->nf = static_cast<int>(fcols.size());
+  b->mode = mode;
+
+  // Dictionaries, first pass: room for every slot's tuple (uint16 ids).
+  DictArgs& D = b->D;
+  D = DictArgs{};
+  D.nl = b->nl;
+  D.nq = nq;
+  b->counts = DevMem<int>(2 * kBatchMaxLinks);
+  D.n_dec = b->counts.get();
+  D.overflow = b->counts.get() + kBatchMaxLinks;
+  std::vector<int64_t> cap(b->nl);
+  for (int j = 0; j < b->nl; ++j) {
+    DictLink& L = D.l[j];
+    L.slots = links[j].slots;
+    unsigned long long miss = 0;
+    for (int q = 0; q < nq; ++q) {
+      L.code[q] = links[j].code[q];
+      if (L.code[q]) miss |= static_cast<unsigned long long>(kLaneFail) << (16 * q);
+    }
+    L.miss = miss;
+    D.start[j + 1] = D.start[j] + ((L.slots + 31) & ~int64_t{31});
+    cap[j] = std::min<int64_t>(L.slots + 1, 65536);
+  }
+  batch_alloc_dict(b, cap, std::vector<int>(b->nl, 2), std::vector<char>(b->nl, 0));
+  batch_build(ctx, b, true);
+  int h[2 * kBatchMaxLinks];
+  LAQ_CUDA(cudaMemcpyAsync(h, b->counts.get(), sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  for (int j = 0; j < b->nl; ++j)
+    if (h[kBatchMaxLinks]) return reject("more than 65535 distinct code tuples on a link");
+  b->n_dec.assign(h, h + b->nl);
+
+  // Pass fraction of each link (slots some joining query keeps), host side, once.
+  std::vector<double> frac(b->nl, 1.0);
+  for (int j = 0; j < b->nl; ++j) {
+    const DictLink& L = D.l[j];
+    std::vector<uint16_t> ids(static_cast<size_t>(L.slots));
+    std::vector<unsigned long long> dec(static_cast<size_t>(b->n_dec[j]));
+    LAQ_CUDA(cudaMemcpy(ids.data(), L.ids, ids.size() * 2, cudaMemcpyDeviceToHost));
+    LAQ_CUDA(cudaMemcpy(dec.data(), L.dec, dec.size() * 8, cudaMemcpyDeviceToHost));
+    std::vector<char> keep(dec.size(), 0);
+    for (size_t t = 0; t < dec.size(); ++t)
+      for (int q = 0; q < nq; ++q)
+        if (L.code[q] && ((dec[t] >> (16 * q)) & 0xFFFF) < kLaneFail) keep[t] = 1;
+    int64_t k = 0;
+    for (uint16_t v : ids) k += keep[v];
+    frac[j] = static_cast<double>(k) / static_cast<double>(std::max<int64_t>(L.slots, 1));
+  }
+
+  // Shared-memory layout: bins, decode tables, then id tables smallest first,
+  // then any-pass bitmaps for the links left in global memory.
+  int optin = 0;
+  LAQ_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+  int64_t room = static_cast<int64_t>(optin) - 2048;
+  int64_t bins = 0;
+  if (mode == 1)
+    for (const laq_plan* p : b->plans) bins += (8 * p->G + 15) & ~int64_t{15};
+  std::vector<int64_t> decb(b->nl), idb(b->nl), bmb(b->nl);
+  std::vector<int> idw(b->nl);
+  for (int j = 0; j < b->nl; ++j) {
+    decb[j] = (8 * int64_t{b->n_dec[j]} + 15) & ~int64_t{15};
+    idw[j] = b->n_dec[j] <= 256 ? 1 : 2;
+    idb[j] = (D.l[j].slots * idw[j] + 15) & ~int64_t{15};
+    bmb[j] = (((D.l[j].slots + 31) / 32) * 4 + 15) & ~int64_t{15};
+    room -= decb[j];
+  }
+  room -= bins;
+  if (room < 0) return reject("decode tables and bins exceed shared memory");
+  std::vector<int> by(b->nl);
+  std::iota(by.begin(), by.end(), 0);
+  std::stable_sort(by.begin(), by.end(), [&](int x, int y) { return idb[x] < idb[y]; });
+  std::vector<char> staged(b->nl, 0), use_bm(b->nl, 0);
+  for (int j : by)
+    if (!std::getenv("LAQ_NOSMEMTAB") && idb[j] <= room) staged[j] = 1, room -= idb[j];
+  for (int j : by)
+    if (!staged[j] && bmb[j] <= room && frac[j] < 0.75) use_bm[j] = 1, room -= bmb[j];
+
+  // Final dictionaries: exact capacities and id widths.
+  for (int j = 0; j < b->nl; ++j) cap[j] = b->n_dec[j];
+  batch_alloc_dict(b, cap, idw, use_bm);
+
+  // Probe order: shared-memory links first, then L2 gathers; most selective first.
+  std::vector<int> order(b->nl);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+    if (staged[x] != staged[y]) return staged[x] > staged[y];
+    return frac[x] < frac[y];
+  });
+  BatchScan& B = b->B;
+  B = BatchScan{};
+  B.n = p0->fact_rows;
+  B.nq = nq;
+  int64_t off = 0;
+  bool gathers = false;
+  for (int t = 0; t < b->nl; ++t) {  // kernel link t = union link order[t]
+    const int j = order[t];
+    const DictLink& L = D.l[j];
+    BatchLink& K = B.link[t];
+    K.base = links[j].base;
+    K.size = links[j].size;
+    K.miss = static_cast<uint32_t>(b->n_dec[j] - 1);
+    K.ids = L.ids;
+    K.dec = L.dec;
+    K.bm = L.bm;
+    K.fmt = staged[j] ? (idw[j] == 1 ? kIdSmemU8 : kIdSmemU16) : (idw[j] == 1 ? kIdGlobU8 : kIdGlobU16);
+    K.dec_byte = static_cast<int>(off);
+    K.dec_bytes = static_cast<int>(decb[j]);
+    off += decb[j];
+    B.fkc[t] = links[j].c;
+    gathers = gathers || !staged[j];
+  }
+  for (int t = 0; t < b->nl; ++t) {
+    const int j = order[t];
+    BatchLink& K = B.link[t];
+    K.id_byte = 0;
+    K.id_bytes = 0;
+    if (staged[j]) {
+      K.id_byte = static_cast<int>(off);
+      K.id_bytes = static_cast<int>(idb[j]);
+      off += idb[j];
+    }
+    K.bm_byte = -1;
+    if (use_bm[j]) {
+      K.bm_byte = static_cast<int>(off);
+      K.bm_bytes = static_cast<int>(bmb[j]);
+      off += bmb[j];
+    }
+  }
+  B.smem_stage_bytes = static_cast<int>(off);
+  for (int f = 0; f < b->nf; ++f) {
+    B.ffc[f] = fcols[f].second;
+    for (int q = 0; q < kBatchMaxQ; ++q) B.ff_lo[f][q] = flo[f][q], B.ff_hi[f][q] = fhi[f][q];
+  }
+  B.has_measure = p0->scan.measure ? 1 : 0;
+  B.mc = p0->scan.mc;
+  int64_t flush = INT64_MAX;
+  for (int q = 0; q < nq; ++q) {
+    const laq_plan* p = b->plans[q];
+    B.G[q] = p->G;
+    if (mode == 1) {
+      B.bins_byte[q] = static_cast<int>(off);
+      off += (8 * p->G + 15) & ~int64_t{15};
+    }
+    flush = std::min<int64_t>(flush, std::max<int64_t>(1, p->scan.flush_every));
+  }
+  B.reject_mask = reject_mask;
+  B.flush_every = flush;
+  B.prefetch = gathers ? 2 : 0;
+  if (const char* pf = std::getenv("LAQ_PREFETCH")) B.prefetch = std::atoi(pf);
+  b->smem = static_cast<size_t>(off);
+  b->grid = ctx->sm_count;
+  b->bytes_per_row = 4 * (b->nl + b->nf + B.has_measure);
+  b->fused = true;
+  b->why.clear();
+  batch_build(ctx, b, true);  // leave the batch ready to scan
+}
+
+}  // namespace
+}  // namespace laq
+
+extern "C" {
+
+int laq_batch_prepare(laq_ctx* ctx, int32_t n_plans, laq_plan* const* plans, laq_batch** out, int32_t* h_fused) {
+  return guard(ctx, [&] {
+    if (n_plans < 1) fail(LAQ_ERR_SHAPE, "empty plan batch");
+    auto b = std::make_unique<laq_batch>();
+    b->ctx = ctx;
+    b->plans.assign(plans, plans + n_plans);
+    batch_prepare(ctx, b.get());
+    if (!b->fused) {
+      b->hkeys = DevMem<unsigned long long>();
+      b->ids.clear();
+      b->dec.clear();
+      b->bm.clear();
+    }
+    if (h_fused) *h_fused = b->fused ? 1 : 0;
+    *out = b.release();
+  });
+}
+
+int laq_batch_build(laq_ctx* ctx, laq_batch* b) {
+  return guard(ctx, [&] { batch_build(ctx, b, b->fused); });
+}
+
+int laq_batch_scan(laq_ctx* ctx, laq_batch* b, int64_t* const* d_accs, int32_t accumulate) {
+  return guard(ctx, [&] {
+    const int nq = static_cast<int>(b->plans.size());
+    if (!accumulate)
+      for (int q = 0; q < nq; ++q)
+        LAQ_CUDA(cudaMemsetAsync(d_accs[q], 0, 2 * b->plans[q]->G * sizeof(int64_t), ctx->stream));
+    if (b->fused) {
+      scan::BatchScan B = b->B;
+      for (int q = 0; q < nq; ++q) B.acc[q] = reinterpret_cast<unsigned long long*>(d_accs[q]);
+      scan::launch_batch(ctx, B, b->nl, b->nf, b->mode, b->smem, b->grid);
+      return;
+    }
+    for (int q = 0; q < nq; ++q) {
+      laq_plan* p = b->plans[q];
+      if (p->fact_rows == 0) continue;
+      ScanArgs a = p->scan;
+      a.acc = reinterpret_cast<unsigned long long*>(d_accs[q]);
+      launch_scan(ctx, a, p->nl, p->nf, p->mode, p->variant, p->vec, p->grid, p->smem);
+    }
+  });
+}
+
+int laq_batch_info(const laq_batch* b, int32_t* fused, int64_t* bytes_per_row, int32_t* n_links, char* why,
+                   size_t why_cap) {
+  if (!b) return LAQ_ERR_GENERIC;
+  if (fused) *fused = b->fused ? 1 : 0;
+  if (bytes_per_row) {
+    int64_t s = 0;
+    for (const laq_plan* p : b->plans) s += p->bytes_per_row;
+    *bytes_per_row = b->fused ? b->bytes_per_row : s;
+  }
+  if (n_links) *n_links = b->nl;
+  if (why && why_cap) {
+    std::strncpy(why, b->why.c_str(), why_cap - 1);
+    why[why_cap - 1] = 0;
+  }
+  return LAQ_OK;
+}
+
+int laq_batch_destroy(laq_batch* b) {
+  delete b;
+  return LAQ_OK;
 }
 
 }  // extern "C"

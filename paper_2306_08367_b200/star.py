@@ -264,6 +264,57 @@ def scan_shared(plans, accs, accumulate=False) -> bool:
     return bool(shared.value)
 
 
+class Batch:
+    """A batch of 1..4 plans over the same fact table scanned in ONE pass with
+    one probe per link for the whole batch (laq_batch_*, csrc/ssb_batch.cuh).
+    build() = every plan's code tables + the link dictionaries; scan(accs)
+    fills each plan's own accumulator, exactly as plan.scan would.  Batches the
+    fused pass cannot take are scanned plan by plan (`fused` False, `why`)."""
+
+    def __init__(self, plans):
+        self.plans = list(plans)
+        self.ctx = self.plans[0].ctx
+        hp = (C.c_void_p * len(self.plans))(*[p.h.value for p in self.plans])
+        h = C.c_void_p()
+        fused = C.c_int32()
+        self.ctx.check(self.ctx.lib.laq_batch_prepare(self.ctx.h, len(self.plans), hp, C.byref(h), C.byref(fused)))
+        self.h = h
+        f, bpr, nl = C.c_int32(), C.c_int64(), C.c_int32()
+        why = C.create_string_buffer(256)
+        self.ctx.lib.laq_batch_info(self.h, C.byref(f), C.byref(bpr), C.byref(nl), why, 256)
+        self.fused = bool(f.value)
+        self.bytes_per_row = int(bpr.value)
+        self.n_links = int(nl.value)
+        self.why = why.value.decode()
+
+    def build(self):
+        self.ctx.check(self.ctx.lib.laq_batch_build(self.ctx.h, self.h))
+
+    def scan(self, accs=None, accumulate=False):
+        accs = [p.acc for p in self.plans] if accs is None else list(accs)
+        ha = (C.c_void_p * len(accs))(*[a.data_ptr() for a in accs])
+        self.ctx.check(self.ctx.lib.laq_batch_scan(self.ctx.h, self.h, ha, 1 if accumulate else 0))
+        return accs
+
+    def run(self):
+        """Build + scan + emit every plan's result rows."""
+        self.ctx.bind_stream()
+        self.build()
+        accs = self.scan()
+        return [p.emit(a.cpu().numpy()) for p, a in zip(self.plans, accs)]
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.laq_batch_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def upload_gen_star(g, ctx=None, row_range=None) -> DeviceStar:
     """Upload a gen.GenStar (or oracle RefStar-like object with .tables/.kinds/.links())."""
     links = g.links() if callable(getattr(g, "links", None)) else g.links
