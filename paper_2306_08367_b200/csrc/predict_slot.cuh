@@ -21,6 +21,7 @@
 #pragma once
 
 #include "probe.cuh"
+#include "tc.cuh"
 
 namespace laq {
 namespace slot {
@@ -44,6 +45,9 @@ struct Args {
   int p_off[kMaxLinks];             // >= 0: partials staged in smem at this double offset (l == 1)
   int smem_words;                   // staged bitmap words
   int smem_doubles;                 // staged partial doubles (after the bitmaps, 8-byte aligned)
+  int bulk_bytes;                   // > 0: direct kernel stages with TMA bulk copies (16-byte granules)
+  int bits_bytes[kMaxLinks];        // bulk bytes of each staged bitmap / partial table
+  int p_bytes[kMaxLinks];
   double* y;
   int64_t* survivors;
   unsigned long long* tile_state;
@@ -190,17 +194,49 @@ __global__ void __launch_bounds__(kWarpThreads) count_chunks_kernel(const Args a
 // BT threads per CTA: 1024 by default -- one CTA per SM holds ONE staged copy
 // of the partials (80 KB for cfg1), so residency is 32 warps/SM instead of the
 // 16 that two 256-thread CTAs with a copy each allow.
+// ONE-launch form (last != nullptr, small inputs): the last CTA to finish
+// (done counter) takes the miss decision on the device -- no miss: *nnz = n;
+// misses: it compacts the rows in place itself (tail_compact) -- and resets
+// the counters, so a call is a single launch and graph replays stay exact.
+template <int NL>
+__device__ void tail_compact(const Args& a, const uint32_t* s_bits, int64_t n_chunks, const int* counts,
+                             int64_t* offsets);
+
 template <int NL, int BT = kWarpThreads>
 __global__ void __launch_bounds__(BT, 1) direct_chunks_kernel(const Args a, int64_t n_chunks, int* counts,
-                                                                     unsigned long long* miss) {
+                                                                     unsigned long long* miss,
+                                                                     unsigned long long* last = nullptr,
+                                                                     int64_t* offsets = nullptr) {
   extern __shared__ __align__(16) uint32_t s_bits[];
   double* s_p = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(s_bits) + ((a.smem_words * 4 + 15) & ~15));
-  stage_bits(a, s_bits, NL);
+  if (a.bulk_bytes > 0) {
+    // One thread hands every staged table (bitmaps, slot-ordered partials) to
+    // the TMA engine; the CTA waits once on the mbarrier.  (A per-thread copy
+    // loop is a chain of dependent L2 round trips: at 1M rows it was most of
+    // the call.)
+    __shared__ __align__(8) uint64_t s_bar;
+    if (threadIdx.x == 0) {
+      tc::mbar_init(&s_bar, 1);
+      tc::fence_mbar_init();
+      tc::mbar_arrive_expect_tx(&s_bar, static_cast<uint32_t>(a.bulk_bytes));
 #pragma unroll
-  for (int j = 0; j < NL; ++j)
-    if (a.p_off[j] >= 0)
-      for (int64_t s = threadIdx.x; s < a.size[j]; s += BT) s_p[a.p_off[j] + s] = __ldg(a.pslot[j] + s);
-  __syncthreads();
+      for (int j = 0; j < NL; ++j) {
+        if (a.bits_off[j] >= 0)
+          tc::bulk_g2s(tc::smem_u32(s_bits + a.bits_off[j]), a.bits[j], static_cast<uint32_t>(a.bits_bytes[j]), &s_bar);
+        if (a.p_off[j] >= 0)
+          tc::bulk_g2s(tc::smem_u32(s_p + a.p_off[j]), a.pslot[j], static_cast<uint32_t>(a.p_bytes[j]), &s_bar);
+      }
+    }
+    __syncthreads();
+    tc::mbar_wait(&s_bar, 0);
+  } else {
+    stage_bits(a, s_bits, NL);
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+      if (a.p_off[j] >= 0)
+        for (int64_t s = threadIdx.x; s < a.size[j]; s += BT) s_p[a.p_off[j] + s] = __ldg(a.pslot[j] + s);
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (BT / 32);
   auto pval = [&](int j, uint32_t s) -> double {
@@ -245,6 +281,94 @@ __global__ void __launch_bounds__(BT, 1) direct_chunks_kernel(const Args a, int6
       if (cnt != rows) atomicAdd(miss, 1ull);
     }
   }
+  if (last == nullptr) return;
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(last, 1ull) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const unsigned long long m = *reinterpret_cast<volatile unsigned long long*>(miss);
+  if (m == 0) {
+    if (threadIdx.x == 0) *a.nnz = a.n;
+  } else {
+    tail_compact<NL>(a, s_bits, n_chunks, counts, offsets);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *miss = 0;
+    *last = 0;
+  }
+}
+
+// The rare miss path of the one-launch form, run by the last CTA alone:
+// exclusive scan of the chunk counts, then every chunk's surviving rows moved
+// down to their compacted position in ascending chunk order (a chunk's
+// destination never reaches past its own start, so reading the whole chunk
+// before writing it keeps the in-place move exact).
+template <int NL>
+__device__ void tail_compact(const Args& a, const uint32_t* s_bits, int64_t n_chunks, const int* counts,
+                             int64_t* offsets) {
+  __shared__ int64_t s_warp[33];
+  __shared__ int64_t s_base, s_total;
+  const int t = threadIdx.x, nt = blockDim.x, lane = t & 31, warp = t >> 5, nw = nt / 32;
+  if (t == 0) {
+    int64_t run = 0;
+    for (int64_t c = 0; c < n_chunks; ++c) {
+      offsets[c] = run;
+      run += *reinterpret_cast<const volatile int*>(counts + c);
+    }
+    s_total = run;
+  }
+  __syncthreads();
+  for (int64_t c = 0; c < n_chunks; ++c) {
+    if (t == 0) s_base = offsets[c];
+    __syncthreads();
+    const int64_t end = min(a.n, (c + 1) * kChunkRows);
+    for (int64_t r0 = c * kChunkRows; r0 < end; r0 += nt) {
+      const int64_t r = r0 + t;
+      bool ok = r < end;
+      if (ok)
+#pragma unroll
+        for (int j = 0; j < NL; ++j) {
+          const int32_t key = a.fk[j][r];
+          const uint32_t sl = static_cast<uint32_t>(key) - static_cast<uint32_t>(a.base[j]);
+          bool o = key >= 0 && sl < static_cast<uint32_t>(a.size[j]);
+          if (o) {
+            const uint32_t word = a.bits_off[j] >= 0 ? s_bits[a.bits_off[j] + (sl >> 5)] : __ldg(a.bits[j] + (sl >> 5));
+            o = (word >> (sl & 31)) & 1u;
+          }
+          ok = ok && o;
+        }
+      const unsigned bal = __ballot_sync(0xffffffffu, ok);
+      if (lane == 0) s_warp[warp] = __popc(bal);
+      __syncthreads();
+      if (t == 0) {
+        int64_t x = 0;
+        for (int w = 0; w < nw; ++w) {
+          const int64_t v = s_warp[w];
+          s_warp[w] = x;
+          x += v;
+        }
+        s_warp[nw] = x;
+      }
+      __syncthreads();
+      const int64_t dst = s_base + s_warp[warp] + __popc(bal & ((1u << lane) - 1u));
+      const double v = ok ? a.y[r] : 0.0;
+      __syncthreads();  // every read of the slice before any write
+      if (ok) {
+        a.y[dst] = v;
+        if (a.survivors) a.survivors[dst] = r;
+      }
+      __syncthreads();
+      if (t == 0) s_base += s_warp[nw];
+      __syncthreads();
+    }
+  }
+  if (t == 0) *a.nnz = s_total;
 }
 
 // Exclusive scan of the per-chunk survivor counts (one 1024-thread CTA: each

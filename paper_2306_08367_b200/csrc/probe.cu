@@ -430,7 +430,8 @@ struct laq_probe {
   // optimistic single pass: [0] chunks with a missing key (counted by the
   // direct pass, moved to [1] and cleared by the scan pass), [1] the decision
   // the write pass reads
-  DevMem<unsigned long long> miss{2};
+  // [2] CTAs finished (the one-launch form's last-CTA counter, reset by that CTA)
+  DevMem<unsigned long long> miss{3};
 };
 
 namespace laq {
@@ -447,9 +448,11 @@ void bind_slots(laq_ctx* ctx, laq_probe* p, const double* const* d_P, int64_t l)
   for (int j = 0; j < p->n_links; ++j) {
     const Probe& pr = p->probes[j];
     const int64_t size = pr.size;
-    const int64_t words = std::max<int64_t>(1, (size + 31) / 32);
-    if (p->pslot_l != l || p->pslot[j].n < static_cast<size_t>(std::max<int64_t>(size * l, 1))) {
-      p->pslot[j] = DevMem<double>(static_cast<size_t>(std::max<int64_t>(size * l, 1)));
+    // padded to 16-byte granules (TMA bulk staging, run_slot_predict)
+    const int64_t words = (std::max<int64_t>(1, (size + 31) / 32) + 3) & ~int64_t{3};
+    const int64_t doubles = (std::max<int64_t>(size * l, 1) + 1) & ~int64_t{1};
+    if (p->pslot_l != l || p->pslot[j].n < static_cast<size_t>(doubles) || p->bits[j].n < static_cast<size_t>(words)) {
+      p->pslot[j] = DevMem<double>(static_cast<size_t>(doubles));
       p->bits[j] = DevMem<uint32_t>(static_cast<size_t>(words));
     }
     LAQ_CUDA(cudaMemsetAsync(p->bits[j].get(), 0, words * sizeof(uint32_t), ctx->stream));
@@ -485,10 +488,15 @@ void run_slot_predict(laq_ctx* ctx, laq_probe* p, const int32_t* const* d_fks, i
   }
   // Shared-memory staging of the existence bitmaps that fit (partials are
   // gathered through L1: high occupancy matters more than staging them).
+  // Tables start on 16-byte boundaries and span whole 16-byte granules (the
+  // direct kernel stages them with TMA bulk copies; the sources are padded).
+  int64_t bulk = 0;
   for (int j = 0; j < p->n_links; ++j) {
-    const int64_t words = std::max<int64_t>(1, (a.size[j] + 31) / 32);
+    const int64_t words = (std::max<int64_t>(1, (a.size[j] + 31) / 32) + 3) & ~int64_t{3};
     if ((words_total + words) * 4 <= 32 * 1024) {
       a.bits_off[j] = static_cast<int>(words_total);
+      a.bits_bytes[j] = static_cast<int>(words * 4);
+      bulk += words * 4;
       words_total += words;
     }
   }
@@ -497,12 +505,17 @@ void run_slot_predict(laq_ctx* ctx, laq_probe* p, const int32_t* const* d_fks, i
   // (shared-memory gathers instead of one L1 wavefront per lane).
   int64_t doubles = 0;
   if (l == 1)
-    for (int j = 0; j < p->n_links; ++j)
-      if ((doubles + a.size[j]) * 8 <= 96 * 1024) {
+    for (int j = 0; j < p->n_links; ++j) {
+      const int64_t d = (std::max<int64_t>(a.size[j], 1) + 1) & ~int64_t{1};
+      if ((doubles + d) * 8 <= 96 * 1024) {
         a.p_off[j] = static_cast<int>(doubles);
-        doubles += a.size[j];
+        a.p_bytes[j] = static_cast<int>(d * 8);
+        bulk += d * 8;
+        doubles += d;
       }
+    }
   a.smem_doubles = static_cast<int>(doubles);
+  a.bulk_bytes = std::getenv("LAQ_PREDICT_NO_BULK") ? 0 : static_cast<int>(bulk);
   a.y = d_out;
   a.survivors = d_survivors;
   a.nnz = d_nnz;
@@ -521,6 +534,11 @@ void run_slot_predict(laq_ctx* ctx, laq_probe* p, const int32_t* const* d_fks, i
   // l == 1 and no LAQ_PREDICT_TWO_PASS: optimistic single pass + device-decided
   // compaction fallback (direct_chunks_kernel); otherwise count + scan + write.
   const bool optimistic = l == 1 && !std::getenv("LAQ_PREDICT_TWO_PASS");
+  // Small inputs (<= 4M rows): one launch per call (launch latency dominates
+  // there: 1M rows = 12 MB = 1.8 us of HBM time); the miss path is compacted by
+  // the last CTA.  LAQ_PREDICT_ONE_LAUNCH=0 keeps the three-launch form.
+  const char* ol = std::getenv("LAQ_PREDICT_ONE_LAUNCH");
+  const bool one_launch = optimistic && n_chunks <= 4096 && !(ol && std::string(ol) == "0");
   unsigned long long* miss = p->miss.get();
   unsigned long long* decision = p->miss.get() + 1;
   auto launch = [&](auto count_k, auto direct_k, auto direct_small_k, auto write_k) {
@@ -534,12 +552,19 @@ void run_slot_predict(laq_ctx* ctx, laq_probe* p, const int32_t* const* d_fks, i
     if (optimistic && big) {
       LAQ_CUDA(cudaFuncSetAttribute(direct_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_w)));
       const unsigned g0 = static_cast<unsigned>(ctx->sm_count);
-      direct_k<<<g0, slot::kDirectBT, smem_w, ctx->stream>>>(a, n_chunks, p->chunk_counts.get(), miss);
+      direct_k<<<g0, slot::kDirectBT, smem_w, ctx->stream>>>(a, n_chunks, p->chunk_counts.get(), miss, nullptr,
+                                                              nullptr);
     } else if (optimistic) {
       LAQ_CUDA(cudaFuncSetAttribute(direct_small_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_w)));
       LAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, direct_small_k, slot::kWarpThreads, smem_w));
       const unsigned g0 = static_cast<unsigned>(std::min<int64_t>(want, int64_t{ctx->sm_count} * std::max(per_sm, 1)));
-      direct_small_k<<<g0, slot::kWarpThreads, smem_w, ctx->stream>>>(a, n_chunks, p->chunk_counts.get(), miss);
+      if (one_launch) {  // the whole call in one launch: the last CTA decides (and compacts on a miss)
+        direct_small_k<<<g0, slot::kWarpThreads, smem_w, ctx->stream>>>(a, n_chunks, p->chunk_counts.get(), miss,
+                                                                          p->miss.get() + 2, p->chunk_offsets.get());
+        return;
+      }
+      direct_small_k<<<g0, slot::kWarpThreads, smem_w, ctx->stream>>>(a, n_chunks, p->chunk_counts.get(), miss,
+                                                                      nullptr, nullptr);
     } else {
       LAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, count_k, slot::kWarpThreads, smem));
       const unsigned g1 = static_cast<unsigned>(std::min<int64_t>(want, int64_t{ctx->sm_count} * std::max(per_sm, 1)));
@@ -608,7 +633,7 @@ int laq_probe_build(laq_ctx* ctx, int32_t n_links, const int32_t* const* d_pks, 
   return guard(ctx, [&] {
     if (n_links < 1 || n_links > kMaxLinks) fail(LAQ_ERR_UNSUPPORTED, "fused star predict supports 1..8 dimensions");
     auto* p = new laq_probe();
-    LAQ_CUDA(cudaMemset(p->miss.get(), 0, 2 * sizeof(unsigned long long)));
+    LAQ_CUDA(cudaMemset(p->miss.get(), 0, 3 * sizeof(unsigned long long)));
     try {
       p->n_links = n_links;
       for (int j = 0; j < n_links; ++j)

@@ -404,6 +404,7 @@ struct laq_plan {
   int grid = 1;
   size_t smem = 0;
   int64_t bytes_per_row = 0;
+  int64_t measure_min = 0;  // smallest measure value (batched scans: presence by non-zero sum when > 0)
 };
 
 namespace laq {
@@ -1069,6 +1070,7 @@ int laq_query_prepare(laq_ctx* ctx, const laq_star* cs, const laq_query_desc* q,
     plan->mode = G == 1 ? 0 : (G <= kSmemBinsPipe ? 1 : (G <= kSmemBinsLdg ? 1 : 2));
     plan->bytes_per_row = 4 * (plan->nl + plan->nf + a.n_fgroups + (a.measure ? 1 : 0));
     plan->packed_only = packed_only;
+    plan->measure_min = mmin;
     lay_out_scan(ctx, plan.get(), fks, fkcols, probes, mmin, mmax, padded);
     if (packed_only && plan->variant != 2 && plan->variant != 4)
       fail(LAQ_ERR_UNSUPPORTED, "byte-packed fact columns need the stream scan (no fact InSet filter, G <= 4096)");
@@ -1410,13 +1412,13 @@ void batch_alloc_dict(laq_batch* b, const std::vector<int64_t>& cap, const std::
     L.hbits = hb[j];
     off += size_t{1} << hb[j];
     L.idw = idw[j];
-    b->ids.emplace_back(static_cast<size_t>(((L.slots * idw[j]) + 15) & ~int64_t{15}));
+    b->ids.emplace_back(static_cast<size_t>((((L.slots + 1) * idw[j]) + 15) & ~int64_t{15}));
     L.ids = b->ids.back().get();
     b->dec.emplace_back(static_cast<size_t>((cap[j] + 1) & ~int64_t{1}));  // 16-byte multiple
     L.dec = b->dec.back().get();
     L.dec_cap = static_cast<int>(cap[j]);
     if (want_bm[j]) {
-      b->bm.emplace_back(static_cast<size_t>((((L.slots + 31) / 32) + 3) & ~int64_t{3}));
+      b->bm.emplace_back(static_cast<size_t>((((L.slots + 32) / 32) + 3) & ~int64_t{3}));
       L.bm = b->bm.back().get();
     } else {
       b->bm.emplace_back();
@@ -1444,7 +1446,7 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
     b->why = why;
   };
   if (std::getenv("LAQ_NO_BATCH_SCAN")) return reject("LAQ_NO_BATCH_SCAN");
-  if (nq < 1 || nq > kBatchMaxQ) return reject("batch of 1..4 plans");
+  if (nq < 2 || nq > kBatchMaxQ) return reject("the fused pass takes batches of 2..4 plans");
   const laq_plan* p0 = b->plans[0];
   if (p0->fact_rows == 0) return reject("empty fact table");
   int mode = 0;
@@ -1458,6 +1460,13 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
       return reject("different measures");
     if (a.measure && a.mc.w != 4) return reject("packed measure");
     mode = std::max(mode, p->mode);
+  }
+  // Bins with a positive measure: sums only (a group is present iff its sum
+  // is non-zero), half the shared atomics of (count, sum) bins.
+  if (mode == 1 && p0->scan.measure) {
+    bool positive = true;
+    for (const laq_plan* p : b->plans) positive = positive && p->measure_min > 0;
+    if (positive && !std::getenv("LAQ_BATCH_COUNT_BINS")) mode = 2;
   }
   // Union of links (keyed by the fact FK column) and of fact filter columns.
   struct U {
@@ -1529,13 +1538,14 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
   for (int j = 0; j < b->nl; ++j) {
     DictLink& L = D.l[j];
     L.slots = links[j].slots;
+    L.size = links[j].size;
     unsigned long long miss = 0;
     for (int q = 0; q < nq; ++q) {
       L.code[q] = links[j].code[q];
       if (L.code[q]) miss |= static_cast<unsigned long long>(kLaneFail) << (16 * q);
     }
     L.miss = miss;
-    D.start[j + 1] = D.start[j] + ((L.slots + 31) & ~int64_t{31});
+    D.start[j + 1] = D.start[j] + ((L.slots + 1 + 31) & ~int64_t{31});  // covers the miss slot `size`
     cap[j] = std::min<int64_t>(L.slots + 1, 65536);
   }
   batch_alloc_dict(b, cap, std::vector<int>(b->nl, 2), std::vector<char>(b->nl, 0));
@@ -1570,15 +1580,16 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
   LAQ_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
   int64_t room = static_cast<int64_t>(optin) - 2048;
   int64_t bins = 0;
-  if (mode == 1)
-    for (const laq_plan* p : b->plans) bins += (8 * p->G + 15) & ~int64_t{15};
+  const int64_t bin_words = mode == 1 ? 2 : 1;  // u32 words per group
+  if (mode != 0)
+    for (const laq_plan* p : b->plans) bins += (4 * bin_words * p->G + 15) & ~int64_t{15};
   std::vector<int64_t> decb(b->nl), idb(b->nl), bmb(b->nl);
   std::vector<int> idw(b->nl);
   for (int j = 0; j < b->nl; ++j) {
     decb[j] = (8 * int64_t{b->n_dec[j]} + 15) & ~int64_t{15};
     idw[j] = b->n_dec[j] <= 256 ? 1 : 2;
-    idb[j] = (D.l[j].slots * idw[j] + 15) & ~int64_t{15};
-    bmb[j] = (((D.l[j].slots + 31) / 32) * 4 + 15) & ~int64_t{15};
+    idb[j] = ((D.l[j].slots + 1) * idw[j] + 15) & ~int64_t{15};
+    bmb[j] = (((D.l[j].slots + 32) / 32) * 4 + 15) & ~int64_t{15};
     room -= decb[j];
   }
   room -= bins;
@@ -1591,6 +1602,19 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
     if (!std::getenv("LAQ_NOSMEMTAB") && idb[j] <= room) staged[j] = 1, room -= idb[j];
   for (int j : by)
     if (!staged[j] && bmb[j] <= room && frac[j] < 0.75) use_bm[j] = 1, room -= bmb[j];
+  // Decode tables replicated `rep` times (entry-interleaved) with what room is
+  // left: lane l reads copy l % rep, so a warp's 32 random decodes conflict at
+  // most 32/rep-way on a bank instead of colliding on the few entries' banks.
+  int rep = 1;
+  {
+    int64_t dec_total = 0;
+    for (int j = 0; j < b->nl; ++j) dec_total += decb[j];
+    while (rep < 16 && dec_total * (2 * rep - rep) <= room) {
+      room -= dec_total * rep;
+      rep *= 2;
+    }
+    if (const char* e = std::getenv("LAQ_BATCH_DEC_REP")) rep = std::max(1, std::min(rep, std::atoi(e)));
+  }
 
   // Final dictionaries: exact capacities and id widths.
   for (int j = 0; j < b->nl; ++j) cap[j] = b->n_dec[j];
@@ -1621,8 +1645,8 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
     K.bm = L.bm;
     K.fmt = staged[j] ? (idw[j] == 1 ? kIdSmemU8 : kIdSmemU16) : (idw[j] == 1 ? kIdGlobU8 : kIdGlobU16);
     K.dec_byte = static_cast<int>(off);
-    K.dec_bytes = static_cast<int>(decb[j]);
-    off += decb[j];
+    K.n_dec = b->n_dec[j];
+    off += decb[j] * rep;
     B.fkc[t] = links[j].c;
     gathers = gathers || !staged[j];
   }
@@ -1643,7 +1667,6 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
       off += bmb[j];
     }
   }
-  B.smem_stage_bytes = static_cast<int>(off);
   for (int f = 0; f < b->nf; ++f) {
     B.ffc[f] = fcols[f].second;
     for (int q = 0; q < kBatchMaxQ; ++q) B.ff_lo[f][q] = flo[f][q], B.ff_hi[f][q] = fhi[f][q];
@@ -1654,13 +1677,20 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
   for (int q = 0; q < nq; ++q) {
     const laq_plan* p = b->plans[q];
     B.G[q] = p->G;
-    if (mode == 1) {
+    if (mode != 0) {
       B.bins_byte[q] = static_cast<int>(off);
-      off += (8 * p->G + 15) & ~int64_t{15};
+      off += (4 * bin_words * p->G + 15) & ~int64_t{15};
     }
     flush = std::min<int64_t>(flush, std::max<int64_t>(1, p->scan.flush_every));
   }
-  B.reject_mask = reject_mask;
+  B.init_lo = B.init_hi = B.fail_lo = B.fail_hi = 0;
+  for (int q = 0; q < nq; ++q) {
+    const uint32_t f = kLaneFail << (16 * (q & 1));
+    (q < 2 ? B.fail_lo : B.fail_hi) += f;
+    if (reject_mask & (1u << q)) (q < 2 ? B.init_lo : B.init_hi) += f;
+  }
+  B.dec_shift = 3;
+  while ((1 << (B.dec_shift - 3)) < rep) ++B.dec_shift;
   B.flush_every = flush;
   B.prefetch = gathers ? 2 : 0;
   if (const char* pf = std::getenv("LAQ_PREFETCH")) B.prefetch = std::atoi(pf);

@@ -49,8 +49,8 @@ struct BatchLink {
   int id_byte;                // smem byte offset of the staged id table
   int id_bytes;               // staged bytes (multiple of 16)
   const void* ids;            // the id table in global memory
-  int dec_byte;               // smem byte offset of the decode table
-  int dec_bytes;              // multiple of 16
+  int dec_byte;               // smem byte offset of the (replicated) decode table
+  int n_dec;                  // decode entries (tuple ids incl. the miss id)
   const unsigned long long* dec;
   int bm_byte;                // >= 0: smem byte offset of the any-pass bitmap (global id formats)
   int bm_bytes;
@@ -67,18 +67,20 @@ struct BatchScan {
   Col mc;
   int has_measure;
   int64_t G[kBatchMaxQ];
-  int bins_byte[kBatchMaxQ];
+  int bins_byte[kBatchMaxQ];  // MODE 1: u32 [count G | sum G]; MODE 2: u32 [sum G]
   unsigned long long* acc[kBatchMaxQ];
   int64_t flush_every;  // grid steps between spills of the u32 bins
   int prefetch;         // L2 prefetch distance in grid steps (0: off)
-  int smem_stage_bytes; // bytes of [ids | dec | bitmaps] staged at kernel start
-  uint32_t reject_mask; // bit q: query q matches no row (an empty fact interval)
+  uint32_t init_lo, init_hi;  // a row's starting lanes: kLaneFail for queries that match nothing
+  uint32_t fail_lo, fail_hi;  // every lane failed (rows past the end)
+  uint32_t dec_shift;         // log2(8 * decode-table replication)
 };
 
 // ---- device dictionary build (one launch per phase for every link) ----------
 
 struct DictLink {
   int64_t slots;
+  int64_t size;                     // probe slots: ids[size] = the miss id (keys are clamped to it)
   const int32_t* code[kBatchMaxQ];  // per query: the link's code table, nullptr = query does not join it
   unsigned long long* hkeys;        // open-addressing table, kDictEmpty = free
   int32_t* hid;

@@ -1,0 +1,320 @@
+// The batched scan kernel (design in ssb_batch.cuh) and its launch templates;
+// instantiated per batch size in ssb_batch_q{2,3,4}.cu (parallel compilation).
+#pragma once
+
+#include "ssb_batch.cuh"
+
+namespace laq {
+namespace scan {
+
+// ---------------------------------------------------------------------------
+// the batched scan
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return static_cast<uint32_t>(v);
+}
+__device__ __forceinline__ uint2 lds_u64(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+
+// Lane q of a row's accumulator (lo: lanes 0-1, hi: lanes 2-3).
+__device__ __forceinline__ uint32_t lane_of(uint32_t lo, uint32_t hi, int q) {
+  const uint32_t w = q < 2 ? lo : hi;
+  return (q & 1) ? (w >> 16) : (w & 0xFFFFu);
+}
+
+// Predicated (branch-free) shared atomic add and L2 gathers.
+__device__ __forceinline__ void reds_add_if(bool p, uint32_t addr, uint32_t v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q red.shared.add.u32 [%0], %1;\n}" ::"r"(addr), "r"(v),
+               "r"(static_cast<uint32_t>(p))
+               : "memory");
+}
+__device__ __forceinline__ uint32_t ldg_u8_if(bool p, const void* ptr, uint32_t dflt) {
+  uint32_t v;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\tmov.b32 %0, %3;\n\t@q ld.global.nc.u8 %0, [%1];\n}"
+               : "=r"(v)
+               : "l"(ptr), "r"(static_cast<uint32_t>(p)), "r"(dflt));
+  return v;
+}
+__device__ __forceinline__ uint32_t ldg_u16_if(bool p, const void* ptr, uint32_t dflt) {
+  uint32_t v;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\tmov.b32 %0, %3;\n\t@q ld.global.nc.u16 %0, [%1];\n}"
+               : "=r"(v)
+               : "l"(ptr), "r"(static_cast<uint32_t>(p)), "r"(dflt));
+  return v;
+}
+
+// Row loads without the bounds test (steps whose rows are all in range).
+__device__ __forceinline__ int4 ld4_nb(const Col& c, int64_t row0) {
+  return __ldcs(reinterpret_cast<const int4*>(static_cast<const int32_t*>(c.p) + row0));
+}
+
+// Four rows per thread.  Each row's accumulator starts at B.init (kLaneFail in
+// the lanes of queries that match nothing) or all-fail past the end; a fact
+// filter adds kLaneFail to the lanes of the queries it rejects.  Every lookup
+// is branch-free: a key outside the probe range is clamped to slot `size`,
+// whose id is the miss tuple; L2 gathers are predicated instructions.  Decode
+// tables are replicated B.dec_rep times with the copies interleaved per
+// entry, lane l reading copy l % dec_rep (no bank conflicts between copies).
+// MODE 0: per-thread register sums (every query has one group); MODE 1: u32
+// (count, sum) bins; MODE 2: u32 sum bins only -- the measure is positive, so
+// a group is present iff its sum is non-zero (half the shared atomics).
+template <int NQ, int NL, int NF, int MODE, bool TAIL>
+__device__ __forceinline__ void batch_rows(const BatchScan& B, int64_t row0, const int4 (&kv)[NL],
+                                           const int4 (&fv)[NF > 0 ? NF : 1], const int4& mv, uint32_t s_base,
+                                           uint32_t dec_base, uint32_t (&r_cnt)[NQ],
+                                           unsigned long long (&r_sum)[NQ]) {
+  uint32_t lo[4], hi[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const bool past = TAIL && row0 + r >= B.n;
+    lo[r] = past ? B.fail_lo : B.init_lo;
+    hi[r] = past ? B.fail_hi : B.init_hi;
+  }
+#pragma unroll
+  for (int f = 0; f < NF; ++f)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const uint32_t flo = static_cast<uint32_t>(B.ff_lo[f][q]);
+      const uint32_t span = static_cast<uint32_t>(B.ff_hi[f][q]) - flo;
+      const uint32_t add = kLaneFail << (16 * (q & 1));
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint32_t a = static_cast<uint32_t>(comp(fv[f], r)) - flo > span ? add : 0u;
+        if (q < 2) lo[r] += a;
+        else hi[r] += a;
+      }
+    }
+  const uint32_t sh = B.dec_shift;  // log2(8 * dec_rep)
+#pragma unroll
+  for (int j = 0; j < NL; ++j) {
+    const BatchLink& L = B.link[j];
+    uint32_t sl[4], id[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) sl[r] = min(static_cast<uint32_t>(comp(kv[j], r)) - L.base, L.size);
+    if (L.fmt == kIdSmemU8) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) id[r] = lds_u8(s_base + L.id_byte + sl[r]);
+    } else if (L.fmt == kIdSmemU16) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) id[r] = lds_u16(s_base + L.id_byte + 2 * sl[r]);
+    } else {
+      // gathered through L2 only for rows some query still keeps (and, with a
+      // staged any-pass bitmap, whose slot passes for some query)
+      bool go[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        bool alive = false;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) alive = alive || lane_of(lo[r], hi[r], q) < kLaneFail;
+        go[r] = alive;
+      }
+      if (L.bm_byte >= 0) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          go[r] = go[r] && ((lds_u32(s_base + L.bm_byte + 4 * (sl[r] >> 5)) >> (sl[r] & 31)) & 1u);
+      }
+      if (L.fmt == kIdGlobU8) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) id[r] = ldg_u8_if(go[r], static_cast<const uint8_t*>(L.ids) + sl[r], L.miss);
+      } else {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) id[r] = ldg_u16_if(go[r], static_cast<const uint16_t*>(L.ids) + sl[r], L.miss);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint2 d = lds_u64(dec_base + L.dec_byte + (id[r] << sh));
+      lo[r] += d.x;
+      hi[r] += d.y;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const uint32_t m = static_cast<uint32_t>(comp(mv, r));
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const uint32_t g = lane_of(lo[r], hi[r], q);
+      const bool ok = g < kLaneFail;
+      if constexpr (MODE == 0) {
+        r_cnt[q] += ok ? 1u : 0u;
+        r_sum[q] += ok ? static_cast<unsigned long long>(static_cast<long long>(static_cast<int32_t>(m))) : 0ull;
+      } else if constexpr (MODE == 1) {
+        const uint32_t ad = s_base + B.bins_byte[q] + 4u * g;
+        reds_add_if(ok, ad, 1u);
+        reds_add_if(ok, ad + 4u * static_cast<uint32_t>(B.G[q]), m);
+      } else {
+        reds_add_if(ok, s_base + B.bins_byte[q] + 4u * g, m);
+      }
+    }
+  }
+}
+
+// MODE 2 spill: sum bins only; the count slot gets 1 per non-empty bin (a
+// presence tally: non-zero iff the group has rows, all laq_plan_emit reads).
+__device__ __forceinline__ void spill_sums32(uint32_t* b32, int64_t G, unsigned long long* acc, int t, int nt) {
+  for (int64_t g = t; g < G; g += nt) {
+    const uint32_t v = b32[g];
+    if (v) {
+      atomicAdd(acc + 2 * g, 1ull);
+      atomicAdd(acc + 2 * g + 1, static_cast<unsigned long long>(v));
+      b32[g] = 0;
+    }
+  }
+}
+
+template <int NQ, int MODE>
+__device__ __forceinline__ void spill_all(const BatchScan& B, unsigned char* smem, int tid) {
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    uint32_t* b = reinterpret_cast<uint32_t*>(smem + B.bins_byte[q]);
+    if constexpr (MODE == 1) spill_bins32(b, B.G[q], B.acc[q], tid, kDirectThreads);
+    else spill_sums32(b, B.G[q], B.acc[q], tid, kDirectThreads);
+  }
+}
+
+template <int NQ, int NL, int NF, int MODE>
+__global__ void __launch_bounds__(kDirectThreads, 1) scan_batch_kernel(const __grid_constant__ BatchScan B) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int tid = threadIdx.x;
+  auto stage = [&](const void* src, int byte, int bytes) {
+    const uint4* s = static_cast<const uint4*>(src);
+    uint4* d = reinterpret_cast<uint4*>(smem + byte);
+    for (int w = tid; w < bytes / 16; w += kDirectThreads) d[w] = __ldg(s + w);
+  };
+  const int rep = 1 << (B.dec_shift - 3);
+#pragma unroll
+  for (int j = 0; j < NL; ++j) {
+    const BatchLink& L = B.link[j];
+    if (L.fmt == kIdSmemU8 || L.fmt == kIdSmemU16) stage(L.ids, L.id_byte, L.id_bytes);
+    unsigned long long* d = reinterpret_cast<unsigned long long*>(smem + L.dec_byte);
+    for (int w = tid; w < L.n_dec * rep; w += kDirectThreads) d[w] = __ldg(L.dec + w / rep);  // entry-interleaved copies
+    if (L.bm_byte >= 0) stage(L.bm, L.bm_byte, L.bm_bytes);
+  }
+  if constexpr (MODE != 0) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      uint32_t* b = reinterpret_cast<uint32_t*>(smem + B.bins_byte[q]);
+      for (int64_t g = tid; g < (MODE == 1 ? 2 : 1) * B.G[q]; g += kDirectThreads) b[g] = 0;
+    }
+  }
+  __syncthreads();
+
+  const uint32_t s_base = smem_u32(smem);
+  const uint32_t dec_base = s_base + 8u * static_cast<uint32_t>(tid & (rep - 1));
+  uint32_t r_cnt[NQ];
+  unsigned long long r_sum[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) r_cnt[q] = 0, r_sum[q] = 0;
+
+  const int64_t step = static_cast<int64_t>(gridDim.x) * kDirectThreads * 4;
+  const int64_t iters = (B.n + step - 1) / step;
+  const int64_t full = B.n / step;
+  int64_t row0 = (static_cast<int64_t>(blockIdx.x) * kDirectThreads + tid) * 4;
+  const bool pf_lane = B.prefetch && (tid & 7) == 0;
+  const int64_t pf_rows = static_cast<int64_t>(B.prefetch) * step;
+
+  int4 kvA[NL], fvA[NF > 0 ? NF : 1], mvA = make_int4(0, 0, 0, 0);
+  int4 kvB[NL], fvB[NF > 0 ? NF : 1], mvB = make_int4(0, 0, 0, 0);
+  auto load = [&](int4 (&kv)[NL], int4 (&fv)[NF > 0 ? NF : 1], int4& mv, int64_t r, bool inb) {
+    if (inb) {  // every row of the step exists: no per-load bounds test
+#pragma unroll
+      for (int j = 0; j < NL; ++j) kv[j] = ld4_nb(B.fkc[j], r);
+#pragma unroll
+      for (int f = 0; f < NF; ++f) fv[f] = ld4_nb(B.ffc[f], r);
+      if (B.has_measure) mv = ld4_nb(B.mc, r);
+    } else {
+#pragma unroll
+      for (int j = 0; j < NL; ++j) kv[j] = dld<0>(B.fkc[j], r, B.n);
+#pragma unroll
+      for (int f = 0; f < NF; ++f) fv[f] = dld<0>(B.ffc[f], r, B.n);
+      if (B.has_measure) mv = dld<0>(B.mc, r, B.n);
+    }
+  };
+  load(kvA, fvA, mvA, row0, full > 0);
+  int64_t until_flush = B.flush_every;
+  auto one = [&](int64_t it, const int4 (&kv)[NL], const int4 (&fv)[NF > 0 ? NF : 1], const int4& mv,
+                 int4 (&nkv)[NL], int4 (&nfv)[NF > 0 ? NF : 1], int4& nmv) {
+    load(nkv, nfv, nmv, row0 + step, it + 1 < full);
+    if (pf_lane && row0 + pf_rows < B.n) {
+#pragma unroll
+      for (int j = 0; j < NL; ++j) prefetch_l2<0>(B.fkc[j], row0 + pf_rows);
+#pragma unroll
+      for (int f = 0; f < NF; ++f) prefetch_l2<0>(B.ffc[f], row0 + pf_rows);
+      if (B.has_measure) prefetch_l2<0>(B.mc, row0 + pf_rows);
+    }
+    if (it < full)
+      batch_rows<NQ, NL, NF, MODE, false>(B, row0, kv, fv, mv, s_base, dec_base, r_cnt, r_sum);
+    else
+      batch_rows<NQ, NL, NF, MODE, true>(B, row0, kv, fv, mv, s_base, dec_base, r_cnt, r_sum);
+    if constexpr (MODE != 0) {
+      if (--until_flush == 0) {
+        until_flush = B.flush_every;
+        if (it + 1 < iters) {
+          __syncthreads();
+          spill_all<NQ, MODE>(B, smem, tid);
+          __syncthreads();
+        }
+      }
+    }
+    row0 += step;
+  };
+  for (int64_t it = 0; it < iters; it += 2) {
+    one(it, kvA, fvA, mvA, kvB, fvB, mvB);
+    if (it + 1 < iters) one(it + 1, kvB, fvB, mvB, kvA, fvA, mvA);
+  }
+  if constexpr (MODE == 0) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) flush_single(r_cnt[q], r_sum[q], B.acc[q]);
+  } else {
+    __syncthreads();
+    spill_all<NQ, MODE>(B, smem, tid);
+  }
+}
+
+template <int NQ, int NL, int NF, int MODE>
+void launch_batch_t(laq_ctx* ctx, const BatchScan& B, size_t smem, int grid) {
+  auto kern = scan_batch_kernel<NQ, NL, NF, MODE>;
+  LAQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  const int64_t blocks_needed = (B.n + kDirectThreads * 4 - 1) / (kDirectThreads * 4);
+  const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(grid, blocks_needed)));
+  kern<<<g, kDirectThreads, smem, ctx->stream>>>(B);
+}
+
+template <int NQ, int NL, int NF>
+void launch_batch_m(laq_ctx* ctx, const BatchScan& B, int mode, size_t smem, int grid) {
+  if (mode == 0) launch_batch_t<NQ, NL, NF, 0>(ctx, B, smem, grid);
+  else if (mode == 1) launch_batch_t<NQ, NL, NF, 1>(ctx, B, smem, grid);
+  else launch_batch_t<NQ, NL, NF, 2>(ctx, B, smem, grid);
+}
+
+template <int NQ, int NL>
+void launch_batch_f(laq_ctx* ctx, const BatchScan& B, int nf, int mode, size_t smem, int grid) {
+  switch (nf) {
+    case 0: launch_batch_m<NQ, NL, 0>(ctx, B, mode, smem, grid); break;
+    case 1: launch_batch_m<NQ, NL, 1>(ctx, B, mode, smem, grid); break;
+    case 2: launch_batch_m<NQ, NL, 2>(ctx, B, mode, smem, grid); break;
+    default: fail(LAQ_ERR_UNSUPPORTED, "batched scan: at most 2 fact filter columns");
+  }
+}
+
+template <int NQ>
+void launch_batch_q(laq_ctx* ctx, const BatchScan& B, int nl, int nf, int mode, size_t smem, int grid) {
+  switch (nl) {
+    case 1: launch_batch_f<NQ, 1>(ctx, B, nf, mode, smem, grid); break;
+    case 2: launch_batch_f<NQ, 2>(ctx, B, nf, mode, smem, grid); break;
+    case 3: launch_batch_f<NQ, 3>(ctx, B, nf, mode, smem, grid); break;
+    case 4: launch_batch_f<NQ, 4>(ctx, B, nf, mode, smem, grid); break;
+    case 5: launch_batch_f<NQ, 5>(ctx, B, nf, mode, smem, grid); break;
+    case 6: launch_batch_f<NQ, 6>(ctx, B, nf, mode, smem, grid); break;
+    default: fail(LAQ_ERR_UNSUPPORTED, "batched scan: 1..6 links");
+  }
+}
+
+}  // namespace scan
+}  // namespace laq

@@ -81,6 +81,14 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 
+// 1-D bulk copy global -> this CTA's shared memory on the TMA engine (SASS
+// UBLKCP), completion counted in bytes on `bar`.  16-byte aligned, size % 16 == 0.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 // ---- TMA ------------------------------------------------------------------------
 // Row gather (tile::gather4): rows r0..r3 of a 2-D tensor map (box {inner, 1}),
 // columns [c0, c0 + inner), land as 4 consecutive smem rows with the map's swizzle;

@@ -10,7 +10,11 @@ decision picked the measured winner.  Cells whose P (r l 4 B), B (r k 8 B) or Y
 (F l 4 B) exceed 64 GB are skipped as CapacityError, as the survey specifies.
 A 512-row sample of every cell is checked against an fp64 product (cond-aware 1e-5).
 
-usage: python scripts/complexity_sweep.py [out.json] [--quick]
+usage: python scripts/complexity_sweep.py [out.json] [--quick | --holdout]
+
+--holdout: a grid disjoint from the one the B200 planner's constants were
+fitted on (r in 3e3..3e6, k in 16/64/256, l in 2..2048): an out-of-sample check
+of fusion.plan_linear_device (constants unchanged).
 """
 import json
 import os
@@ -30,6 +34,8 @@ L = [1, 4, 16, 64, 256, 1024, 4096]
 CAP = 64 << 30
 if "--quick" in sys.argv:
     R, K, L = [1_000, 100_000], [8, 128], [1, 64, 1024]
+if "--holdout" in sys.argv:
+    R, K, L = [3_000, 30_000, 300_000, 3_000_000], [16, 64, 256], [2, 8, 32, 128, 512, 2048]
 out_path = next((a for a in sys.argv[1:] if a.endswith(".json")), "gpurun_out/complexity_sweep.json")
 
 
@@ -95,6 +101,10 @@ for r in R:
             cell["measured_winner"] = "fused" if cell["ms_fused"] < cell["ms_nonfused"] else "nonfused"
             cell["planner_right"] = cell["planner"] == cell["measured_winner"]
             cell["device_planner"] = fusion.plan_linear_device(F, k, l, [r])
+            pick = cell["ms_fused"] if cell["device_planner"] == "fused" else cell["ms_nonfused"]
+            cell["device_planner_slowdown"] = pick / min(cell["ms_fused"], cell["ms_nonfused"])
+            pick = cell["ms_fused"] if cell["planner"] == "fused" else cell["ms_nonfused"]
+            cell["planner_slowdown"] = pick / min(cell["ms_fused"], cell["ms_nonfused"])
             flop = 2.0 * F * k * l
             cell["nonfused_alg_tflops"] = flop / (cell["ms_nonfused"] / 1e3) / 1e12
             cell["prefuse_alg_tflops"] = 2.0 * r * k * l / (cell["ms_prefuse"] / 1e3) / 1e12
@@ -110,6 +120,9 @@ summary = {
     "cells": len(rows), "measured": len(done), "skipped": len(rows) - len(done),
     "planner_agrees_with_measurement": sum(c["planner_right"] for c in done),
     "device_planner_agrees": sum(c["device_planner"] == c["measured_winner"] for c in done),
+    "device_planner_max_slowdown": max([c["device_planner_slowdown"] for c in done], default=1.0),
+    "planner_max_slowdown": max([c["planner_slowdown"] for c in done], default=1.0),
+    "grid": {"r": R, "k": K, "l": L, "F": F},
     "max_cond_err": max([max(c["cond_err_fused"], c["cond_err_nonfused"]) for c in done], default=0.0),
     "best_nonfused_alg_tflops": max([c["nonfused_alg_tflops"] for c in done], default=0.0),
     "best_prefuse_alg_tflops": max([c["prefuse_alg_tflops"] for c in done], default=0.0),

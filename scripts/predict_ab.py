@@ -1,0 +1,71 @@
+"""A/B of the cfg1 fused join+predict call forms (one launch vs three) at 1M
+and 1e8 rows, CUDA-graph replay timing, plus a miss-path exactness check of
+the one-launch form (dangling keys -> last-CTA compaction) vs the oracle.
+
+  python scripts/predict_ab.py   (on a GPU box)
+"""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle import laq_oracle as O  # noqa: E402
+from paper_2306_08367_b200 import fusion, gen  # noqa: E402
+
+
+def timed(pred, fkd, y, reps=20, iters=5):
+    s = torch.cuda.current_stream()
+    for _ in range(3):
+        pred([fkd], out=y, sync=False)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            pred([fkd], out=y, sync=False)
+    pred.ctx.bind_stream(s)
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / (iters * reps)
+
+
+def main():
+    fk, pk, feats, W = gen.cfg1_inputs(1_000_000, 10_000, 16, 1)
+    f = fusion.prefuse_linear([feats], [np.arange(16)], W)
+    out = {}
+    for mode in ("1", "0"):
+        os.environ["LAQ_PREDICT_ONE_LAUNCH"] = mode
+        pred = fusion.FusedStarPredictor([pk], f.partials)
+        for n in (1_000_000, 4_000_000, 100_000_000):
+            fkd = torch.from_numpy(fk.astype(np.int32)).cuda() if n == 1_000_000 else \
+                torch.randint(0, 10_000, (n,), dtype=torch.int32, device="cuda")
+            y = torch.empty((n, 1), dtype=torch.float64, device="cuda")
+            ms = timed(pred, fkd, y)
+            out[f"one_launch={mode} n={n}"] = {"us": round(ms * 1e3, 2), "GB/s": round(12 * n / ms / 1e6, 1)}
+        # exactness incl. the miss path (dangling keys) in this mode
+        rng = np.random.default_rng(5)
+        for n in (1, 1000, 777_777, 1_000_000):
+            k = rng.integers(0, 10_000, n).astype(np.int32)
+            if n > 1:
+                k[rng.random(n) < 0.01] = 10_000 + 5
+            y, nnz = pred([torch.from_numpy(k).cuda()])
+            ws, wr = O.multiway_star_join([k.astype(np.int64)], [pk])
+            wy = O.apply_fused_linear(wr, O.prefuse_linear([feats], [np.arange(16)], W))
+            ok = nnz == len(ws) and np.array_equal(y.cpu().numpy(), wy)
+            # graph replay after a miss call must still be exact
+            out[f"one_launch={mode} exact n={n}"] = bool(ok)
+        pred.close()
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
