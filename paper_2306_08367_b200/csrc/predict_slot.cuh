@@ -199,10 +199,12 @@ __global__ void __launch_bounds__(kWarpThreads) count_chunks_kernel(const Args a
 // misses: it compacts the rows in place itself (tail_compact) -- and resets
 // the counters, so a call is a single launch and graph replays stay exact.
 template <int NL>
-__device__ void tail_compact(const Args& a, const uint32_t* s_bits, int64_t n_chunks, const int* counts,
-                             int64_t* offsets);
+__device__ void tail_compact(const Args& a, const uint32_t* s_bits, int64_t n_chunks, int64_t chunk_rows,
+                             const int* counts, int64_t* offsets);
 
-template <int NL, int BT = kWarpThreads>
+// SEGS: 128-row segments per warp chunk (the one-launch form uses short
+// chunks so a small input still spreads over every warp of the grid).
+template <int NL, int BT = kWarpThreads, int SEGS = kSegs>
 __global__ void __launch_bounds__(BT, 1) direct_chunks_kernel(const Args a, int64_t n_chunks, int* counts,
                                                                      unsigned long long* miss,
                                                                      unsigned long long* last = nullptr,
@@ -237,6 +239,7 @@ __global__ void __launch_bounds__(BT, 1) direct_chunks_kernel(const Args a, int6
         for (int64_t s = threadIdx.x; s < a.size[j]; s += BT) s_p[a.p_off[j] + s] = __ldg(a.pslot[j] + s);
     __syncthreads();
   }
+  constexpr int64_t kRows = int64_t{SEGS} * kSegRows;
   const int lane = threadIdx.x & 31;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (BT / 32);
   auto pval = [&](int j, uint32_t s) -> double {
@@ -247,12 +250,12 @@ __global__ void __launch_bounds__(BT, 1) direct_chunks_kernel(const Args a, int6
     // Every key load of the chunk first (8 segments x 16 B per link and lane in
     // flight: the partials' shared-memory footprint caps residency at 2 CTAs/SM,
     // so memory-level parallelism has to come from within the warp).
-    int4 kv[kSegs][NL];
+    int4 kv[SEGS][NL];
 #pragma unroll
-    for (int g = 0; g < kSegs; ++g) load_kv<NL>(a, c * kChunkRows + g * kSegRows + 4 * lane, kv[g]);
+    for (int g = 0; g < SEGS; ++g) load_kv<NL>(a, c * kRows + g * kSegRows + 4 * lane, kv[g]);
 #pragma unroll
-    for (int g = 0; g < kSegs; ++g) {
-      const int64_t r0 = c * kChunkRows + g * kSegRows + 4 * lane;
+    for (int g = 0; g < SEGS; ++g) {
+      const int64_t r0 = c * kRows + g * kSegRows + 4 * lane;
       uint32_t slot[NL][4];
       bool ok[4];
       cnt += probe4_rows<NL>(a, s_bits, r0, kv[g], slot, ok);
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(BT, 1) direct_chunks_kernel(const Args a, int6
     for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     if (lane == 0) {
       counts[c] = cnt;
-      const int64_t rows = min(static_cast<int64_t>(kChunkRows), a.n - c * kChunkRows);
+      const int64_t rows = min(static_cast<int64_t>(kRows), a.n - c * kRows);
       if (cnt != rows) atomicAdd(miss, 1ull);
     }
   }
@@ -295,7 +298,7 @@ __global__ void __launch_bounds__(BT, 1) direct_chunks_kernel(const Args a, int6
   if (m == 0) {
     if (threadIdx.x == 0) *a.nnz = a.n;
   } else {
-    tail_compact<NL>(a, s_bits, n_chunks, counts, offsets);
+    tail_compact<NL>(a, s_bits, n_chunks, kRows, counts, offsets);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -310,8 +313,8 @@ __global__ void __launch_bounds__(BT, 1) direct_chunks_kernel(const Args a, int6
 // destination never reaches past its own start, so reading the whole chunk
 // before writing it keeps the in-place move exact).
 template <int NL>
-__device__ void tail_compact(const Args& a, const uint32_t* s_bits, int64_t n_chunks, const int* counts,
-                             int64_t* offsets) {
+__device__ void tail_compact(const Args& a, const uint32_t* s_bits, int64_t n_chunks, int64_t chunk_rows,
+                             const int* counts, int64_t* offsets) {
   __shared__ int64_t s_warp[33];
   __shared__ int64_t s_base, s_total;
   const int t = threadIdx.x, nt = blockDim.x, lane = t & 31, warp = t >> 5, nw = nt / 32;
@@ -327,8 +330,8 @@ __device__ void tail_compact(const Args& a, const uint32_t* s_bits, int64_t n_ch
   for (int64_t c = 0; c < n_chunks; ++c) {
     if (t == 0) s_base = offsets[c];
     __syncthreads();
-    const int64_t end = min(a.n, (c + 1) * kChunkRows);
-    for (int64_t r0 = c * kChunkRows; r0 < end; r0 += nt) {
+    const int64_t end = min(a.n, (c + 1) * chunk_rows);
+    for (int64_t r0 = c * chunk_rows; r0 < end; r0 += nt) {
       const int64_t r = r0 + t;
       bool ok = r < end;
       if (ok)

@@ -539,9 +539,10 @@ void run_slot_predict(laq_ctx* ctx, laq_probe* p, const int32_t* const* d_fks, i
   // the last CTA.  LAQ_PREDICT_ONE_LAUNCH=0 keeps the three-launch form.
   const char* ol = std::getenv("LAQ_PREDICT_ONE_LAUNCH");
   const bool one_launch = optimistic && n_chunks <= 4096 && !(ol && std::string(ol) == "0");
+  constexpr int64_t kOneChunkRows = 256;
   unsigned long long* miss = p->miss.get();
   unsigned long long* decision = p->miss.get() + 1;
-  auto launch = [&](auto count_k, auto direct_k, auto direct_small_k, auto write_k) {
+  auto launch = [&](auto count_k, auto direct_k, auto direct_small_k, auto direct_one_k, auto write_k) {
     LAQ_CUDA(cudaFuncSetAttribute(write_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_w)));
     const int64_t want = (n_chunks + slot::kWarpThreads / 32 - 1) / (slot::kWarpThreads / 32);
     int per_sm = 0;
@@ -559,8 +560,18 @@ void run_slot_predict(laq_ctx* ctx, laq_probe* p, const int32_t* const* d_fks, i
       LAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, direct_small_k, slot::kWarpThreads, smem_w));
       const unsigned g0 = static_cast<unsigned>(std::min<int64_t>(want, int64_t{ctx->sm_count} * std::max(per_sm, 1)));
       if (one_launch) {  // the whole call in one launch: the last CTA decides (and compacts on a miss)
-        direct_small_k<<<g0, slot::kWarpThreads, smem_w, ctx->stream>>>(a, n_chunks, p->chunk_counts.get(), miss,
-                                                                          p->miss.get() + 2, p->chunk_offsets.get());
+        // 1024-thread CTAs (one staged copy of the tables per SM) over 256-row
+        // chunks (1M rows = 3.9K chunks: every warp of the grid gets one).
+        const int64_t chunks1 = (n + kOneChunkRows - 1) / kOneChunkRows;
+        if (p->chunk_cap < chunks1) {
+          p->chunk_counts = DevMem<int>(chunks1);
+          p->chunk_offsets = DevMem<int64_t>(chunks1);
+          p->chunk_cap = chunks1;
+        }
+        LAQ_CUDA(cudaFuncSetAttribute(direct_one_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_w)));
+        const unsigned g1 = static_cast<unsigned>(std::min<int64_t>((chunks1 + 31) / 32, ctx->sm_count));
+        direct_one_k<<<g1, slot::kDirectBT, smem_w, ctx->stream>>>(a, chunks1, p->chunk_counts.get(), miss,
+                                                                   p->miss.get() + 2, p->chunk_offsets.get());
         return;
       }
       direct_small_k<<<g0, slot::kWarpThreads, smem_w, ctx->stream>>>(a, n_chunks, p->chunk_counts.get(), miss,
@@ -581,7 +592,9 @@ void run_slot_predict(laq_ctx* ctx, laq_probe* p, const int32_t* const* d_fks, i
   switch (p->n_links) {
 #define LAQ_SLOT_CASE(N) \
     case N: launch(slot::count_chunks_kernel<N>, slot::direct_chunks_kernel<N, slot::kDirectBT>, \
-                   slot::direct_chunks_kernel<N, slot::kWarpThreads>, slot::write_chunks_kernel<N>); break;
+                   slot::direct_chunks_kernel<N, slot::kWarpThreads>, \
+                   slot::direct_chunks_kernel<N, slot::kDirectBT, kOneChunkRows / slot::kSegRows>, \
+                   slot::write_chunks_kernel<N>); break;
     LAQ_SLOT_CASE(1) LAQ_SLOT_CASE(2) LAQ_SLOT_CASE(3) LAQ_SLOT_CASE(4)
     LAQ_SLOT_CASE(5) LAQ_SLOT_CASE(6) LAQ_SLOT_CASE(7) LAQ_SLOT_CASE(8)
 #undef LAQ_SLOT_CASE

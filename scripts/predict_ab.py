@@ -42,6 +42,26 @@ def main():
     fk, pk, feats, W = gen.cfg1_inputs(1_000_000, 10_000, 16, 1)
     f = fusion.prefuse_linear([feats], [np.arange(16)], W)
     out = {}
+    # calibration: the same HBM traffic as cfg1 (4 MB of int32 keys read, 8 MB
+    # of fp64 written) as one torch elementwise copy, and an empty launch
+    fkd = torch.from_numpy(fk.astype(np.int32)).cuda()
+    y = torch.empty(1_000_000, dtype=torch.float64, device="cuda")
+    for name, fn in (("torch copy int32->f64 (12 MB)", lambda: y.copy_(fkd)), ("empty launch", lambda: y[:1].zero_())):
+        for _ in range(3):
+            fn()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(20):
+                fn()
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        out["calibration: " + name] = {"us": round(e0.elapsed_time(e1) / 100 * 1e3, 2)}
     for mode in ("1", "0"):
         os.environ["LAQ_PREDICT_ONE_LAUNCH"] = mode
         pred = fusion.FusedStarPredictor([pk], f.partials)
