@@ -688,6 +688,33 @@ def fused_predict_bench(ctx):
     e2e_ms = (time.perf_counter() - t0) * 1e3 / 10
     out["e2e"] = {"value": 1e6 / (e2e_ms / 1e3), "unit": UNIT, "ms": e2e_ms, "h2d_bytes_per_step": 4_000_000,
                   "d2h_bytes_per_step": 8_000_000}
+    # e2e through the reference's UNCHANGED C++ API with host std::vectors
+    # (integration/dropin_bench.cpp over the drop-in: multiway_star_join ->
+    # csr_from_coo -> prefuse_linear -> apply_fused_linear, each call H2D + D2H)
+    exe = os.path.join(ROOT, "integration", "_build", "dropin_bench")
+    if os.path.exists(exe):
+        import subprocess
+        import tempfile
+        with tempfile.TemporaryDirectory() as d:
+            np.ascontiguousarray(fk, np.int64).tofile(os.path.join(d, "fk.bin"))
+            np.ascontiguousarray(pk, np.int64).tofile(os.path.join(d, "pk.bin"))
+            np.ascontiguousarray(feats, np.float64).tofile(os.path.join(d, "feats.bin"))
+            np.ascontiguousarray(W, np.float64).tofile(os.path.join(d, "W.bin"))
+            with open(os.path.join(d, "meta.txt"), "w") as fh:
+                fh.write(f"{len(fk)} {len(pk)} {feats.shape[1]} {W.shape[1]}\n")
+            r = subprocess.run([exe, d, "10"], capture_output=True, text=True, timeout=600)
+            if r.returncode == 0:
+                res = json.loads(r.stdout.strip().splitlines()[-1])
+                yb = np.fromfile(os.path.join(d, "y.bin"), np.float64).reshape(-1, W.shape[1])
+                res["bit_exact_vs_device_path"] = bool(np.array_equal(yb, y1))
+                if not res["bit_exact_vs_device_path"]:
+                    raise SystemExit("PARITY FAILURE: drop-in C++ API predictions differ from the device path")
+                res["path"] = ("integration/dropin_bench.cpp: the reference's C++ operator API (drop-in, liblaq_b200 "
+                               "underneath) with host std::vector inputs/outputs; rows_per_s over join + csr + apply "
+                               "(prefuse_linear is the one-time model preparation)")
+                out["e2e_reference_api"] = res
+            else:
+                out["e2e_reference_api"] = {"error": (r.stderr or r.stdout)[-300:]}
     try:
         from oracle import ref
         if ref.available():

@@ -297,7 +297,12 @@ __global__ void __launch_bounds__(kPipeThreads, 1) scan_pipe_kernel(const ScanAr
       int st = 0;
       uint32_t phase = 0;
       for (int64_t i = 0; i < my_tiles; ++i) {
-        if (i >= S) mbar_wait(empty + st, phase ^ 1);  // consumers released this stage
+        if (i >= S) {
+          mbar_wait(empty + st, phase ^ 1);  // consumers released this stage
+          // order the consumers' generic-proxy reads of the stage before the
+          // async-proxy (TMA) writes that refill it
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
         const int64_t row0 = (blockIdx.x + i * gridDim.x) * kTile;
         const int64_t rows = min(static_cast<int64_t>(kTile), a.n - row0);
         const uint32_t bytes = static_cast<uint32_t>((rows * 4 + 15) & ~15ll);

@@ -61,6 +61,17 @@ def _worker(rank, world, port, result_file):
             errors.append(f"plan {grp}.{qi}")
         if ds.measure_selectivity(q) != O.measure_selectivity(full.tables, q):
             errors.append(f"selectivity {grp}.{qi}")
+    # batched scans (the bench's path): each rank scans its shard for a whole
+    # query group in one pass; the per-query accumulators are all-reduced
+    for grp, dials in ((3, (105, 79, 43)), (4, (249, 199, 284))):
+        qs = [Q.spec_with_dial(d, grp, x) for d, x in zip(Q.group_defs(grp), dials)]
+        b = star.Batch([ds.prepare(q) for q in qs])
+        if not b.fused:
+            errors.append(f"batch {grp} not fused: {b.why}")
+        b.build()
+        for q, p, acc in zip(qs, b.plans, b.scan()):
+            if not np.array_equal(p.emit(ctx.allreduce_acc(acc).cpu().numpy()), F.run_query(full.tables, q)):
+                errors.append(f"batch {grp} {q.id}")
     # fused join + predict: no collective; the rank-ordered concatenation is the answer
     fk, pk, feats, W = gen.cfg1_inputs(200_003, 1_000, 16, 1)
     fk[::997] = 5_000  # dangling keys: survivors differ per shard
