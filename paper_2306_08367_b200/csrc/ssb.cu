@@ -1697,6 +1697,9 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
     (q < 2 ? B.fail_lo : B.fail_hi) += f;
     if (reject_mask & (1u << q)) (q < 2 ? B.init_lo : B.init_hi) += f;
   }
+  // Software pipelining of the last link's L2 gather (scan_batch_pipe_kernel)
+  // when that link is gathered and the bins live in shared memory.
+  B.pipe = !staged[order[b->nl - 1]] && mode != 0 && !std::getenv("LAQ_BATCH_NO_PIPE") ? 1 : 0;
   B.dec_shift = 3;
   while ((1 << (B.dec_shift - 3)) < rep) ++B.dec_shift;
   B.flush_every = flush;

@@ -74,6 +74,7 @@ struct BatchScan {
   uint32_t init_lo, init_hi;  // a row's starting lanes: kLaneFail for queries that match nothing
   uint32_t fail_lo, fail_hi;  // every lane failed (rows past the end)
   uint32_t dec_shift;         // log2(8 * decode-table replication)
+  int pipe;                   // the last link is L2-gathered: software-pipelined 2-row kernel
 };
 
 // ---- device dictionary build (one launch per phase for every link) ----------

@@ -277,8 +277,209 @@ __global__ void __launch_bounds__(kDirectThreads, 1) scan_batch_kernel(const __g
   }
 }
 
+// ---------------------------------------------------------------------------
+// Software-pipelined form for batches whose LAST probe link is gathered
+// through L2 (SF=100 Q4.x: the 1.4M-slot part ids; SF=10 Q2.x).  Two rows per
+// thread; iteration i runs stage A of its own rows (fact filters, the staged
+// links, then ISSUES the predicated L2 gather of the last link) and stage B of
+// iteration i-1's rows (that gather's decode + the bins), so each gather has a
+// whole iteration of other work to hide behind.  Fact columns are register
+// double-buffered 8-byte vectors and prefetched into L2 two steps ahead.
+// ---------------------------------------------------------------------------
+struct PipeState {
+  uint32_t lo[2], hi[2], id[2], m[2];
+};
+
+__device__ __forceinline__ int comp2(const int2& v, int i) { return i == 0 ? v.x : v.y; }
+
+__device__ __forceinline__ int2 ld2(const Col& c, int64_t row0, int64_t n, bool inb) {
+  const int2* p = reinterpret_cast<const int2*>(static_cast<const int32_t*>(c.p) + row0);
+  return inb || row0 < n ? __ldcs(p) : make_int2(0, 0);  // columns are padded past the end
+}
+
+template <int NQ, int NL, int NF, bool TAIL>
+__device__ __forceinline__ void pipe_stage_a(const BatchScan& B, int64_t row0, const int2 (&kv)[NL],
+                                             const int2 (&fv)[NF > 0 ? NF : 1], const int2& mv, uint32_t s_base,
+                                             uint32_t dec_base, PipeState& st) {
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const bool past = TAIL && row0 + r >= B.n;
+    st.lo[r] = past ? B.fail_lo : B.init_lo;
+    st.hi[r] = past ? B.fail_hi : B.init_hi;
+    st.m[r] = static_cast<uint32_t>(comp2(mv, r));
+  }
+#pragma unroll
+  for (int f = 0; f < NF; ++f)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const uint32_t flo = static_cast<uint32_t>(B.ff_lo[f][q]);
+      const uint32_t span = static_cast<uint32_t>(B.ff_hi[f][q]) - flo;
+      const uint32_t add = kLaneFail << (16 * (q & 1));
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const uint32_t a = static_cast<uint32_t>(comp2(fv[f], r)) - flo > span ? add : 0u;
+        if (q < 2) st.lo[r] += a;
+        else st.hi[r] += a;
+      }
+    }
+  const uint32_t sh = B.dec_shift;
+#pragma unroll
+  for (int j = 0; j < NL; ++j) {
+    const BatchLink& L = B.link[j];
+    uint32_t sl[2], id[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) sl[r] = min(static_cast<uint32_t>(comp2(kv[j], r)) - L.base, L.size);
+    if (L.fmt == kIdSmemU8) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) id[r] = lds_u8(s_base + L.id_byte + sl[r]);
+    } else if (L.fmt == kIdSmemU16) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) id[r] = lds_u16(s_base + L.id_byte + 2 * sl[r]);
+    } else {
+      bool go[2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        bool alive = false;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) alive = alive || lane_of(st.lo[r], st.hi[r], q) < kLaneFail;
+        go[r] = alive;
+        if (L.bm_byte >= 0)
+          go[r] = go[r] && ((lds_u32(s_base + L.bm_byte + 4 * (sl[r] >> 5)) >> (sl[r] & 31)) & 1u);
+      }
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+        id[r] = L.fmt == kIdGlobU8 ? ldg_u8_if(go[r], static_cast<const uint8_t*>(L.ids) + sl[r], L.miss)
+                                   : ldg_u16_if(go[r], static_cast<const uint16_t*>(L.ids) + sl[r], L.miss);
+    }
+    if (j == NL - 1) {  // the last link's decode waits for stage B (one iteration later)
+#pragma unroll
+      for (int r = 0; r < 2; ++r) st.id[r] = id[r];
+    } else {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const uint2 d = lds_u64(dec_base + L.dec_byte + (id[r] << sh));
+        st.lo[r] += d.x;
+        st.hi[r] += d.y;
+      }
+    }
+  }
+}
+
+template <int NQ, int NL, int MODE>
+__device__ __forceinline__ void pipe_stage_b(const BatchScan& B, const PipeState& st, uint32_t s_base,
+                                             uint32_t dec_base) {
+  const BatchLink& L = B.link[NL - 1];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const uint2 d = lds_u64(dec_base + L.dec_byte + (st.id[r] << B.dec_shift));
+    const uint32_t lo = st.lo[r] + d.x, hi = st.hi[r] + d.y;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const uint32_t g = lane_of(lo, hi, q);
+      const bool ok = g < kLaneFail;
+      if constexpr (MODE == 1) {
+        const uint32_t ad = s_base + B.bins_byte[q] + 4u * g;
+        reds_add_if(ok, ad, 1u);
+        reds_add_if(ok, ad + 4u * static_cast<uint32_t>(B.G[q]), st.m[r]);
+      } else {
+        reds_add_if(ok, s_base + B.bins_byte[q] + 4u * g, st.m[r]);
+      }
+    }
+  }
+}
+
+template <int NQ, int NL, int NF, int MODE>
+__global__ void __launch_bounds__(kDirectThreads, 1) scan_batch_pipe_kernel(const __grid_constant__ BatchScan B) {
+  static_assert(MODE == 1 || MODE == 2, "bins modes only");
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int tid = threadIdx.x;
+  auto stage = [&](const void* src, int byte, int bytes) {
+    const uint4* s = static_cast<const uint4*>(src);
+    uint4* d = reinterpret_cast<uint4*>(smem + byte);
+    for (int w = tid; w < bytes / 16; w += kDirectThreads) d[w] = __ldg(s + w);
+  };
+  const int rep = 1 << (B.dec_shift - 3);
+#pragma unroll
+  for (int j = 0; j < NL; ++j) {
+    const BatchLink& L = B.link[j];
+    if (L.fmt == kIdSmemU8 || L.fmt == kIdSmemU16) stage(L.ids, L.id_byte, L.id_bytes);
+    unsigned long long* d = reinterpret_cast<unsigned long long*>(smem + L.dec_byte);
+    for (int w = tid; w < L.n_dec * rep; w += kDirectThreads) d[w] = __ldg(L.dec + w / rep);
+    if (L.bm_byte >= 0) stage(L.bm, L.bm_byte, L.bm_bytes);
+  }
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    uint32_t* b = reinterpret_cast<uint32_t*>(smem + B.bins_byte[q]);
+    for (int64_t g = tid; g < (MODE == 1 ? 2 : 1) * B.G[q]; g += kDirectThreads) b[g] = 0;
+  }
+  __syncthreads();
+  const uint32_t s_base = smem_u32(smem);
+  const uint32_t dec_base = s_base + 8u * static_cast<uint32_t>(tid & (rep - 1));
+
+  const int64_t step = static_cast<int64_t>(gridDim.x) * kDirectThreads * 2;
+  const int64_t iters = (B.n + step - 1) / step;
+  const int64_t full = B.n / step;
+  int64_t row0 = (static_cast<int64_t>(blockIdx.x) * kDirectThreads + tid) * 2;
+  const bool pf_lane = B.prefetch && (tid & 15) == 0;  // one 128-byte line per 16 lanes
+  const int64_t pf_rows = static_cast<int64_t>(B.prefetch) * step;
+
+  int2 kvA[NL], fvA[NF > 0 ? NF : 1], mvA = make_int2(0, 0);
+  int2 kvB[NL], fvB[NF > 0 ? NF : 1], mvB = make_int2(0, 0);
+  auto load = [&](int2 (&kv)[NL], int2 (&fv)[NF > 0 ? NF : 1], int2& mv, int64_t r, bool inb) {
+#pragma unroll
+    for (int j = 0; j < NL; ++j) kv[j] = ld2(B.fkc[j], r, B.n, inb);
+#pragma unroll
+    for (int f = 0; f < NF; ++f) fv[f] = ld2(B.ffc[f], r, B.n, inb);
+    if (B.has_measure) mv = ld2(B.mc, r, B.n, inb);
+  };
+  PipeState sA, sB;
+  load(kvA, fvA, mvA, row0, full > 0);
+  int64_t until_flush = B.flush_every;
+  // iteration it: loads for it+1, stage A(it), stage B(it-1)
+  auto one = [&](int64_t it, const int2 (&kv)[NL], const int2 (&fv)[NF > 0 ? NF : 1], const int2& mv,
+                 int2 (&nkv)[NL], int2 (&nfv)[NF > 0 ? NF : 1], int2& nmv, PipeState& cur, const PipeState& prev) {
+    if (it + 1 < iters) load(nkv, nfv, nmv, row0 + step, it + 1 < full);
+    if (pf_lane && row0 + pf_rows < B.n) {
+#pragma unroll
+      for (int j = 0; j < NL; ++j) prefetch_l2<0>(B.fkc[j], row0 + pf_rows);
+#pragma unroll
+      for (int f = 0; f < NF; ++f) prefetch_l2<0>(B.ffc[f], row0 + pf_rows);
+      if (B.has_measure) prefetch_l2<0>(B.mc, row0 + pf_rows);
+    }
+    if (it < full) pipe_stage_a<NQ, NL, NF, false>(B, row0, kv, fv, mv, s_base, dec_base, cur);
+    else pipe_stage_a<NQ, NL, NF, true>(B, row0, kv, fv, mv, s_base, dec_base, cur);
+    if (it > 0) {
+      pipe_stage_b<NQ, NL, MODE>(B, prev, s_base, dec_base);
+      if (--until_flush == 0) {
+        until_flush = B.flush_every;
+        __syncthreads();
+        spill_all<NQ, MODE>(B, smem, tid);
+        __syncthreads();
+      }
+    }
+    row0 += step;
+  };
+  for (int64_t it = 0; it < iters; it += 2) {
+    one(it, kvA, fvA, mvA, kvB, fvB, mvB, sA, sB);
+    if (it + 1 < iters) one(it + 1, kvB, fvB, mvB, kvA, fvA, mvA, sB, sA);
+  }
+  if (iters > 0) pipe_stage_b<NQ, NL, MODE>(B, (iters & 1) ? sA : sB, s_base, dec_base);
+  __syncthreads();
+  spill_all<NQ, MODE>(B, smem, tid);
+}
+
 template <int NQ, int NL, int NF, int MODE>
 void launch_batch_t(laq_ctx* ctx, const BatchScan& B, size_t smem, int grid) {
+  if constexpr (MODE != 0) {
+    if (B.pipe) {
+      auto kern = scan_batch_pipe_kernel<NQ, NL, NF, MODE>;
+      LAQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      const int64_t blocks_needed = (B.n + kDirectThreads * 2 - 1) / (kDirectThreads * 2);
+      const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(grid, blocks_needed)));
+      kern<<<g, kDirectThreads, smem, ctx->stream>>>(B);
+      return;
+    }
+  }
   auto kern = scan_batch_kernel<NQ, NL, NF, MODE>;
   LAQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int64_t blocks_needed = (B.n + kDirectThreads * 4 - 1) / (kDirectThreads * 4);

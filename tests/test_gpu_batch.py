@@ -176,3 +176,31 @@ def test_sf10_bench_groups_fused_vs_golden(gpu_ctx):
         assert b.fused, b.why
         for m, x in zip(got, sel):
             assert m.shape == (x["rows"], x["cols"]) and np.array_equal(m.ravel(), fa(x["result"])), x["id"]
+
+
+@pytest.mark.parametrize("env", [{"LAQ_NOSMEMTAB": "1"}, {"LAQ_NOSMEMTAB": "1", "LAQ_BATCH_NO_PIPE": "1"},
+                                 {"LAQ_BATCH_COUNT_BINS": "1"}, {"LAQ_BATCH_SUM_BINS": "1", "LAQ_NOSMEMTAB": "1"}])
+def test_layout_variants_match_oracle(gpu_ctx, monkeypatch, env):
+    """Every kernel form the layout can pick: all links gathered through L2
+    (the software-pipelined 2-row kernel for the last link, synchronous
+    gathers for the others), the unpipelined form, (count, sum) vs sum-only
+    bins -- same results as the oracle on the SSB groups and random batches."""
+    from paper_2306_08367_b200 import gen, star
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    g = gen.gen_star("S2", 2, 42, narrow=True)
+    ds = star.upload_gen_star(g)
+    for grp in (2, 3, 4):
+        qs = ds.gen_queries(grp)
+        b, got = _run_batch(ds, qs)
+        assert b.fused, b.why
+        for q, m in zip(qs, got):
+            assert np.array_equal(m, O.run_query(g.tables, q)), (env, q.id)
+    rng = np.random.default_rng(77)
+    for trial in range(6):
+        tables, kinds, links, joins = _random_star(rng, int(rng.integers(1, 300_000)), dangling=0.02 * (trial % 2))
+        dsr = star.DeviceStar.from_tables(tables, kinds, links)
+        qs = [_random_query(rng, joins, i) for i in range(int(rng.integers(2, 5)))]
+        b, got = _run_batch(dsr, qs)
+        for q, m in zip(qs, got):
+            assert np.array_equal(m, O.run_query(tables, q)), (env, trial, q, b.fused, b.why)
