@@ -569,7 +569,7 @@ void run_slot_predict(laq_ctx* ctx, laq_probe* p, const int32_t* const* d_fks, i
           p->chunk_cap = chunks1;
         }
         LAQ_CUDA(cudaFuncSetAttribute(direct_one_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_w)));
-        const unsigned g1 = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(chunks1, ctx->sm_count)));
+        const unsigned g1 = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((chunks1 + 31) / 32, ctx->sm_count)));
         direct_one_k<<<g1, slot::kDirectBT, smem_w, ctx->stream>>>(a, chunks1, p->chunk_counts.get(), miss,
                                                                    p->miss.get() + 2, p->chunk_offsets.get());
         return;

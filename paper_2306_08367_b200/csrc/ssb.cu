@@ -1601,10 +1601,16 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
   std::iota(by.begin(), by.end(), 0);
   std::stable_sort(by.begin(), by.end(), [&](int x, int y) { return idb[x] < idb[y]; });
   std::vector<char> staged(b->nl, 0), use_bm(b->nl, 0);
+  if (std::getenv("LAQ_BATCH_BITMAP_FIRST") && b->nl > 0) {
+    // A/B knob: the largest link keeps only its any-pass bitmap in shared
+    // memory (its ids gathered through L2) before the id tables are placed.
+    const int big = by.back();
+    if (bmb[big] <= room && frac[big] < 0.75) use_bm[big] = 1, room -= bmb[big];
+  }
   for (int j : by)
-    if (!std::getenv("LAQ_NOSMEMTAB") && idb[j] <= room) staged[j] = 1, room -= idb[j];
+    if (!std::getenv("LAQ_NOSMEMTAB") && !use_bm[j] && idb[j] <= room) staged[j] = 1, room -= idb[j];
   for (int j : by)
-    if (!staged[j] && bmb[j] <= room && frac[j] < 0.75) use_bm[j] = 1, room -= bmb[j];
+    if (!staged[j] && !use_bm[j] && bmb[j] <= room && frac[j] < 0.75) use_bm[j] = 1, room -= bmb[j];
   // Decode tables replicated `rep` times (entry-interleaved) with what room is
   // left: lane l reads copy l % rep, so a warp's 32 random decodes conflict at
   // most 32/rep-way on a bank instead of colliding on the few entries' banks.
@@ -1697,9 +1703,11 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
     (q < 2 ? B.fail_lo : B.fail_hi) += f;
     if (reject_mask & (1u << q)) (q < 2 ? B.init_lo : B.init_hi) += f;
   }
-  // Software pipelining of the last link's L2 gather (scan_batch_pipe_kernel)
-  // when that link is gathered and the bins live in shared memory.
-  B.pipe = !staged[order[b->nl - 1]] && mode != 0 && !std::getenv("LAQ_BATCH_NO_PIPE") ? 1 : 0;
+  // Software pipelining of the last link's L2 gather (scan_batch_pipe_kernel,
+  // 2 rows per thread) when that link is gathered: opt-in (LAQ_BATCH_PIPE=1).
+  // It removes the gather stalls (long-scoreboard 33 % -> 5 %) but doubles the
+  // per-row instruction count: SF=100 Q4 group 3.22 -> 3.48 ms, issue-bound.
+  B.pipe = !staged[order[b->nl - 1]] && mode != 0 && std::getenv("LAQ_BATCH_PIPE") ? 1 : 0;
   B.dec_shift = 3;
   while ((1 << (B.dec_shift - 3)) < rep) ++B.dec_shift;
   B.flush_every = flush;
