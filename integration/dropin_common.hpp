@@ -47,7 +47,10 @@ inline void check(int rc) {
   if (rc != LAQ_OK) raise(rc, laq_ctx_last_error(ctx()));
 }
 
-// Device mirror of a host vector (freed on scope exit).
+// Device mirror of a host vector (freed on scope exit).  Allocated from the
+// stream-ordered pool on the legacy stream, which the drop-in's context runs on
+// (laq_ctx_create keeps freed blocks in the pool): a value-type call allocates
+// and frees several buffers, and cudaMalloc/cudaFree synchronise the device.
 template <class T>
 struct Dev {
   T* p = nullptr;
@@ -55,7 +58,7 @@ struct Dev {
   Dev() = default;
   explicit Dev(size_t count) : n(count) {
     ctx();
-    if (n && cudaMalloc(reinterpret_cast<void**>(&p), n * sizeof(T)) != cudaSuccess)
+    if (n && cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(T), 0) != cudaSuccess)
       throw CapacityError("laq_b200: device allocation of " + std::to_string(n * sizeof(T)) + " bytes failed");
   }
   Dev(const T* h, size_t count) : Dev(count) { up(h, count); }
@@ -64,14 +67,14 @@ struct Dev {
   Dev& operator=(const Dev&) = delete;
   Dev(Dev&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; }
   Dev& operator=(Dev&& o) noexcept {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, 0);
     p = o.p;
     n = o.n;
     o.p = nullptr;
     return *this;
   }
   ~Dev() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, 0);
   }
   void up(const T* h, size_t m) {
     if (m && cudaMemcpy(p, h, m * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess) throw Error("laq_b200: H2D");
