@@ -1586,10 +1586,20 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
   const int64_t bin_words = mode == 1 ? 2 : 1;  // u32 words per group (room reserved for (count, sum) bins)
   if (mode != 0)
     for (const laq_plan* p : b->plans) bins += (4 * bin_words * p->G + 15) & ~int64_t{15};
+  // Narrow decode (4-byte entries, 3 x 10-bit lanes) when every lane fits:
+  // contributions < fail32 (a power of two >= every G) and at most
+  // (links + fact filters + 1) fails: G - 1 + (nl + nf + 1) * fail32 < 1024.
+  int64_t max_g = 1;
+  for (const laq_plan* p : b->plans) max_g = std::max<int64_t>(max_g, p->G);
+  int64_t f32 = 1;
+  while (f32 < max_g) f32 <<= 1;
+  const bool dec32 = nq <= 3 && b->nl <= 3 && !std::getenv("LAQ_BATCH_PIPE") && !std::getenv("LAQ_BATCH_DEC64") &&
+                     (max_g - 1) + (b->nl + b->nf + 1) * f32 <= 1023;
+  const int64_t dec_entry = dec32 ? 4 : 8;
   std::vector<int64_t> decb(b->nl), idb(b->nl), bmb(b->nl);
   std::vector<int> idw(b->nl);
   for (int j = 0; j < b->nl; ++j) {
-    decb[j] = (8 * int64_t{b->n_dec[j]} + 15) & ~int64_t{15};
+    decb[j] = (dec_entry * int64_t{b->n_dec[j]} + 15) & ~int64_t{15};
     idw[j] = b->n_dec[j] <= 256 ? 1 : 2;
     idb[j] = ((D.l[j].slots + 1) * idw[j] + 15) & ~int64_t{15};
     bmb[j] = (((D.l[j].slots + 32) / 32) * 4 + 15) & ~int64_t{15};
@@ -1698,7 +1708,14 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
     flush = std::min<int64_t>(flush, std::max<int64_t>(1, p->scan.flush_every));
   }
   B.init_lo = B.init_hi = B.fail_lo = B.fail_hi = 0;
+  B.dec32 = dec32 ? 1 : 0;
+  B.fail32 = static_cast<uint32_t>(f32);
   for (int q = 0; q < nq; ++q) {
+    if (dec32) {
+      B.fail_lo += static_cast<uint32_t>(f32) << (10 * q);
+      if (reject_mask & (1u << q)) B.init_lo += static_cast<uint32_t>(f32) << (10 * q);
+      continue;
+    }
     const uint32_t f = kLaneFail << (16 * (q & 1));
     (q < 2 ? B.fail_lo : B.fail_hi) += f;
     if (reject_mask & (1u << q)) (q < 2 ? B.init_lo : B.init_hi) += f;
@@ -1708,8 +1725,8 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
   // It removes the gather stalls (long-scoreboard 33 % -> 5 %) but doubles the
   // per-row instruction count: SF=100 Q4 group 3.22 -> 3.48 ms, issue-bound.
   B.pipe = !staged[order[b->nl - 1]] && mode != 0 && std::getenv("LAQ_BATCH_PIPE") ? 1 : 0;
-  B.dec_shift = 3;
-  while ((1 << (B.dec_shift - 3)) < rep) ++B.dec_shift;
+  B.dec_shift = dec32 ? 2 : 3;  // log2(entry bytes * rep)
+  while ((1 << (B.dec_shift - (dec32 ? 2 : 3))) < rep) ++B.dec_shift;
   B.flush_every = flush;
   B.prefetch = gathers ? 2 : 0;
   if (const char* pf = std::getenv("LAQ_PREFETCH")) B.prefetch = std::atoi(pf);

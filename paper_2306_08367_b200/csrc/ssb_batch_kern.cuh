@@ -28,6 +28,27 @@ __device__ __forceinline__ uint32_t lane_of(uint32_t lo, uint32_t hi, int q) {
   return (q & 1) ? (w >> 16) : (w & 0xFFFFu);
 }
 
+// Accumulator layouts.  DW = 64: 4 x 16-bit lanes in (lo, hi), fail = 4096.
+// DW = 32 (narrow decode, up to 3 queries): 3 x 10-bit lanes in lo alone, fail
+// = B.fail32 (a power of two >= every G; the host checks that G - 1 + (links +
+// filters + 1) fails fit 10 bits): one 4-byte decode load per link instead of
+// 8 bytes (half the shared-memory wavefronts of the decode).
+template <int DW>
+__device__ __forceinline__ uint32_t lane_w(uint32_t lo, uint32_t hi, int q) {
+  if constexpr (DW == 64) return lane_of(lo, hi, q);
+  else return (lo >> (10 * q)) & 0x3FFu;
+}
+template <int DW>
+__device__ __forceinline__ void add_fail(const BatchScan& B, uint32_t& lo, uint32_t& hi, int q, bool f) {
+  if constexpr (DW == 64) {
+    const uint32_t a = f ? (kLaneFail << (16 * (q & 1))) : 0u;
+    if (q < 2) lo += a;
+    else hi += a;
+  } else {
+    lo += f ? (B.fail32 << (10 * q)) : 0u;
+  }
+}
+
 // Predicated (branch-free) shared atomic add and L2 gathers.
 __device__ __forceinline__ void reds_add_if(bool p, uint32_t addr, uint32_t v) {
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q red.shared.add.u32 [%0], %1;\n}" ::"r"(addr), "r"(v),
@@ -64,17 +85,18 @@ __device__ __forceinline__ int4 ld4_nb(const Col& c, int64_t row0) {
 // MODE 0: per-thread register sums (every query has one group); MODE 1: u32
 // (count, sum) bins; MODE 2: u32 sum bins only -- the measure is positive, so
 // a group is present iff its sum is non-zero (half the shared atomics).
-template <int NQ, int NL, int NF, int MODE, bool TAIL>
+template <int NQ, int NL, int NF, int MODE, int DW, bool TAIL>
 __device__ __forceinline__ void batch_rows(const BatchScan& B, int64_t row0, const int4 (&kv)[NL],
                                            const int4 (&fv)[NF > 0 ? NF : 1], const int4& mv, uint32_t s_base,
                                            uint32_t dec_base, uint32_t (&r_cnt)[NQ],
                                            unsigned long long (&r_sum)[NQ]) {
+  const uint32_t FL = DW == 64 ? kLaneFail : B.fail32;
   uint32_t lo[4], hi[4];
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const bool past = TAIL && row0 + r >= B.n;
     lo[r] = past ? B.fail_lo : B.init_lo;
-    hi[r] = past ? B.fail_hi : B.init_hi;
+    hi[r] = DW == 32 ? 0u : (past ? B.fail_hi : B.init_hi);
   }
 #pragma unroll
   for (int f = 0; f < NF; ++f)
@@ -82,15 +104,11 @@ __device__ __forceinline__ void batch_rows(const BatchScan& B, int64_t row0, con
     for (int q = 0; q < NQ; ++q) {
       const uint32_t flo = static_cast<uint32_t>(B.ff_lo[f][q]);
       const uint32_t span = static_cast<uint32_t>(B.ff_hi[f][q]) - flo;
-      const uint32_t add = kLaneFail << (16 * (q & 1));
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const uint32_t a = static_cast<uint32_t>(comp(fv[f], r)) - flo > span ? add : 0u;
-        if (q < 2) lo[r] += a;
-        else hi[r] += a;
-      }
+      for (int r = 0; r < 4; ++r)
+        add_fail<DW>(B, lo[r], hi[r], q, static_cast<uint32_t>(comp(fv[f], r)) - flo > span);
     }
-  const uint32_t sh = B.dec_shift;  // log2(8 * dec_rep)
+  const uint32_t sh = B.dec_shift;  // log2(entry bytes * dec_rep)
 #pragma unroll
   for (int j = 0; j < NL; ++j) {
     const BatchLink& L = B.link[j];
@@ -111,7 +129,7 @@ __device__ __forceinline__ void batch_rows(const BatchScan& B, int64_t row0, con
       for (int r = 0; r < 4; ++r) {
         bool alive = false;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) alive = alive || lane_of(lo[r], hi[r], q) < kLaneFail;
+        for (int q = 0; q < NQ; ++q) alive = alive || lane_w<DW>(lo[r], hi[r], q) < FL;
         go[r] = alive;
       }
       if (L.bm_byte >= 0) {
@@ -129,9 +147,13 @@ __device__ __forceinline__ void batch_rows(const BatchScan& B, int64_t row0, con
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      const uint2 d = lds_u64(dec_base + L.dec_byte + (id[r] << sh));
-      lo[r] += d.x;
-      hi[r] += d.y;
+      if constexpr (DW == 64) {
+        const uint2 d = lds_u64(dec_base + L.dec_byte + (id[r] << sh));
+        lo[r] += d.x;
+        hi[r] += d.y;
+      } else {
+        lo[r] += lds_u32(dec_base + L.dec_byte + (id[r] << sh));
+      }
     }
   }
 #pragma unroll
@@ -139,8 +161,8 @@ __device__ __forceinline__ void batch_rows(const BatchScan& B, int64_t row0, con
     const uint32_t m = static_cast<uint32_t>(comp(mv, r));
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-      const uint32_t g = lane_of(lo[r], hi[r], q);
-      const bool ok = g < kLaneFail;
+      const uint32_t g = lane_w<DW>(lo[r], hi[r], q);
+      const bool ok = g < FL;
       if constexpr (MODE == 0) {
         r_cnt[q] += ok ? 1u : 0u;
         r_sum[q] += ok ? static_cast<unsigned long long>(static_cast<long long>(static_cast<int32_t>(m))) : 0ull;
@@ -178,7 +200,7 @@ __device__ __forceinline__ void spill_all(const BatchScan& B, unsigned char* sme
   }
 }
 
-template <int NQ, int NL, int NF, int MODE>
+template <int NQ, int NL, int NF, int MODE, int DW>
 __global__ void __launch_bounds__(kDirectThreads, 1) scan_batch_kernel(const __grid_constant__ BatchScan B) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x;
@@ -187,13 +209,28 @@ __global__ void __launch_bounds__(kDirectThreads, 1) scan_batch_kernel(const __g
     uint4* d = reinterpret_cast<uint4*>(smem + byte);
     for (int w = tid; w < bytes / 16; w += kDirectThreads) d[w] = __ldg(s + w);
   };
-  const int rep = 1 << (B.dec_shift - 3);
+  const int rep = 1 << (B.dec_shift - (DW == 64 ? 3 : 2));
 #pragma unroll
   for (int j = 0; j < NL; ++j) {
     const BatchLink& L = B.link[j];
     if (L.fmt == kIdSmemU8 || L.fmt == kIdSmemU16) stage(L.ids, L.id_byte, L.id_bytes);
-    unsigned long long* d = reinterpret_cast<unsigned long long*>(smem + L.dec_byte);
-    for (int w = tid; w < L.n_dec * rep; w += kDirectThreads) d[w] = __ldg(L.dec + w / rep);  // entry-interleaved copies
+    if constexpr (DW == 64) {
+      unsigned long long* d = reinterpret_cast<unsigned long long*>(smem + L.dec_byte);
+      for (int w = tid; w < L.n_dec * rep; w += kDirectThreads) d[w] = __ldg(L.dec + w / rep);  // entry-interleaved copies
+    } else {
+      // 16-bit lanes (fail = 4096) -> 10-bit lanes (fail = B.fail32)
+      uint32_t* d = reinterpret_cast<uint32_t*>(smem + L.dec_byte);
+      for (int w = tid; w < L.n_dec * rep; w += kDirectThreads) {
+        const unsigned long long e = __ldg(L.dec + w / rep);
+        uint32_t v = 0;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const uint32_t x = static_cast<uint32_t>(e >> (16 * q)) & 0xFFFFu;
+          v |= (x >= kLaneFail ? B.fail32 : x) << (10 * q);
+        }
+        d[w] = v;
+      }
+    }
     if (L.bm_byte >= 0) stage(L.bm, L.bm_byte, L.bm_bytes);
   }
   if constexpr (MODE != 0) {
@@ -206,7 +243,7 @@ __global__ void __launch_bounds__(kDirectThreads, 1) scan_batch_kernel(const __g
   __syncthreads();
 
   const uint32_t s_base = smem_u32(smem);
-  const uint32_t dec_base = s_base + 8u * static_cast<uint32_t>(tid & (rep - 1));
+  const uint32_t dec_base = s_base + (DW == 64 ? 8u : 4u) * static_cast<uint32_t>(tid & (rep - 1));
   uint32_t r_cnt[NQ];
   unsigned long long r_sum[NQ];
 #pragma unroll
@@ -249,9 +286,9 @@ __global__ void __launch_bounds__(kDirectThreads, 1) scan_batch_kernel(const __g
       if (B.has_measure) prefetch_l2<0>(B.mc, row0 + pf_rows);
     }
     if (it < full)
-      batch_rows<NQ, NL, NF, MODE, false>(B, row0, kv, fv, mv, s_base, dec_base, r_cnt, r_sum);
+      batch_rows<NQ, NL, NF, MODE, DW, false>(B, row0, kv, fv, mv, s_base, dec_base, r_cnt, r_sum);
     else
-      batch_rows<NQ, NL, NF, MODE, true>(B, row0, kv, fv, mv, s_base, dec_base, r_cnt, r_sum);
+      batch_rows<NQ, NL, NF, MODE, DW, true>(B, row0, kv, fv, mv, s_base, dec_base, r_cnt, r_sum);
     if constexpr (MODE != 0) {
       if (--until_flush == 0) {
         until_flush = B.flush_every;
@@ -480,7 +517,10 @@ void launch_batch_t(laq_ctx* ctx, const BatchScan& B, size_t smem, int grid) {
       return;
     }
   }
-  auto kern = scan_batch_kernel<NQ, NL, NF, MODE>;
+  auto kern = scan_batch_kernel<NQ, NL, NF, MODE, 64>;
+  if constexpr (NQ <= 3 && NL <= 3) {
+    if (B.dec32) kern = scan_batch_kernel<NQ, NL, NF, MODE, 32>;
+  }
   LAQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int64_t blocks_needed = (B.n + kDirectThreads * 4 - 1) / (kDirectThreads * 4);
   const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(grid, blocks_needed)));
