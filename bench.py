@@ -477,8 +477,8 @@ def main():
                         "batch_not_fused_why": [b.why for b in batches if not b.fused],
                         "result_rows": [int(r.shape[0]) for r in results],
                         "lineorder_rows_per_gpu": n_local,
-                        "parallelism": f"row-sharded x{world}, int64 accumulators all-reduced by the C-ABI's "
-                                       f"NCCL communicator" if world > 1 else "1 GPU",
+                        "parallelism": f"row-sharded x{world}, int64 accumulators all-reduced through the "
+                                       f"C-ABI: {ctx.transport}" if world > 1 else "1 GPU",
                         "gen_s": round(gen_s, 1), "device_tuning_s": round(tune_s, 2)},
             "fused_join_predict": fused,
         }

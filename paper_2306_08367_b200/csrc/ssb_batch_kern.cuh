@@ -70,6 +70,17 @@ __device__ __forceinline__ uint32_t ldg_u16_if(bool p, const void* ptr, uint32_t
   return v;
 }
 
+// Bulk L2 prefetch on the TMA engine (one instruction moves a warp's 512-byte
+// slice of a column; no LSU wavefronts, no registers).
+__device__ __forceinline__ void bulk_prefetch_l2(const Col& c, int64_t row0, int64_t n) {
+  const int64_t rows = min(static_cast<int64_t>(128), n - row0);
+  if (rows <= 0) return;
+  const uint32_t bytes = static_cast<uint32_t>((rows * 4 + 15) & ~int64_t{15});
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(static_cast<const int32_t*>(c.p) + row0),
+               "r"(bytes)
+               : "memory");
+}
+
 // Row loads without the bounds test (steps whose rows are all in range).
 __device__ __forceinline__ int4 ld4_nb(const Col& c, int64_t row0) {
   return __ldcs(reinterpret_cast<const int4*>(static_cast<const int32_t*>(c.p) + row0));
@@ -253,8 +264,11 @@ __global__ void __launch_bounds__(kDirectThreads, 1) scan_batch_kernel(const __g
   const int64_t iters = (B.n + step - 1) / step;
   const int64_t full = B.n / step;
   int64_t row0 = (static_cast<int64_t>(blockIdx.x) * kDirectThreads + tid) * 4;
-  const bool pf_lane = B.prefetch && (tid & 7) == 0;
-  const int64_t pf_rows = static_cast<int64_t>(B.prefetch) * step;
+  // prefetch > 0: prefetch.global.L2 by every 8th lane; prefetch < 0: TMA bulk
+  // prefetch of the warp's slice by lane 0, |prefetch| steps ahead
+  const bool pf_lane = B.prefetch > 0 && (tid & 7) == 0;
+  const bool pf_bulk = B.prefetch < 0 && (tid & 31) == 0;
+  const int64_t pf_rows = static_cast<int64_t>(B.prefetch < 0 ? -B.prefetch : B.prefetch) * step;
 
   int4 kvA[NL], fvA[NF > 0 ? NF : 1], mvA = make_int4(0, 0, 0, 0);
   int4 kvB[NL], fvB[NF > 0 ? NF : 1], mvB = make_int4(0, 0, 0, 0);
@@ -284,6 +298,13 @@ __global__ void __launch_bounds__(kDirectThreads, 1) scan_batch_kernel(const __g
 #pragma unroll
       for (int f = 0; f < NF; ++f) prefetch_l2<0>(B.ffc[f], row0 + pf_rows);
       if (B.has_measure) prefetch_l2<0>(B.mc, row0 + pf_rows);
+    }
+    if (pf_bulk && row0 + pf_rows < B.n) {
+#pragma unroll
+      for (int j = 0; j < NL; ++j) bulk_prefetch_l2(B.fkc[j], row0 + pf_rows, B.n);
+#pragma unroll
+      for (int f = 0; f < NF; ++f) bulk_prefetch_l2(B.ffc[f], row0 + pf_rows, B.n);
+      if (B.has_measure) bulk_prefetch_l2(B.mc, row0 + pf_rows, B.n);
     }
     if (it < full)
       batch_rows<NQ, NL, NF, MODE, DW, false>(B, row0, kv, fv, mv, s_base, dec_base, r_cnt, r_sum);

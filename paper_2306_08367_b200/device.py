@@ -17,6 +17,8 @@ _tls = threading.local()
 class Context:
     """laq_ctx (include/laq_b200.h): one device, one stream."""
 
+    transport = "single process"  # set by dist.attach
+
     def __init__(self, device: int = 0):
         if not torch.cuda.is_available():
             raise errors.CudaError("no CUDA device: the LAQ engine has no CPU fallback")

@@ -32,14 +32,35 @@ def attach(ctx, group=None):
         return ctx
     if dist.get_backend(group) == "nccl":
         from .device import nccl_unique_id
-        obj = [nccl_unique_id() if rank == 0 else None]
+        try:
+            obj = [nccl_unique_id() if rank == 0 else None]
+        except Exception as e:  # libnccl.so.2 not loadable from the library
+            obj = [e]
         dist.broadcast_object_list(obj, src=0, group=group)
-        ctx.attach_nccl(world, rank, obj[0])
+        ok = not isinstance(obj[0], Exception)
+        if ok:
+            try:
+                ctx.attach_nccl(world, rank, obj[0])
+            except Exception:
+                ok = False
+        flag = torch.tensor([1 if ok else 0], device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        if flag.item() == 1:
+            ctx.transport = "nccl (C-ABI communicator)"
+            return ctx
+        # Fallback: the same int64 all-reduce through torch's NCCL group.
+        def hook(buf):
+            t = torch.from_numpy(buf).cuda()
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+            buf[:] = t.cpu().numpy()
+        ctx.set_allreduce_host(world, rank, hook)
+        ctx.transport = "nccl (torch.distributed via the C-ABI host hook)"
     else:
         def hook(buf):
             t = torch.from_numpy(buf)  # shares memory with the C buffer
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
         ctx.set_allreduce_host(world, rank, hook)
+        ctx.transport = "gloo (C-ABI host hook)"
     return ctx
 
 
