@@ -380,10 +380,15 @@ def main():
     launches0 = ctx.launches
     clocks.mark()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    prof = os.environ.get("LAQ_PROFILE_TIMED") == "1"  # ncu --profile-from-start off: the timed steps only
+    if prof:
+        torch.cuda.cudart().cudaProfilerStart()
     t_start.record(stream)
     results = run(args.steps, True)
     t_end.record(stream)
     torch.cuda.synchronize()
+    if prof:
+        torch.cuda.cudart().cudaProfilerStop()
     clocks.mark()
     clk = clocks.stop()
     launches = ctx.launches - launches0

@@ -258,14 +258,24 @@ DenseMat general_query(const StarSchema& data, const bench::QuerySpec& q) {
 }
 
 // ---- the fast path: a cached int32 device star per StarSchema -----------------
-uint64_t fingerprint(const std::int64_t* p, size_t n) {  // size + 64 sampled values + both ends
+// Identity of a cached column: (data pointer, size) plus this fingerprint --
+// 4096 values sampled evenly over the column and its first and last 256 values.
+// The reference's Table is immutable through its API; what the fingerprint
+// guards against is a Table destroyed or reassigned (same-size vector storage
+// can be reused) with different contents.  Columns under 8K rows are hashed in
+// full.  LAQ_DROPIN_CACHE=0 disables the cache.
+uint64_t fingerprint(const std::int64_t* p, size_t n) {
   uint64_t h = 0xcbf29ce484222325ull ^ n;
   auto mix = [&](uint64_t v) {
     h ^= v;
     h *= 0x100000001b3ull;
   };
-  for (size_t k = 0; k < 64 && n; ++k) mix(static_cast<uint64_t>(p[(n - 1) * k / 63]));
-  for (size_t k = 0; k < std::min<size_t>(8, n); ++k) mix(static_cast<uint64_t>(p[k]) ^ static_cast<uint64_t>(p[n - 1 - k]));
+  if (n <= 8192) {
+    for (size_t k = 0; k < n; ++k) mix(static_cast<uint64_t>(p[k]));
+    return h;
+  }
+  for (size_t k = 0; k < 4096; ++k) mix(static_cast<uint64_t>(p[(n - 1) * k / 4095]));
+  for (size_t k = 0; k < 256; ++k) mix(static_cast<uint64_t>(p[k]) ^ (static_cast<uint64_t>(p[n - 1 - k]) << 1));
   return h;
 }
 
