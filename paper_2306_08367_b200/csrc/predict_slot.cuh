@@ -211,12 +211,13 @@ __global__ void __launch_bounds__(BT, 1) direct_chunks_kernel(const Args a, int6
                                                                      int64_t* offsets = nullptr) {
   extern __shared__ __align__(16) uint32_t s_bits[];
   double* s_p = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(s_bits) + ((a.smem_words * 4 + 15) & ~15));
+  __shared__ __align__(8) uint64_t s_bar;
+  bool staged = a.bulk_bytes <= 0;  // bulk copies in flight until the first wait
   if (a.bulk_bytes > 0) {
     // One thread hands every staged table (bitmaps, slot-ordered partials) to
     // the TMA engine; the CTA waits once on the mbarrier.  (A per-thread copy
     // loop is a chain of dependent L2 round trips: at 1M rows it was most of
     // the call.)
-    __shared__ __align__(8) uint64_t s_bar;
     if (threadIdx.x == 0) {
       tc::mbar_init(&s_bar, 1);
       tc::fence_mbar_init();
@@ -229,8 +230,7 @@ __global__ void __launch_bounds__(BT, 1) direct_chunks_kernel(const Args a, int6
           tc::bulk_g2s(tc::smem_u32(s_p + a.p_off[j]), a.pslot[j], static_cast<uint32_t>(a.p_bytes[j]), &s_bar);
       }
     }
-    __syncthreads();
-    tc::mbar_wait(&s_bar, 0);
+    __syncthreads();  // the barrier's init is visible; the copies land while the first keys load
   } else {
     stage_bits(a, s_bits, NL);
 #pragma unroll
@@ -253,6 +253,10 @@ __global__ void __launch_bounds__(BT, 1) direct_chunks_kernel(const Args a, int6
     int4 kv[SEGS][NL];
 #pragma unroll
     for (int g = 0; g < SEGS; ++g) load_kv<NL>(a, c * kRows + g * kSegRows + 4 * lane, kv[g]);
+    if (!staged) {  // the staged tables are needed from here on
+      tc::mbar_wait(&s_bar, 0);
+      staged = true;
+    }
 #pragma unroll
     for (int g = 0; g < SEGS; ++g) {
       const int64_t r0 = c * kRows + g * kSegRows + 4 * lane;
@@ -283,6 +287,10 @@ __global__ void __launch_bounds__(BT, 1) direct_chunks_kernel(const Args a, int6
       const int64_t rows = min(static_cast<int64_t>(kRows), a.n - c * kRows);
       if (cnt != rows) atomicAdd(miss, 1ull);
     }
+  }
+  if (!staged) {  // no CTA may exit with bulk copies still landing in its shared memory
+    tc::mbar_wait(&s_bar, 0);
+    staged = true;
   }
   if (last == nullptr) return;
   __shared__ int s_last;
