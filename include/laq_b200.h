@@ -535,6 +535,18 @@ int laq_speedup_ratio_linear(int64_t i, int64_t k, int64_t l, const int64_t* dim
 int laq_speedup_ratio_tree(int64_t i, int64_t k, int64_t l, int64_t p, const int64_t* dim_rows,
                            int32_t n_dims, double* h_out);
 int laq_decide_fusion(double ratio, double threshold, int32_t* h_out);
+/* The B200 plan model for the tensor-core operators (no reference function:
+ * the paper's Eq. 2 above counts CPU sparse-matrix work; on the tensor cores
+ * both plans are GEMM + gather and the winner is set by tensor time vs HBM
+ * bytes).  Predicted seconds of the fused plan (prefuse P_j = B_j W on every
+ * dim + the fp32 gather-apply) and of the non-fused plan (one GEMM over the
+ * gathered rows), from the measured bf16 tensor rate (FLOP/s) and HBM
+ * bandwidth (B/s); *h_fused = t_fused < t_nonfused.  Calibrated on the
+ * 164-cell complexity sweep, checked on a disjoint hold-out grid
+ * (profiles/round2/planner_holdout.json).  No device needed. */
+int laq_plan_linear_device(int64_t target_rows, int64_t k, int64_t l, const int64_t* dim_rows, int32_t n_dims,
+                           double tensor_flops, double hbm_bytes_per_s, double* h_t_fused, double* h_t_nonfused,
+                           int32_t* h_fused);
 
 #ifdef __cplusplus
 }

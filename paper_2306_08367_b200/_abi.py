@@ -133,6 +133,7 @@ _SIGS = {
     "laq_speedup_ratio_linear": (C.c_int, [i64, i64, i64, i64p, i32, f64p]),
     "laq_speedup_ratio_tree": (C.c_int, [i64, i64, i64, i64, i64p, i32, f64p]),
     "laq_decide_fusion": (C.c_int, [C.c_double, C.c_double, i32p]),
+    "laq_plan_linear_device": (C.c_int, [i64, i64, i64, i64p, i32, C.c_double, C.c_double, f64p, f64p, i32p]),
 }
 
 EXPORTED = tuple(_SIGS)

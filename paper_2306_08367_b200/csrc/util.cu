@@ -1,6 +1,8 @@
 // Context lifecycle, cost model and small device utilities (min/max, scans).
 #include <cub/cub.cuh>
 
+#include <algorithm>
+
 #include <climits>
 #include <cmath>
 
@@ -200,6 +202,36 @@ int laq_speedup_ratio_tree(int64_t i, int64_t k, int64_t l, int64_t p, const int
   if (di * dl * sum_r == 0.0) return LAQ_ERR_DOMAIN;
   *out = dk / dl + dk * dk / (3.0 * di * dl) + dk * dk / (dl * sum_r) + dk / sum_r + dk / (dl * sum_r) +
          1.0 / sum_r;
+  return LAQ_OK;
+}
+
+int laq_plan_linear_device(int64_t target_rows, int64_t k, int64_t l, const int64_t* dim_rows, int32_t n_dims,
+                           double tensor_flops, double hbm_bytes_per_s, double* t_fused, double* t_nonfused,
+                           int32_t* fused) {
+  if (target_rows < 0 || k < 1 || l < 1 || n_dims < 1 || !dim_rows || tensor_flops <= 0 || hbm_bytes_per_s <= 0)
+    return LAQ_ERR_DOMAIN;
+  const double pt = tensor_flops * 0.85;   // tensor-pipe rate gemm_tc.cu reaches on long GEMMs
+  const double bw = hbm_bytes_per_s * 0.76;  // gather + streaming mix
+  const double ovh = 20e-6;                  // launch + pipeline fill per kernel
+  const double F = static_cast<double>(target_rows);
+  const double kp = static_cast<double>((k + 31) / 32 * 32);
+  const double lp = static_cast<double>(std::max<int64_t>(16, (l + 15) / 16 * 16));
+  const double dl = static_cast<double>(l), nd = static_cast<double>(n_dims);
+  double R = 0, t_pre = 0;
+  for (int32_t j = 0; j < n_dims; ++j) {
+    if (dim_rows[j] < 0) return LAQ_ERR_DOMAIN;
+    const double r = static_cast<double>(dim_rows[j]);
+    R += r;
+    t_pre += std::max(6.0 * r * kp * lp / pt, (r * kp * 4 + r * dl * 4) / bw);
+  }
+  // non-fused: one GEMM over the gathered rows (3 MMAs per product, fp16x2 split)
+  const double t_nf = ovh + std::max(6.0 * F * kp * lp / pt, (F * 4 * nd + F * kp * 4 + F * dl * 4) / bw);
+  // fused: P reads hit L2 while sum r_j l 4 B fits (~100 MB)
+  const double gather_p = R * dl * 4 <= 100e6 ? 0.0 : F * dl * 4 * nd;
+  const double t_f = (1 + nd) * ovh + t_pre + (F * 4 * nd + F * dl * 4 + gather_p) / bw;
+  if (t_fused) *t_fused = t_f;
+  if (t_nonfused) *t_nonfused = t_nf;
+  if (fused) *fused = t_f < t_nf ? 1 : 0;
   return LAQ_OK;
 }
 

@@ -269,3 +269,16 @@ def plan_linear_device(target_rows: int, k: int, l: int, dim_rows) -> str:
     predicted device time (device_plan_costs)."""
     t_f, t_nf = device_plan_costs(target_rows, k, l, dim_rows)
     return "fused" if t_f < t_nf else "nonfused"
+
+
+def device_plan_costs_abi(target_rows: int, k: int, l: int, dim_rows, peaks=None):
+    """The same model through the C-ABI (laq_plan_linear_device): what a C++
+    host calls.  Returns (t_fused, t_nonfused, fused)."""
+    from . import _abi
+    pt, bw = peaks or _device_peaks()
+    dims = (C.c_int64 * len(dim_rows))(*[int(r) for r in dim_rows])
+    tf, tn, fu = C.c_double(), C.c_double(), C.c_int32()
+    rc = _abi.lib().laq_plan_linear_device(int(target_rows), int(k), int(l), dims, len(dim_rows), pt, bw,
+                                           C.byref(tf), C.byref(tn), C.byref(fu))
+    errors.raise_for(rc, "plan_linear_device: non-positive inputs")
+    return tf.value, tn.value, bool(fu.value)

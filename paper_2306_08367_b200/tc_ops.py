@@ -134,3 +134,37 @@ def predict_nonfused_tc(i_maps, dims, placements, L, features: TCFeatures | None
         if features is None:
             f.close()
 
+
+
+def predict_star_linear(i_maps, dims, placements, L, planner: str = "device", threshold: float = 1.0,
+                        features: TCFeatures | None = None, plan: str | None = None):
+    """The planner-driven linear predict over a star join on the tensor cores:
+    the plan (fused: prefuse P_j = B_j (M_j L) + gather-apply; non-fused: one
+    GEMM over the gathered rows) is CHOSEN by a cost model, as the paper
+    prescribes (fusion.cpp:199-224 decide_fusion; cli.cpp:648-652 leaves the
+    choice to the user):
+
+      planner="device": laq_plan_linear_device (the B200 roofline model);
+      planner="paper":  speedup_ratio_linear (Eq. 2) + decide_fusion(threshold);
+      plan="fused"|"nonfused" forces one.
+
+    Returns (Y [rows x l] fp32 device tensor, the plan taken)."""
+    from . import fusion
+    Ld = dev(L, f64)
+    k, l = int(Ld.shape[0]), int(Ld.shape[1])
+    rows = int(len(i_maps[0])) if len(i_maps) else 0
+    dim_rows = [int(d.shape[0]) for d in dims]
+    if plan is None:
+        if planner == "device":
+            fused = fusion.device_plan_costs_abi(rows, k, l, dim_rows)[2]
+        elif planner == "paper":
+            r = fusion.speedup_ratio_linear(fusion.CostInputs(rows, k, l, k, dim_rows))
+            fused = fusion.decide_fusion(r, threshold)
+        else:
+            raise errors.ShapeError(f"unknown planner {planner!r}")
+        plan = "fused" if fused else "nonfused"
+    if plan == "fused":
+        return apply_fused_linear_tc(i_maps, prefuse_linear_tc(dims, placements, Ld)), plan
+    if plan == "nonfused":
+        return predict_nonfused_tc(i_maps, dims, placements, Ld, features), plan
+    raise errors.ShapeError(f"unknown plan {plan!r}")

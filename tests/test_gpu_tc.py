@@ -68,3 +68,29 @@ def test_gemm_errors(tco):
     with pytest.raises(errors.ShapeError):
         f.gemm(rng.random((3, 5)))
     assert f.gemm(rng.random((2, 5)), row_maps=[np.zeros(0, np.int32)]).shape == (0, 5)
+
+
+@pytest.mark.parametrize("rows,k,l,n", [(300, 16, 1, 50_000), (40_000, 64, 256, 3_000), (2_000, 32, 8, 20_000)])
+def test_planner_driven_predict(tco, rows, k, l, n):
+    """tc_ops.predict_star_linear: the cost model picks the plan (device model
+    via the C-ABI, or the paper's Eq. 2 + decide_fusion); whichever it picks,
+    the answer equals the fp64 oracle condition-aware."""
+    from paper_2306_08367_b200 import fusion
+    tc, _ = tco
+    rng = np.random.default_rng(rows + k + l)
+    dims = [rng.random((rows, k // 2)), rng.random((rows // 2 + 1, k - k // 2))]
+    pl = [np.arange(k // 2), np.arange(k // 2, k)]
+    L = rng.uniform(-1, 1, (k, l))
+    idx = [rng.integers(0, d.shape[0], n) for d in dims]
+    T = O.materialize(idx, dims, pl, k)
+    ref, bound = T @ L, np.abs(T) @ np.abs(L)
+    want_dev = fusion.plan_linear_device(n, k, l, [d.shape[0] for d in dims])
+    want_paper = fusion.plan_linear(n, k, l, [d.shape[0] for d in dims])
+    for planner, want in (("device", want_dev), ("paper", want_paper)):
+        y, plan = tc.predict_star_linear(idx, dims, pl, L, planner=planner)
+        assert plan == want
+        _check(y.cpu().numpy(), ref, bound)
+    for forced in ("fused", "nonfused"):
+        y, plan = tc.predict_star_linear(idx, dims, pl, L, plan=forced)
+        assert plan == forced
+        _check(y.cpu().numpy(), ref, bound)

@@ -36,3 +36,18 @@ def test_device_planner_tracks_measurements():
     assert dev > paper
     for c in cells:  # the sweep's accuracy record: condition-aware 1e-5
         assert c["cond_err_fused"] <= 1e-5 and c["cond_err_nonfused"] <= 1e-5
+
+
+def test_device_plan_model_c_abi_equals_python():
+    """laq_plan_linear_device (the C-ABI a C++ host calls) == fusion.device_plan_costs
+    on the sweep and hold-out grids; no device needed."""
+    from paper_2306_08367_b200 import fusion
+    peaks = (1628e12, 6548e9)
+    for r in (1_000, 3_000, 100_000, 3_000_000, 10_000_000):
+        for k in (8, 16, 64, 256, 1024):
+            for l in (1, 2, 32, 512, 4096):
+                for dims in ([r], [r, r // 3 + 1]):
+                    tf, tn = fusion.device_plan_costs(1_000_000, k, l, dims, peaks)
+                    cf, cn, fused = fusion.device_plan_costs_abi(1_000_000, k, l, dims, peaks)
+                    assert abs(cf - tf) <= 1e-12 * tf and abs(cn - tn) <= 1e-12 * tn
+                    assert fused == (tf < tn)
