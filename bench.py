@@ -460,7 +460,8 @@ def main():
                     "draws the canonical lineorder stream and keeps its contiguous row shard",
             "config": W.config(),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "traffic_source": traffic_src,
+                         "traffic": None if traffic is None else float(sum(traffic) / len(traffic)),
+                         "traffic_per_launch": traffic, "traffic_source": traffic_src,
                          "kernel": "scan_batch_kernel (K4 batched: one pass per query group, csrc/ssb_batch.cu)",
                          "algorithmic_bytes_per_launch": [int(b) for b in bytes_per_launch],
                          "unit_bytes": "the union of the group's touched fact columns x 4 B per row, read once per group (Q3.x: "
@@ -591,11 +592,14 @@ def _fact_cols(q):
 
 
 def ncu_traffic(workload):
-    """DRAM bytes (read + write) per scan launch from the committed ncu --set
-    full capture of this workload's scan launches (profiles/<round>/)."""
+    """DRAM bytes (read + write) per batched-pass launch from the committed ncu
+    --set full capture of this workload's passes (profiles/<round>/
+    batch_scan_ncu.json; one entry per query group).  Returns (per-launch
+    list, source) or (None, None) when no capture of this workload exists."""
     import glob
-    pat = "scan_sf100_full_metrics.json" if workload == "q3q4" else "shared_full_metrics.json"
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", pat)))
+    if workload != "q3q4":
+        return None, None
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "batch_scan_ncu.json")))
     if not files:
         return None, None
     rows = json.load(open(files[-1]))
@@ -607,7 +611,7 @@ def ncu_traffic(workload):
             v, u = r[k].split()
             b += float(v) * unit[u]
         tot.append(b)
-    return sum(tot) / len(tot), os.path.relpath(files[-1], ROOT)
+    return tot, os.path.relpath(files[-1], ROOT)
 
 
 def fused_predict_bench(ctx):
