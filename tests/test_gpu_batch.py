@@ -206,3 +206,35 @@ def test_layout_variants_match_oracle(gpu_ctx, monkeypatch, env):
         b, got = _run_batch(dsr, qs)
         for q, m in zip(qs, got):
             assert np.array_equal(m, O.run_query(tables, q)), (env, trial, q, b.fused, b.why)
+
+
+def test_wide_dictionaries_and_fallbacks(gpu_ctx):
+    """uint16 tuple ids (> 256 distinct tuples on a link), a group space above
+    4096 (plan-by-plan fallback) and more than 65,535 distinct tuples on a link
+    (dictionary overflow -> fallback): every case equals the oracle."""
+    from paper_2306_08367_b200 import query as Q, star
+    rng = np.random.default_rng(11)
+    n, r = 300_000, 120_000
+    dim = {"pk": np.arange(r, dtype=np.int64), "a": rng.integers(0, 41, r).astype(np.int64),
+           "b": rng.integers(0, 41, r).astype(np.int64), "c": rng.integers(0, 41, r).astype(np.int64),
+           "w": rng.integers(0, 1000, r).astype(np.int64), "big": rng.integers(0, 5000, r).astype(np.int64)}
+    fact = {"fk": rng.integers(0, r, n).astype(np.int64), "m": rng.integers(1, 100, n).astype(np.int64)}
+    tables = {"lineorder": fact, "d": dim}
+    kinds = {"lineorder": {"fk": 0, "m": 1}, "d": {k: (0 if k == "pk" else 1) for k in dim}}
+    ds = star.DeviceStar.from_tables(tables, kinds, [("fk", "d", "pk")])
+    j = [Q.StarLink("fk", "d", "pk")]
+
+    def q(i, group, flt=None):
+        return Q.QuerySpec(id=f"w{i}", group=0, joins=j, filters=[] if flt is None else [flt], measure="m",
+                           group_by=[Q.GroupRef(0, g) for g in group], order_by=True)
+
+    cases = {
+        "u16 ids": ([q(0, ["w"]), q(1, ["a"], Q.FilterSpec(0, "b", Q.Pred.lt(20)))], True),
+        "G > 4096": ([q(2, ["big"]), q(3, ["a"])], False),
+        "> 65535 tuples": ([q(4, ["a"]), q(5, ["b"]), q(6, ["c"])], False),
+    }
+    for name, (qs, fused) in cases.items():
+        b, got = _run_batch(ds, qs)
+        assert b.fused == fused, (name, b.why)
+        for qq, m in zip(qs, got):
+            assert np.array_equal(m, O.run_query(tables, qq)), (name, qq.id)
