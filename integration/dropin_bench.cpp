@@ -12,6 +12,14 @@
 // W.bin (f64 k x l) and meta.txt ("n r k l"); y.bin (f64 n x l) is written
 // back for the caller's bit-exactness check.  Prints one JSON line of median
 // per-stage seconds over `reps` timed repetitions (after 2 warm-ups).
+//
+//   dropin_bench --query <sf> <dial21> <dial31> [reps]
+// SSB-style queries through cli::run_query_laq (cli.cpp:73-138) on the
+// reference generator's data (bench::gen_star, Setting::Ssb, seed 42): Q2.1 and
+// Q3.1 with the given dials (the query defs of benchgen.cpp:259-289).  Times
+// the first call (H2D of the query's columns into the drop-in's device cache +
+// the device run) and the cached calls after it, and checks every result
+// against the reference's own run_query_oracle (cli.cpp:140-225) at tolerance 0.
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
@@ -19,10 +27,14 @@
 #include <string>
 #include <vector>
 
+#include "laq/benchgen.hpp"
+#include "laq/cli.hpp"
 #include "laq/fusion.hpp"
 #include "laq/laqops.hpp"
 #include "laq/matrix.hpp"
 #include "laq/mlops.hpp"
+#include "laq/predicate.hpp"
+#include "laq/report.hpp"
 #include "laq/storage.hpp"
 
 using namespace laq;
@@ -45,7 +57,64 @@ static double median(std::vector<double> v) {
   return v[v.size() / 2];
 }
 
+static int query_mode(int argc, char** argv) {
+  if (argc < 5) return 2;
+  bench::GenConfig cfg;
+  cfg.setting = bench::Setting::Ssb;
+  cfg.sf = std::atoi(argv[2]);
+  cfg.seed = 42;
+  cfg.max_bytes = std::int64_t{64} << 30;
+  const int reps = argc > 5 ? std::atoi(argv[5]) : 5;
+  double t0 = now_s();
+  const StarSchema s = bench::gen_star(cfg);
+  const double gen_s = now_s() - t0;
+  const StarLink part{"lo_part", "part", "p_key"}, supp{"lo_supplier", "supplier", "s_key"},
+      date{"lo_orderdate", "date", "d_key"};
+  bench::QuerySpec q21;  // benchgen.cpp:259-266
+  q21.id = "21";
+  q21.group = bench::QueryGroup::G2;
+  q21.joins = {part, supp, date};
+  q21.filters = {{1, "s_region", Predicate::eq(std::int64_t{0})}, {0, "p_size", Predicate::lt(static_cast<std::int64_t>(std::atoll(argv[3])))}};
+  q21.measure = "lo_revenue";
+  q21.group_by = {{2, "d_year"}, {0, "p_brand"}};
+  q21.order_by = true;
+  bench::QuerySpec q31;  // benchgen.cpp:283-289
+  q31.id = "31";
+  q31.group = bench::QueryGroup::G3;
+  q31.joins = {part, supp, date};
+  q31.filters = {{2, "d_year", Predicate::between(std::int64_t{1992}, std::int64_t{1997})},
+                 {1, "s_rank", Predicate::lt(static_cast<std::int64_t>(std::atoll(argv[4])))}};
+  q31.measure = "lo_revenue";
+  q31.group_by = {{1, "s_nation"}, {2, "d_year"}};
+  q31.order_by = true;
+  std::printf("{\"sf\": %d, \"fact_rows\": %lld, \"gen_s\": %.3f", cfg.sf,
+              static_cast<long long>(s.fact().row_count()), gen_s);
+  for (const auto* q : {&q21, &q31}) {
+    t0 = now_s();
+    const DenseMat first = cli::run_query_laq(s, *q);
+    const double cold = now_s() - t0;
+    std::vector<double> warm;
+    DenseMat last;
+    for (int i = 0; i < reps; ++i) {
+      t0 = now_s();
+      last = cli::run_query_laq(s, *q);
+      warm.push_back(now_s() - t0);
+    }
+    t0 = now_s();
+    const DenseMat want = cli::run_query_oracle(s, *q);
+    const double oracle_s = now_s() - t0;
+    const bool ok = cli::compare_matrices(first, want, 0.0).ok && cli::compare_matrices(last, want, 0.0).ok;
+    std::printf(", \"Q%s\": {\"rows\": %lld, \"first_call_s\": %.6g, \"cached_call_s\": %.6g, "
+                "\"reference_oracle_s\": %.6g, \"equal_to_reference_oracle\": %s}",
+                q->id.c_str(), static_cast<long long>(first.rows()), cold, median(warm), oracle_s,
+                ok ? "true" : "false");
+  }
+  std::printf("}\n");
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc >= 2 && std::string(argv[1]) == "--query") return query_mode(argc, argv);
   if (argc < 2) {
     std::fprintf(stderr, "usage: dropin_bench <dir> [reps]\n");
     return 2;
