@@ -291,10 +291,47 @@ struct CachedStar {
   std::vector<ColRef> key;
   laq_star* star = nullptr;
   int status = LAQ_OK;  // != OK: this column set needs the general path
+  // Prepared plans of the queries run over this star (a prepared-statement
+  // cache): keyed by the query's full description, so a repeated query skips
+  // plan construction (probe / code-table allocation, pass-fraction counts).
+  struct Prepared {
+    laq_plan* plan = nullptr;
+    int64_t groups = 0;
+  };
+  std::map<std::string, Prepared> plans;
   ~CachedStar() {
+    for (auto& [k, p] : plans) laq_plan_destroy(p.plan);
     if (star) laq_star_destroy(star);
   }
 };
+
+// Canonical text of a query description (the plan cache key).
+std::string query_key(const laq_query_desc& d) {
+  std::string k;
+  auto add = [&](const std::string& x) {
+    k += std::to_string(x.size());
+    k += ':';
+    k += x;
+  };
+  for (int32_t j = 0; j < d.n_joins; ++j) {
+    add(d.joins[j].fact_fk);
+    add(d.joins[j].dim_name);
+    add(d.joins[j].dim_pk);
+  }
+  k += '|';
+  for (int32_t i = 0; i < d.n_filters; ++i) {
+    const laq_filter_desc& f = d.filters[i];
+    add(std::to_string(f.target) + "," + f.column + "," + std::to_string(f.kind) + "," + std::to_string(f.is_float) +
+        "," + std::to_string(f.lo) + "," + std::to_string(f.hi));
+    for (int64_t t = 0; t < f.set_len; ++t) add(std::to_string(f.set[t]));
+    k += ';';
+  }
+  k += '|';
+  add(d.measure ? d.measure : "");
+  for (int32_t g = 0; g < d.n_group; ++g) add(std::to_string(d.group_by[g].target) + "," + d.group_by[g].column);
+  k += d.order_by ? "o" : "-";
+  return k;
+}
 
 std::mutex g_cache_mu;
 std::list<std::unique_ptr<CachedStar>> g_cache;  // most recent first
@@ -431,12 +468,28 @@ bool fast_query(const StarSchema& data, const bench::QuerySpec& q, DenseMat* res
   laq_query_desc desc{static_cast<int32_t>(links.size()), links.data(), static_cast<int32_t>(filters.size()),
                       filters.data(),   q.measure.c_str(), static_cast<int32_t>(groups.size()),
                       groups.data(),    q.order_by ? 1 : 0};
+  // The prepared plan of this query over this star (built on first use).
+  CachedStar::Prepared* prep = nullptr;
+  const std::string qkey = query_key(desc);
+  auto hit = entry->plans.find(qkey);
+  if (hit != entry->plans.end()) {
+    prep = &hit->second;
+  } else {
+    CachedStar::Prepared np;
+    if (laq_query_prepare(ctx(), star, &desc, &np.plan, &np.groups) != LAQ_OK) return false;
+    prep = &entry->plans.emplace(qkey, np).first->second;
+  }
+  const int64_t G = prep->groups;
+  Dev<int64_t> acc(static_cast<size_t>(2 * G));
+  if (laq_plan_execute(ctx(), prep->plan, acc.p, 0) != LAQ_OK) return false;
+  if (laq_allreduce_acc(ctx(), acc.p, 2 * G) != LAQ_OK) return false;  // row-sharded schemas
+  const std::vector<int64_t> h = acc.to_vector(static_cast<size_t>(2 * G));
   std::vector<double> buf(1 << 16);
   int64_t rows = 0, ncols = 0;
-  int rc = laq_run_query(ctx(), star, &desc, buf.data(), static_cast<int64_t>(buf.size()), &rows, &ncols);
+  int rc = laq_plan_emit(prep->plan, h.data(), buf.data(), static_cast<int64_t>(buf.size()), &rows, &ncols);
   if (rc == LAQ_ERR_CAPACITY && rows * ncols > static_cast<int64_t>(buf.size())) {
     buf.resize(static_cast<size_t>(rows * ncols));
-    rc = laq_run_query(ctx(), star, &desc, buf.data(), static_cast<int64_t>(buf.size()), &rows, &ncols);
+    rc = laq_plan_emit(prep->plan, h.data(), buf.data(), static_cast<int64_t>(buf.size()), &rows, &ncols);
   }
   if (rc != LAQ_OK) return false;
   buf.resize(static_cast<size_t>(rows * ncols));
