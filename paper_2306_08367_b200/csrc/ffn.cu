@@ -87,23 +87,23 @@ struct Smem {  // offsets into the 1024-aligned dynamic buffer
   uint32_t b, a, w2, bars, stage_bytes;
 };
 
-__host__ __device__ inline Smem layout(int nb, int N, int lp, int S) {
+// cg = 2 (CTA pair): each CTA holds N/2 rows of every W1 block (its half of B).
+__host__ __device__ inline Smem layout(int nb, int N, int lp, int S, int cg = 1) {
   Smem m;
   m.b = 0;
-  m.a = static_cast<uint32_t>(nb) * N * 128u;
+  m.a = static_cast<uint32_t>(nb) * (N / cg) * 128u;
   m.stage_bytes = static_cast<uint32_t>(nb) * kBlockBytes;
   m.w2 = m.a + S * m.stage_bytes;
   m.bars = (m.w2 + N * lp * 4u + 15u) & ~15u;
   return m;
 }
-__host__ __device__ inline uint32_t smem_bytes(int nb, int N, int lp, int S) {
+__host__ __device__ inline uint32_t smem_bytes(int nb, int N, int lp, int S, int cg = 1) {
   // barriers: full[S], empty[S], acc_full[2], acc_empty[2] + tmem slot; +1 KB alignment slack
-  return layout(nb, N, lp, S).bars + (2 * S + 4) * 8 + 16 + 1024;
+  return layout(nb, N, lp, S, cg).bars + (2 * S + 4) * 8 + 16 + 1024;
 }
 
-// Key (or row-map entry) of row `r` of `tile` for every dim, clamped to n-1.
-__device__ __forceinline__ void load_keys(const Args& a, int64_t tile, int r, int32_t (&k)[kMaxDims]) {
-  int64_t g = tile * kRows + r;
+// Key (or row-map entry) of fact row `g` for every dim, clamped to n-1.
+__device__ __forceinline__ void load_keys(const Args& a, int64_t g, int32_t (&k)[kMaxDims]) {
   if (g >= a.n) g = a.n - 1;
 #pragma unroll
   for (int j = 0; j < kMaxDims; ++j)
@@ -115,12 +115,23 @@ __device__ __forceinline__ void resolve(const Args& a, const int32_t (&k)[kMaxDi
     if (j < a.n_dims) r[j] = a.probe_mode ? a.probe[j].row(k[j]) : k[j];
 }
 
-template <int LP>
+// CG = 1: one CTA per SM, M = 128 UMMAs.  CG = 2: a CTA pair (cluster of 2)
+// runs M = 256 UMMAs (cta_group::2) over 256-row tiles: each CTA gathers its
+// 128 rows and holds half of W1, so every SM's shared memory serves half of
+// the B operand reads; only the leader issues MMAs; the peer's producers
+// report through a relay arrive on the leader's stage barrier, its epilogue
+// warps release the accumulator on the leader's barrier.
+template <int LP, int CG>
 __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant__ Args a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int S = a.stages, NB = a.n_blocks, N = a.N, l = a.l;
-  const Smem L = layout(NB, N, LP, S);
+  const Smem L = layout(NB, N, LP, S, CG);
+  const uint32_t rank = CG == 2 ? tc::cluster_rank() : 0u;
+  const bool leader = rank == 0;
+  const int64_t tile0 = CG == 2 ? blockIdx.x / 2 : blockIdx.x;   // tiles of kRows * CG rows
+  const int64_t tstep = CG == 2 ? gridDim.x / 2 : gridDim.x;
+  const int64_t row_off = static_cast<int64_t>(rank) * kRows;    // this CTA's rows within a tile
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
   uint64_t* empty = full + S;
   uint64_t* acc_full = empty + S;
@@ -132,30 +143,36 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant_
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // ---- one-time setup: W1 blocks -> SW128 K-major rows; W2 -> smem ----------------
-  for (int e = threadIdx.x; e < NB * N * 8; e += kThreads) {
-    const int c = e & 7, row = e >> 3;  // row = b * N + n
-    const uint4 v = *reinterpret_cast<const uint4*>(a.w1 + static_cast<int64_t>(row) * 64 + c * 8);
-    *reinterpret_cast<uint4*>(smem + L.b + tc::sw128_off(row, c)) = v;  // N is a multiple of 8
+  const int NH = N / CG;  // W1 rows (hidden units) this CTA holds per block
+  for (int e = threadIdx.x; e < NB * NH * 8; e += kThreads) {
+    const int c = e & 7, row = e >> 3;  // row = b * NH + n_local
+    const int b = row / NH, nl = row - b * NH;
+    const int64_t src = static_cast<int64_t>(b) * N + static_cast<int64_t>(rank) * NH + nl;
+    const uint4 v = *reinterpret_cast<const uint4*>(a.w1 + src * 64 + c * 8);
+    *reinterpret_cast<uint4*>(smem + L.b + tc::sw128_off(row, c)) = v;  // NH is a multiple of 8
   }
   for (int e = threadIdx.x; e < N * LP; e += kThreads) s_w2[e] = a.w2[e] * a.unscale;  // exact (power of two)
   if (warp == kMmaWarp) {
     if (lane == 0) {
       for (int s = 0; s < S; ++s) {
-        tc::mbar_init(&full[s], kProdWarps * 32);
+        // the leader's stage barrier also counts the peer's relay arrive
+        tc::mbar_init(&full[s], kProdWarps * 32 + (CG == 2 && leader ? 1 : 0));
         tc::mbar_init(&empty[s], 1);
       }
       for (int b = 0; b < 2; ++b) {
         tc::mbar_init(&acc_full[b], 1);
-        tc::mbar_init(&acc_empty[b], kEpiWarps);
+        tc::mbar_init(&acc_empty[b], kEpiWarps * CG);  // the leader's counts both CTAs' epilogues
       }
       tc::fence_mbar_init();
     }
     __syncwarp();
-    tc::tmem_alloc<512>(tmem_slot);
+    if constexpr (CG == 2) tc::tmem_alloc2<512>(tmem_slot);
+    else tc::tmem_alloc<512>(tmem_slot);
   }
   tc::fence_proxy_async();  // W1 st.shared -> async proxy
   tc::tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) tc::cluster_sync();  // both CTAs' barriers exist before any remote arrive
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -164,17 +181,19 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant_
     const int pw = warp - kProdWarp0;  // tile rows 32*pw .. 32*pw+31
     __shared__ int32_t s_rows[kProdWarps][kMaxDims][32];
     int32_t k1[kMaxDims] = {}, k2[kMaxDims] = {}, r1[kMaxDims] = {};
-    int64_t tile = blockIdx.x;
-    const int64_t step = gridDim.x;
+    int64_t tile = tile0;
+    const int64_t step = tstep;
+    const int64_t TR = static_cast<int64_t>(kRows) * CG;  // rows per tile
+    const int64_t my = row_off + 32 * pw + lane;          // this lane's row within a tile
     unsigned long long misses = 0;
     // prologue: keys of the first two tiles, rows of the first
-    if (tile < a.n_tiles) load_keys(a, tile, 32 * pw + lane, k1);
-    if (tile + step < a.n_tiles) load_keys(a, tile + step, 32 * pw + lane, k2);
+    if (tile < a.n_tiles) load_keys(a, tile * TR + my, k1);
+    if (tile + step < a.n_tiles) load_keys(a, (tile + step) * TR + my, k2);
     resolve(a, k1, r1);
     const int sub = lane >> 3, chunk = lane & 7;  // 4 rows x 8 16-byte chunks per instruction
     for (int it = 0; tile < a.n_tiles; tile += step, ++it) {
       const int s = it % S;
-      const bool live = tile * kRows + 32 * pw + lane < a.n;
+      const bool live = tile * TR + my < a.n;
 #pragma unroll
       for (int j = 0; j < kMaxDims; ++j)
         if (j < a.n_dims) {
@@ -187,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant_
         }
       // look ahead: rows of the next tile (keys loaded an iteration ago), keys two ahead
       resolve(a, k2, r1);
-      if (tile + 2 * step < a.n_tiles) load_keys(a, tile + 2 * step, 32 * pw + lane, k2);
+      if (tile + 2 * step < a.n_tiles) load_keys(a, (tile + 2 * step) * TR + my, k2);
       __syncwarp();
 
       tc::mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
@@ -212,12 +231,26 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant_
       for (int o = 16; o; o >>= 1) misses += __shfl_xor_sync(0xffffffffu, misses, o);
       if (lane == 0 && misses) atomicAdd(a.miss, misses);
     }
+  } else if (warp == kMmaWarp && CG == 2 && !leader) {
+    // ================= peer relay (CTA pair) =================
+    // When this CTA's producers have filled stage s, tell the leader (its MMA
+    // reads this CTA's half of A and B from this shared memory).
+    if (lane == 0) {
+      int it = 0;
+      for (int64_t tile = tile0; tile < a.n_tiles; tile += tstep, ++it) {
+        const int s = it % S;
+        tc::mbar_wait(&full[s], (it / S) & 1);
+        tc::fence_proxy_async();  // cp.async (generic proxy) writes -> the leader's tensor-core reads
+        tc::mbar_arrive_cluster(tc::mapa(&full[s], 0));
+      }
+    }
+    __syncwarp();
   } else if (warp == kMmaWarp) {
     // ================= MMA issuer =================
     if (lane == 0) {
-      const uint32_t idesc = tc::idesc_f16_f32(kRows, N);
+      const uint32_t idesc = tc::idesc_f16_f32(kRows * CG, N);
       int it = 0;
-      for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x, ++it) {
+      for (int64_t tile = tile0; tile < a.n_tiles; tile += tstep, ++it) {
         const int s = it % S, ab = it & 1;
         tc::mbar_wait(&acc_empty[ab], ((it >> 1) & 1) ^ 1);
         tc::mbar_wait(&full[s], (it / S) & 1);
@@ -232,13 +265,19 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant_
           for (int b = 0; b < NB; ++b)
             for (int st = 0; st < a.block_steps[b]; ++st) {
               const uint64_t ad = tc::sdesc_sw128(abase + b * kBlockBytes + pa + st * 32u);
-              const uint64_t bd = tc::sdesc_sw128(sbase + L.b + b * (N * 128u) + pb + st * 32u);
-              tc::mma_f16(d, ad, bd, idesc, acc);
+              const uint64_t bd = tc::sdesc_sw128(sbase + L.b + b * ((N / CG) * 128u) + pb + st * 32u);
+              if constexpr (CG == 2) tc::mma_f16_pair(d, ad, bd, idesc, acc);
+              else tc::mma_f16(d, ad, bd, idesc, acc);
               acc = 1;
             }
         }
-        tc::mma_commit(&empty[s]);
-        tc::mma_commit(&acc_full[ab]);
+        if constexpr (CG == 2) {
+          tc::mma_commit_pair(&empty[s]);
+          tc::mma_commit_pair(&acc_full[ab]);
+        } else {
+          tc::mma_commit(&empty[s]);
+          tc::mma_commit(&acc_full[ab]);
+        }
       }
     }
     __syncwarp();
@@ -248,7 +287,9 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant_
     const int q = warp & 3, hh = warp >> 2;  // TMEM lane group, column half
     const uint32_t w2a = tc::smem_u32(s_w2);
     int it = 0;
-    for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x, ++it) {
+    // the accumulator is released on the leader's barrier (a cluster address for the peer)
+    const uint32_t rel[2] = {CG == 2 ? tc::mapa(&acc_empty[0], 0) : 0u, CG == 2 ? tc::mapa(&acc_empty[1], 0) : 0u};
+    for (int64_t tile = tile0; tile < a.n_tiles; tile += tstep, ++it) {
       const int ab = it & 1;
       tc::mbar_wait(&acc_full[ab], (it >> 1) & 1);
       tc::tc_fence_after();
@@ -274,7 +315,10 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant_
           // before the arithmetic, so the MMA warp can start the tile after next
           tc::tc_fence_before();
           __syncwarp();
-          if (lane == 0) tc::mbar_arrive(&acc_empty[ab]);
+          if (lane == 0) {
+            if constexpr (CG == 2) tc::mbar_arrive_cluster(rel[ab]);
+            else tc::mbar_arrive(&acc_empty[ab]);
+          }
           released = true;
         }
         if (a.diag == 4) {
@@ -312,7 +356,10 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant_
       if (!released) {
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&acc_empty[ab]);
+        if (lane == 0) {
+          if constexpr (CG == 2) tc::mbar_arrive_cluster(rel[ab]);
+          else tc::mbar_arrive(&acc_empty[ab]);
+        }
       }
       float yy[LP];
       if constexpr (LP == 1) {
@@ -330,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant_
       }
       asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");  // the two warps of lane group q
       if (hh == 0) {
-        const int64_t row = tile * kRows + 32 * q + lane;
+        const int64_t row = tile * (static_cast<int64_t>(kRows) * CG) + row_off + 32 * q + lane;
         if (row < a.n) {
 #pragma unroll
           for (int c = 0; c < LP; ++c)
@@ -341,9 +388,11 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant_
   }
   tc::tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) tc::cluster_sync();  // the pair is done with TMEM and each other's barriers
   if (warp == kMmaWarp) {
     tc::tc_fence_after();
-    tc::tmem_dealloc<512>(tmem);
+    if constexpr (CG == 2) tc::tmem_dealloc2<512>(tmem);
+    else tc::tmem_dealloc<512>(tmem);
   }
 }
 
@@ -406,20 +455,43 @@ ffn::Args make_args(const laq_ffn* f, int64_t n, float* y) {
 }
 
 template <int LP>
-void launch_lp(laq_ctx* ctx, const ffn::Args& a, unsigned grid, uint32_t bytes) {
-  LAQ_CUDA(cudaFuncSetAttribute(ffn::ffn_kernel<LP>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  ffn::ffn_kernel<LP><<<grid, ffn::kThreads, bytes, ctx->stream>>>(a);
+void launch_lp(laq_ctx* ctx, const ffn::Args& a, unsigned grid, uint32_t bytes, int cg) {
+  if (cg == 2) {  // CTA pairs: clusters of 2 on neighbouring SMs
+    auto kern = ffn::ffn_kernel<LP, 2>;
+    LAQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(ffn::kThreads);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    LAQ_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+    return;
+  }
+  LAQ_CUDA(cudaFuncSetAttribute(ffn::ffn_kernel<LP, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  ffn::ffn_kernel<LP, 1><<<grid, ffn::kThreads, bytes, ctx->stream>>>(a);
 }
 
-void launch_ffn(laq_ctx* ctx, const laq_ffn* f, const ffn::Args& a) {
-  if (a.n_tiles == 0) return;
-  const uint32_t bytes = ffn::smem_bytes(f->n_blocks, f->N, f->lp, f->stages);
-  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(a.n_tiles, ctx->sm_count));
+void launch_ffn(laq_ctx* ctx, const laq_ffn* f, const ffn::Args& a0) {
+  if (a0.n_tiles == 0) return;
+  // LAQ_FFN_2CTA=1: M = 256 UMMAs on CTA pairs (cta_group::2) over 256-row tiles.
+  const char* e = std::getenv("LAQ_FFN_2CTA");
+  const int cg = e && std::string(e) == "1" ? 2 : 1;
+  ffn::Args a = a0;
+  a.n_tiles = (a.n + int64_t{ffn::kRows} * cg - 1) / (int64_t{ffn::kRows} * cg);
+  const uint32_t bytes = ffn::smem_bytes(f->n_blocks, f->N, f->lp, f->stages, cg);
+  const unsigned grid = static_cast<unsigned>(cg * std::min<int64_t>(a.n_tiles, ctx->sm_count / cg));
   switch (f->lp) {
-    case 1: launch_lp<1>(ctx, a, grid, bytes); break;
-    case 2: launch_lp<2>(ctx, a, grid, bytes); break;
-    case 4: launch_lp<4>(ctx, a, grid, bytes); break;
-    default: launch_lp<8>(ctx, a, grid, bytes); break;
+    case 1: launch_lp<1>(ctx, a, grid, bytes, cg); break;
+    case 2: launch_lp<2>(ctx, a, grid, bytes, cg); break;
+    case 4: launch_lp<4>(ctx, a, grid, bytes, cg); break;
+    default: launch_lp<8>(ctx, a, grid, bytes, cg); break;
   }
   launched(ctx);
 }
