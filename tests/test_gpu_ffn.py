@@ -121,3 +121,12 @@ def test_ffn_cfg3_ssb_sample(mods):
     ws, wrows = O.multiway_star_join([f[:n] for f in fks], pks)
     ref, bound = O.ffn_predict(wrows, dims, pl, 64, W1, W2)
     _check(y.cpu().numpy(), ref, bound)
+
+
+@pytest.mark.parametrize("widths,h,l,n", [((32, 32), 256, 1, 5000), ((16, 40), 128, 3, 777)])
+def test_ffn_cta_pair_variant_matches_oracle(mods, monkeypatch, widths, h, l, n):
+    """LAQ_FFN_2CTA=1: M = 256 UMMAs on CTA pairs (cta_group::2, W1 split by
+    hidden units across the pair, the peer's stages relayed to the leader) give
+    the same condition-aware answer, including a ragged last 256-row tile."""
+    monkeypatch.setenv("LAQ_FFN_2CTA", "1")
+    test_ffn_rows_matches_oracle(mods, widths, h, l, n)
