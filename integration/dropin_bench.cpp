@@ -113,8 +113,59 @@ static int query_mode(int argc, char** argv) {
   return 0;
 }
 
+// dropin_bench --pipeline <sf> [reps]: the reference's PipelineRunner (cli.cpp:246-378)
+// on its acceptance dataset shape (S2, seed 9001, 64 features, linear model with
+// 4 outputs): one-time prepare_joins + prefuse, then run_fused / run_nonfused
+// repetitions; every result's checksum must equal run_oracle's.
+static int pipeline_mode(int argc, char** argv) {
+  if (argc < 3) return 2;
+  bench::GenConfig cfg;
+  cfg.setting = bench::Setting::S2;
+  cfg.sf = std::atoi(argv[2]);
+  cfg.seed = 9001;
+  cfg.feature_width = 64;
+  const int reps = argc > 3 ? std::atoi(argv[3]) : 5;
+  const StarSchema s = bench::gen_star(cfg);
+  const bench::FeatureLayout lay = bench::feature_layout(s);
+  const ml::LinearOperator op = bench::gen_linear(lay.total, 4, 3);
+  cli::PipelineRunner runner(s, nullptr, &op);
+  cli::StageTimes st;
+  double t0 = now_s();
+  runner.prepare_joins(st);
+  const double join_s = now_s() - t0;
+  t0 = now_s();
+  runner.prefuse(st);
+  const double prefuse_s = now_s() - t0;
+  std::vector<double> tf, tn;
+  uint64_t cf = 0, cn = 0;
+  for (int i = 0; i < reps + 1; ++i) {
+    t0 = now_s();
+    const cli::PipelineResult f = runner.run_fused(st);
+    const double a = now_s() - t0;
+    t0 = now_s();
+    const cli::PipelineResult n = runner.run_nonfused(st);
+    const double b = now_s() - t0;
+    cf = f.checksum();
+    cn = n.checksum();
+    if (i > 0) tf.push_back(a), tn.push_back(b);
+  }
+  t0 = now_s();
+  const uint64_t co = runner.run_oracle(st).checksum();
+  const double oracle_s = now_s() - t0;
+  std::printf("{\"sf\": %d, \"target_rows\": %lld, \"k\": %lld, \"l\": 4, \"prepare_joins_s\": %.6g, "
+              "\"prefuse_s\": %.6g, \"run_fused_s\": %.6g, \"run_nonfused_s\": %.6g, \"run_oracle_s\": %.6g, "
+              "\"checksum_fused\": \"%llu\", \"checksum_nonfused\": \"%llu\", \"checksum_oracle\": \"%llu\", "
+              "\"fused_equals_oracle\": %s, \"nonfused_equals_oracle\": %s}\n",
+              cfg.sf, static_cast<long long>(runner.target_rows()), static_cast<long long>(lay.total), join_s,
+              prefuse_s, median(tf), median(tn), oracle_s, static_cast<unsigned long long>(cf),
+              static_cast<unsigned long long>(cn), static_cast<unsigned long long>(co), cf == co ? "true" : "false",
+              cn == co ? "true" : "false");
+  return 0;
+}
+
 int main(int argc, char** argv) {
   if (argc >= 2 && std::string(argv[1]) == "--query") return query_mode(argc, argv);
+  if (argc >= 2 && std::string(argv[1]) == "--pipeline") return pipeline_mode(argc, argv);
   if (argc < 2) {
     std::fprintf(stderr, "usage: dropin_bench <dir> [reps]\n");
     return 2;
