@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(256) dgemm_seq_kernel(const double* __restrict
   __shared__ double sA[TK][TM + 1];
   __shared__ double sB[TK][TN];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const int64_t row0 = blockIdx.y * (int64_t)TM, col0 = blockIdx.x * (int64_t)TN;
+  const int64_t row0 = blockIdx.x * (int64_t)TM, col0 = blockIdx.y * (int64_t)TN;  // rows on x: no 65535 cap
   double acc[RM][RN];
 #pragma unroll
   for (int i = 0; i < RM; ++i)
@@ -131,8 +131,8 @@ void dgemm_seq(laq_ctx* ctx, const double* A, int64_t m, int64_t k, const double
   if (n == 1) {
     dgemv_seq_kernel<<<grid_for(m, 128, ctx->sm_count * 16), 128, 0, ctx->stream>>>(A, m, k, B, C);
   } else {
-    const dim3 grid(static_cast<unsigned>((n + TN - 1) / TN), static_cast<unsigned>((m + TM - 1) / TM));
-    if (grid.y > 65535) fail(LAQ_ERR_UNSUPPORTED, "dense_matmul: too many rows for one launch");
+    const dim3 grid(static_cast<unsigned>((m + TM - 1) / TM), static_cast<unsigned>((n + TN - 1) / TN));
+    if (grid.y > 65535 || (m + TM - 1) / TM > 0x7fffffff) fail(LAQ_ERR_UNSUPPORTED, "dense_matmul: output too wide for one launch");
     dgemm_seq_kernel<<<grid, 256, 0, ctx->stream>>>(A, m, k, B, n, C);
   }
   launched(ctx);

@@ -269,3 +269,16 @@ def test_predictor_miss_fallback_alternating(lib):
         torch.cuda.synchronize()
         check(fk, out.cpu().numpy(), int(pred.nnz_dev.item()))
     pred.ctx.bind_stream()
+
+
+def test_dense_matmul_more_row_tiles_than_grid_y(gpu_ctx):
+    """dense_matmul (matrix.cpp:158-174) over more than 65,535 row tiles of 64
+    (the drop-in's non-fused pipeline at S2 sf=2000 multiplies 6M x 64 by 64 x 4):
+    bit-exact vs the sequential oracle."""
+    from paper_2306_08367_b200 import fusion
+    rng = np.random.default_rng(17)
+    m = 64 * 65_536 + 5
+    a = rng.random((m, 3))
+    a[::7, 1] = 0.0  # zero entries are skipped (matrix.cpp:168)
+    b = rng.uniform(-1, 1, (3, 5))
+    assert np.array_equal(np.asarray(fusion.dense_matmul(a, b)), O.dense_matmul(a, b))
