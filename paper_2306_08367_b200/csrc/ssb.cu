@@ -1725,11 +1725,7 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
   // It removes the gather stalls (long-scoreboard 33 % -> 5 %) but doubles the
   // per-row instruction count: SF=100 Q4 group 3.22 -> 3.48 ms, issue-bound.
   B.pipe = !staged[order[b->nl - 1]] && mode != 0 && std::getenv("LAQ_BATCH_PIPE") ? 1 : 0;
-  B.early_at = -1;
-  if (const char* e = std::getenv("LAQ_BATCH_ISSUE_AT")) {  // A/B knob (scripts/batch_ab.py)
-    const int at = std::atoi(e);
-    if (!staged[order[b->nl - 1]] && at >= 0 && at < b->nl - 1) B.early_at = at;
-  }
+
   B.dec_shift = dec32 ? 2 : 3;  // log2(entry bytes * rep)
   while ((1 << (B.dec_shift - (dec32 ? 2 : 3))) < rep) ++B.dec_shift;
   B.flush_every = flush;

@@ -75,7 +75,6 @@ struct BatchScan {
   uint32_t fail_lo, fail_hi;  // every lane failed (rows past the end)
   uint32_t dec_shift;         // log2(8 * decode-table replication)
   int pipe;                   // the last link is L2-gathered: software-pipelined 2-row kernel
-  int early_at;               // >= 0: issue the last (L2-gathered) link's gather after link early_at
   int dec32;                  // narrow decode: 3 x 10-bit lanes in 4-byte entries (<= 3 queries, <= 3 links)
   uint32_t fail32;            // the narrow lanes' fail value (a power of two >= every G)
 };

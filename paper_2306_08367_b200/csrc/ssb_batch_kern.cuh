@@ -120,20 +120,13 @@ __device__ __forceinline__ void batch_rows(const BatchScan& B, int64_t row0, con
         add_fail<DW>(B, lo[r], hi[r], q, static_cast<uint32_t>(comp(fv[f], r)) - flo > span);
     }
   const uint32_t sh = B.dec_shift;  // log2(entry bytes * dec_rep)
-  // early_at >= 0 (the last link gathered through L2): that gather is issued
-  // right after link early_at, so the remaining staged links hide its latency.
-  const int early_at = B.early_at;
-  uint32_t eid[4] = {0, 0, 0, 0};
 #pragma unroll
   for (int j = 0; j < NL; ++j) {
     const BatchLink& L = B.link[j];
     uint32_t sl[4], id[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) sl[r] = min(static_cast<uint32_t>(comp(kv[j], r)) - L.base, L.size);
-    if (j == NL - 1 && early_at >= 0) {
-#pragma unroll
-      for (int r = 0; r < 4; ++r) id[r] = eid[r];
-    } else if (L.fmt == kIdSmemU8) {
+    if (L.fmt == kIdSmemU8) {
 #pragma unroll
       for (int r = 0; r < 4; ++r) id[r] = lds_u8(s_base + L.id_byte + sl[r]);
     } else if (L.fmt == kIdSmemU16) {
@@ -171,19 +164,6 @@ __device__ __forceinline__ void batch_rows(const BatchScan& B, int64_t row0, con
         hi[r] += d.y;
       } else {
         lo[r] += lds_u32(dec_base + L.dec_byte + (id[r] << sh));
-      }
-    }
-    if (j < NL - 1 && j == early_at) {
-      const BatchLink& G = B.link[NL - 1];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const uint32_t gs = min(static_cast<uint32_t>(comp(kv[NL - 1], r)) - G.base, G.size);
-        bool alive = false;
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) alive = alive || lane_w<DW>(lo[r], hi[r], q) < FL;
-        if (G.bm_byte >= 0) alive = alive && ((lds_u32(s_base + G.bm_byte + 4 * (gs >> 5)) >> (gs & 31)) & 1u);
-        eid[r] = G.fmt == kIdGlobU8 ? ldg_u8_if(alive, static_cast<const uint8_t*>(G.ids) + gs, G.miss)
-                                    : ldg_u16_if(alive, static_cast<const uint16_t*>(G.ids) + gs, G.miss);
       }
     }
   }

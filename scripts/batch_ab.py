@@ -33,8 +33,7 @@ def main():
                 ("bitmap_first+pipe", {"LAQ_BATCH_BITMAP_FIRST": "1", "LAQ_BATCH_PIPE": "1"}),
                 ("pipe", {"LAQ_BATCH_PIPE": "1"}), ("dec64", {"LAQ_BATCH_DEC64": "1"}),
                 ("bulkpf=-1", {"LAQ_PREFETCH": "-1"}), ("bulkpf=-2", {"LAQ_PREFETCH": "-2"}),
-                ("bulkpf=-4", {"LAQ_PREFETCH": "-4"}),
-                ("issue_at=0", {"LAQ_BATCH_ISSUE_AT": "0"}), ("issue_at=1", {"LAQ_BATCH_ISSUE_AT": "1"})]
+                ("bulkpf=-4", {"LAQ_PREFETCH": "-4"})]
     out = {"sf": SF}
     for grp in (3, 4):
         qs = [Q.spec_with_dial(d, grp, x) for d, x in zip(Q.group_defs(grp), dials[grp])]
