@@ -3,7 +3,7 @@
 (count, sum) vs sum-only bins.  Knobs are read when a batch is prepared, so
 each setting prepares its own batch.  Prints one JSON object.
 
-  python scripts/batch_ab.py [--sf 100]
+  python scripts/batch_ab.py [--sf 100] [--only default,vec=2,...]
 """
 import json
 import os
@@ -34,6 +34,9 @@ def main():
                 ("pipe", {"LAQ_BATCH_PIPE": "1"}), ("dec64", {"LAQ_BATCH_DEC64": "1"}),
                 ("bulkpf=-1", {"LAQ_PREFETCH": "-1"}), ("bulkpf=-2", {"LAQ_PREFETCH": "-2"}),
                 ("bulkpf=-4", {"LAQ_PREFETCH": "-4"})]
+    if "--only" in sys.argv:
+        keep = sys.argv[sys.argv.index("--only") + 1].split(",")
+        settings = [s for s in settings if s[0] in keep]
     out = {"sf": SF}
     for grp in (3, 4):
         qs = [Q.spec_with_dial(d, grp, x) for d, x in zip(Q.group_defs(grp), dials[grp])]
