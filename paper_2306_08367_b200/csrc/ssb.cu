@@ -20,6 +20,7 @@
 //    (the NCCL all-reduce buffer when the fact table is sharded across GPUs).
 // Integer sums are exact, so results equal the reference bit for bit.
 #include <algorithm>
+#include <cstdio>
 #include <climits>
 #include <cstdlib>
 #include <cstring>
@@ -1736,6 +1737,16 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
   b->bytes_per_row = 4 * (b->nl + b->nf + B.has_measure);
   b->fused = true;
   b->why.clear();
+  if (std::getenv("LAQ_BATCH_VERBOSE")) {
+    std::fprintf(stderr, "[laq batch] nq=%d nl=%d nf=%d mode=%d dec32=%d rep=%d smem=%lld\n", nq, b->nl, b->nf, mode,
+                 dec32 ? 1 : 0, rep, static_cast<long long>(off));
+    for (int t = 0; t < b->nl; ++t) {
+      const int j = order[t];
+      std::fprintf(stderr, "[laq batch]   link %d: slots=%lld tuples=%d frac=%.3f fmt=%d id_bytes=%d bm_bytes=%d\n", t,
+                   static_cast<long long>(D.l[j].slots), b->n_dec[j], frac[j], B.link[t].fmt, B.link[t].id_bytes,
+                   B.link[t].bm_byte >= 0 ? B.link[t].bm_bytes : 0);
+    }
+  }
   batch_build(ctx, b, true);  // leave the batch ready to scan
 }
 
