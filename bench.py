@@ -681,22 +681,37 @@ def fused_predict_bench(ctx):
                        "note": "12 B/row (4 B key + 8 B fp64 prediction), measured at 1e8 rows; at 1M rows one call "
                                "is a single launch (n1000000.ms) against a same-traffic torch copy "
                                "(n1000000.same_traffic_torch_copy_ms)"}
-    # e2e through the API with host buffers (H2D keys, fused join+predict, D2H predictions)
+    # e2e through the API with host buffers: FusedStarPredictor.predict_host
+    # (laq_probe_fused_predict_host): pinned keys in, pinned predictions out,
+    # H2D / probe / D2H pipelined in chunks over two copy streams
     fk_pin = torch.from_numpy(fk.astype(np.int32)).pin_memory()
     y_pin = torch.empty((1_000_000, 1), dtype=torch.float64).pin_memory()
-    fkd = torch.empty(1_000_000, dtype=torch.int32, device="cuda")
-    y = torch.empty((1_000_000, 1), dtype=torch.float64, device="cuda")
     for it in range(13):
         if it == 3:
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-        fkd.copy_(fk_pin, non_blocking=True)
-        pred([fkd], out=y, sync=False)
-        y_pin.copy_(y, non_blocking=True)
-        torch.cuda.synchronize()
+        yh, nnz = pred.predict_host([fk_pin], out=y_pin)
     e2e_ms = (time.perf_counter() - t0) * 1e3 / 10
+    if nnz != 1_000_000 or not np.array_equal(yh.numpy(), y1):
+        raise SystemExit("PARITY FAILURE: host-buffer fused predict differs from the device path")
     out["e2e"] = {"value": 1e6 / (e2e_ms / 1e3), "unit": UNIT, "ms": e2e_ms, "h2d_bytes_per_step": 4_000_000,
-                  "d2h_bytes_per_step": 8_000_000}
+                  "d2h_bytes_per_step": 8_000_000,
+                  "path": "FusedStarPredictor.predict_host -> laq_probe_fused_predict_host (C-ABI): pinned host keys "
+                          "in, pinned host predictions out, one call (host clock)"}
+    # the same call at 1e8 rows, where it pipelines 8 pieces over two copy streams
+    big = torch.randint(0, 10_000, (100_000_000,), dtype=torch.int32).pin_memory()
+    ybig = torch.empty((100_000_000, 1), dtype=torch.float64).pin_memory()
+    pred.predict_host([big], out=ybig)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        _, nb = pred.predict_host([big], out=ybig)
+    big_ms = (time.perf_counter() - t0) * 1e3 / 3
+    out["e2e_n100000000"] = {"value": 1e8 / (big_ms / 1e3), "unit": UNIT, "ms": big_ms,
+                             "h2d_bytes_per_step": 400_000_000, "d2h_bytes_per_step": 800_000_000,
+                             "pcie_gbs": 1.2e9 / (big_ms / 1e3) / 1e9, "nnz": nb,
+                             "path": "predict_host: 8 pieces, keys H2D / probe / predictions D2H overlapped"}
+    del big, ybig
     # e2e through the reference's UNCHANGED C++ API with host std::vectors
     # (integration/dropin_bench.cpp over the drop-in: multiway_star_join ->
     # csr_from_coo -> prefuse_linear -> apply_fused_linear, each call H2D + D2H)

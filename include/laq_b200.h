@@ -203,6 +203,17 @@ int laq_probe_bind_partials(laq_ctx* ctx, laq_probe* probe, const double* const*
 int laq_probe_fused_predict(laq_ctx* ctx, const laq_probe* probe, const int32_t* const* d_fks,
                             int64_t n_fact, const double* const* d_partials, int64_t l,
                             double* d_out, int64_t* d_survivors, int64_t* d_nnz);
+/* The same with HOST buffers (the reference-facing call: keys in, predictions
+ * out in host memory): h_fks[j] are n_fact int32 keys, h_out has room for
+ * n_fact * l doubles and receives the *h_nnz surviving rows in ascending fact
+ * order.  The keys stream H2D and the predictions D2H in chunk_rows pieces
+ * (0: one piece up to 4M rows, else n_fact / 8) on two copy streams,
+ * overlapped with each other and with the probe kernel; pinned host memory
+ * gives the full PCIe rate.
+ * Needs direct probes and partials bound with laq_probe_bind_partials.
+ * Synchronises before returning. */
+int laq_probe_fused_predict_host(laq_ctx* ctx, const laq_probe* probe, const int32_t* const* h_fks,
+                                 int64_t n_fact, int64_t l, double* h_out, int64_t chunk_rows, int64_t* h_nnz);
 int laq_probe_destroy(laq_probe* probe);
 
 /* Star join over prebuilt probe tables, compacted to int32 row maps

@@ -77,6 +77,7 @@ _SIGS = {
     "laq_fused_star_predict": (C.c_int, [vp, i32, vp, i64, vp, i64p, vp, i64, vp, vp, i64p]),
     "laq_probe_build": (C.c_int, [vp, i32, vp, i64p, C.POINTER(vp)]),
     "laq_probe_fused_predict": (C.c_int, [vp, vp, vp, i64, vp, i64, vp, vp, vp]),
+    "laq_probe_fused_predict_host": (C.c_int, [vp, vp, vp, i64, i64, vp, i64, vp]),
     "laq_probe_destroy": (C.c_int, [vp]),
     "laq_probe_bind_partials": (C.c_int, [vp, vp, vp, i64]),
     "laq_probe_join_rows": (C.c_int, [vp, vp, vp, i64, vp, vp, vp]),

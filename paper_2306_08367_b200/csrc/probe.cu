@@ -12,6 +12,8 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
+#include <memory>
 
 #include "predict_slot.cuh"
 #include "probe.cuh"
@@ -409,6 +411,35 @@ void run_star(laq_ctx* ctx, StarArgs<K>& a, StarScratch& scratch, bool predict) 
   launched(ctx);
 }
 
+// Host-buffer pipeline of laq_probe_fused_predict_host: fact keys H2D on
+// `up`, the fused predict on the context stream, predictions D2H on `down`,
+// double-buffered so chunk c+1's keys and chunk c-1's predictions cross PCIe
+// (full duplex) while chunk c is probed.
+struct HostPipe {
+  cudaStream_t up = nullptr, down = nullptr;
+  cudaEvent_t loaded[2]{}, computed[2]{}, drained[2]{};
+  DevMem<int32_t> keys[2];  // [link][cap] per buffer
+  DevMem<double> y[2];      // [cap][l] per buffer
+  DevMem<int64_t> nnz;      // survivors per chunk
+  int64_t* h_nnz = nullptr;  // pinned copy of nnz
+  int64_t cap = 0, chunks = 0;
+  int nl = 0, l = 0;
+  HostPipe() {
+    LAQ_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
+    LAQ_CUDA(cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b)
+      for (cudaEvent_t* e : {&loaded[b], &computed[b], &drained[b]})
+        LAQ_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
+  ~HostPipe() {
+    for (int b = 0; b < 2; ++b)
+      for (cudaEvent_t e : {loaded[b], computed[b], drained[b]}) cudaEventDestroy(e);
+    if (up) cudaStreamDestroy(up);
+    if (down) cudaStreamDestroy(down);
+    if (h_nnz) cudaFreeHost(h_nnz);
+  }
+};
+
 }  // namespace laq
 
 using namespace laq;
@@ -432,6 +463,7 @@ struct laq_probe {
   // the write pass reads
   // [2] CTAs finished (the one-launch form's last-CTA counter, reset by that CTA)
   DevMem<unsigned long long> miss{3};
+  std::unique_ptr<HostPipe> host;  // laq_probe_fused_predict_host's streams and buffers
 };
 
 namespace laq {
@@ -721,6 +753,93 @@ int laq_probe_fused_predict(laq_ctx* ctx, const laq_probe* probe, const int32_t*
     a.nnz = d_nnz;
     a.err = p->err.get();
     run_star(ctx, a, p->scratch, true);
+  });
+}
+
+int laq_probe_fused_predict_host(laq_ctx* ctx, const laq_probe* probe, const int32_t* const* h_fks, int64_t n_fact,
+                                 int64_t l, double* h_out, int64_t chunk_rows, int64_t* h_nnz) {
+  return guard(ctx, [&] {
+    auto* p = const_cast<laq_probe*>(probe);
+    if (l < 1 || l > 8) fail(LAQ_ERR_UNSUPPORTED, "fused single-pass predict handles l <= 8 (use star join + apply)");
+    for (int j = 0; j < p->n_links; ++j)
+      if (p->probes[j].kind != PROBE_DIRECT)
+        fail(LAQ_ERR_UNSUPPORTED, "host-buffer fused predict: hashed dimension keys (use laq_probe_fused_predict)");
+    if (!p->bound || p->pslot_l != l) fail(LAQ_ERR_SHAPE, "host-buffer fused predict: bind the partials first");
+    if (n_fact < 0) fail(LAQ_ERR_SHAPE, "negative row count");
+    // Default: one piece up to 4M rows (PCIe runs H2D and D2H only partly in
+    // parallel on these boxes: 4 MB up + 8 MB down take 197 us concurrently vs
+    // 231 us back to back, less than the per-piece stream/event overhead at that
+    // size), eight pieces above.
+    if (chunk_rows <= 0) chunk_rows = n_fact <= (int64_t{4} << 20) ? n_fact : (n_fact + 7) / 8;
+    chunk_rows = std::max<int64_t>(1024, (chunk_rows + 1023) & ~int64_t{1023});  // 16-byte aligned key pieces
+    const int64_t chunks = std::max<int64_t>(1, (n_fact + chunk_rows - 1) / chunk_rows);
+    if (!p->host) p->host = std::make_unique<HostPipe>();
+    HostPipe& h = *p->host;
+    if (h.cap < chunk_rows || h.nl != p->n_links || h.l != l) {
+      for (int b = 0; b < 2; ++b) {
+        h.keys[b] = DevMem<int32_t>(static_cast<size_t>(chunk_rows * p->n_links));
+        h.y[b] = DevMem<double>(static_cast<size_t>(chunk_rows * l));
+      }
+      h.cap = chunk_rows, h.nl = p->n_links, h.l = static_cast<int>(l);
+    }
+    if (h.chunks < chunks) {
+      h.nnz = DevMem<int64_t>(static_cast<size_t>(chunks));
+      if (h.h_nnz) cudaFreeHost(h.h_nnz);
+      h.h_nnz = nullptr;
+      LAQ_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h.h_nnz), chunks * sizeof(int64_t)));
+      h.chunks = chunks;
+    }
+    if (chunks == 1) {  // one piece: H2D, probe, D2H in order on the context stream
+      const int32_t* kp[kMaxLinks];
+      for (int j = 0; j < p->n_links; ++j) {
+        int32_t* d = h.keys[0].get() + j * h.cap;
+        if (n_fact > 0)
+          LAQ_CUDA(cudaMemcpyAsync(d, h_fks[j], n_fact * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+        kp[j] = d;
+      }
+      run_slot_predict(ctx, p, kp, n_fact, nullptr, l, h.y[0].get(), nullptr, h.nnz.get());
+      if (n_fact > 0)
+        LAQ_CUDA(cudaMemcpyAsync(h_out, h.y[0].get(), n_fact * l * sizeof(double), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+      LAQ_CUDA(cudaMemcpyAsync(h.h_nnz, h.nnz.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+      sync(ctx);
+      *h_nnz = h.h_nnz[0];
+      return;
+    }
+    // the copies may not start before earlier work on the context stream
+    LAQ_CUDA(cudaEventRecord(h.computed[1], ctx->stream));
+    LAQ_CUDA(cudaStreamWaitEvent(h.up, h.computed[1], 0));
+    for (int64_t c = 0; c < chunks; ++c) {
+      const int b = static_cast<int>(c & 1);
+      const int64_t r0 = c * chunk_rows, m = std::min(chunk_rows, n_fact - r0);
+      if (c >= 2) LAQ_CUDA(cudaStreamWaitEvent(h.up, h.drained[b], 0));  // buffer b's previous chunk is out
+      const int32_t* kp[kMaxLinks];
+      for (int j = 0; j < p->n_links; ++j) {
+        int32_t* d = h.keys[b].get() + j * h.cap;
+        if (m > 0) LAQ_CUDA(cudaMemcpyAsync(d, h_fks[j] + r0, m * sizeof(int32_t), cudaMemcpyHostToDevice, h.up));
+        kp[j] = d;
+      }
+      LAQ_CUDA(cudaEventRecord(h.loaded[b], h.up));
+      LAQ_CUDA(cudaStreamWaitEvent(ctx->stream, h.loaded[b], 0));
+      run_slot_predict(ctx, p, kp, m, nullptr, l, h.y[b].get(), nullptr, h.nnz.get() + c);
+      LAQ_CUDA(cudaEventRecord(h.computed[b], ctx->stream));
+      LAQ_CUDA(cudaStreamWaitEvent(h.down, h.computed[b], 0));
+      if (m > 0)
+        LAQ_CUDA(cudaMemcpyAsync(h_out + r0 * l, h.y[b].get(), m * l * sizeof(double), cudaMemcpyDeviceToHost,
+                                 h.down));
+      LAQ_CUDA(cudaEventRecord(h.drained[b], h.down));
+    }
+    LAQ_CUDA(cudaMemcpyAsync(h.h_nnz, h.nnz.get(), chunks * sizeof(int64_t), cudaMemcpyDeviceToHost, h.down));
+    LAQ_CUDA(cudaStreamSynchronize(h.down));
+    // Each chunk's survivors sit at its own start: close the gaps (none when
+    // every key joins, the common case) keeping ascending fact order.
+    int64_t at = 0;
+    for (int64_t c = 0; c < chunks; ++c) {
+      const int64_t r0 = c * chunk_rows, k = h.h_nnz[c];
+      if (at != r0 && k > 0) std::memmove(h_out + at * l, h_out + r0 * l, static_cast<size_t>(k * l) * sizeof(double));
+      at += k;
+    }
+    *h_nnz = at;
   });
 }
 

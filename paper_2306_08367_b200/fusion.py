@@ -133,6 +133,32 @@ class FusedStarPredictor:
         nnz = int(self.nnz_dev.item())
         return out[:nnz], nnz
 
+    def predict_host(self, fact_fks, out=None, chunk_rows=0):
+        """The same operator with HOST buffers (laq_probe_fused_predict_host):
+        int32 keys in host memory, predictions written to a host float64
+        [n, l] buffer (`out`, allocated pinned when None); the keys' H2D and
+        the predictions' D2H are chunked over two copy streams and overlap the
+        probe kernel.  Returns (out[:nnz], nnz).  Pinned inputs (torch
+        pin_memory tensors) stream at the full PCIe rate."""
+        if not self.bound:
+            raise errors.ShapeError("predict_host needs partials bound at construction")
+        keys = [f if isinstance(f, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(f, np.int32))
+                for f in fact_fks]
+        for k in keys:
+            if k.is_cuda or k.dtype != torch.int32 or not k.is_contiguous():
+                raise errors.ShapeError("predict_host takes contiguous int32 host keys")
+        n = keys[0].numel()
+        if out is None:
+            out = torch.empty((n, self.l), dtype=f64, pin_memory=True)
+        if out.is_cuda or out.dtype != f64 or out.numel() < n * self.l:
+            raise errors.ShapeError("predict_host writes a float64 host buffer of n * l values")
+        nnz = C.c_int64(0)
+        kp = (C.c_void_p * len(keys))(*[k.data_ptr() for k in keys])
+        self.ctx.bind_stream()
+        self.ctx.check(self.ctx.lib.laq_probe_fused_predict_host(
+            self.ctx.h, self.h, kp, n, self.l, out.data_ptr(), int(chunk_rows), C.byref(nnz)))
+        return out[:nnz.value], int(nnz.value)
+
     def close(self):
         if getattr(self, "h", None):
             self.ctx.lib.laq_probe_destroy(self.h)

@@ -271,6 +271,35 @@ def test_predictor_miss_fallback_alternating(lib):
     pred.ctx.bind_stream()
 
 
+@pytest.mark.parametrize("n,chunk", [(0, 0), (1, 0), (1_000_000, 0), (700_001, 65_536), (300_000, 1_000)])
+def test_predictor_host_buffers_pipelined(lib, n, chunk):
+    """laq_probe_fused_predict_host: keys in and predictions out in host
+    memory, chunked over two copy streams; with and without missing keys (the
+    per-chunk survivors are closed up on the host) -- equal to the oracle's
+    fused pipeline (bit-exact) and to the device-buffer call."""
+    import torch
+    _, fusion, _ = lib
+    rng = np.random.default_rng(31 + n)
+    pk = [np.arange(4_000) + 3, np.arange(900)]
+    P = [rng.random((4_000, 2)), rng.random((900, 2))]
+    pred = fusion.FusedStarPredictor(pk, P)
+    full = [rng.integers(3, 4_003, n), rng.integers(0, 900, n)]
+    miss = [full[0].copy(), full[1]]
+    miss[0][rng.random(n) < 0.02] = 5_000  # past the domain: dropped (inner join)
+    for fks in (full, miss):
+        keys = [torch.from_numpy(f.astype(np.int32)).pin_memory() for f in fks]
+        y, nnz = pred.predict_host(keys, chunk_rows=chunk)
+        ws, wr = O.multiway_star_join(fks, pk)
+        want = O.apply_fused_linear(wr, P)
+        assert nnz == len(ws) and np.array_equal(y.numpy(), want)
+        # pageable numpy keys take the same path
+        y2, nnz2 = pred.predict_host([f.astype(np.int32) for f in fks], chunk_rows=chunk)
+        assert nnz2 == nnz and np.array_equal(y2.numpy(), want)
+        if n:
+            yd, nd = pred([torch.from_numpy(f.astype(np.int32)).cuda() for f in fks])
+            assert nd == nnz and np.array_equal(yd.cpu().numpy(), want)
+
+
 def test_dense_matmul_more_row_tiles_than_grid_y(gpu_ctx):
     """dense_matmul (matrix.cpp:158-174) over more than 65,535 row tiles of 64
     (the drop-in's non-fused pipeline at S2 sf=2000 multiplies 6M x 64 by 64 x 4):
