@@ -20,10 +20,14 @@
 //   warps 0-7   epilogue: tcgen05.ld (thread = row, 32 columns per load), unscale,
 //               transpose through a swizzled 4 KB shared tile so every store
 //               instruction writes four full 128-byte row segments of C;
-//   warps 8-11  cp.async producers: per stage (one 32-feature K block) the 128
-//               A lines (gathered) + BN W lines, cp.async.mbarrier.arrive.noinc;
+//   warps 8-11  producers: per stage (one 32-feature K block) the 128 A lines
+//               (gathered rows: cp.async, cp.async.mbarrier.arrive.noinc) and the
+//               BN W lines (dense: ONE TMA tile load, 128B-swizzled by the tensor
+//               map, issued by one thread with expect_tx on the same barrier);
 //   warp 12     TMEM owner + MMA issuer: 3 x (1..2) tcgen05.mma per stage into
 //               one of two TMEM accumulators.
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstdlib>
 #include <string>
@@ -45,6 +49,8 @@ constexpr int kMaxBlocks = 64;  // K <= 2048
 constexpr uint32_t kABytes = kRows * 128u;
 
 struct Args {
+  CUtensorMap wmap;                   // W as a 2-D fp16 tensor [n_blocks * n_pad rows][64], box {64, BN}, 128B swizzle
+  int w_tma;                          // 1: W tiles by TMA (wmap), 0: by cp.async
   const tc::elem* block[kMaxBlocks];  // A block b: [rows_j x 64]
   int block_dim[kMaxBlocks];
   int block_steps[kMaxBlocks];
@@ -87,7 +93,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   if (warp == kMmaWarp) {
     if (lane == 0) {
       for (int s = 0; s < S; ++s) {
-        tc::mbar_init(&full[s], kProdWarps * 32);
+        tc::mbar_init(&full[s], kProdWarps * 32 + a.w_tma);  // + the TMA issuer's expect_tx arrive
         tc::mbar_init(&empty[s], 1);
       }
       for (int b = 0; b < 2; ++b) {
@@ -131,10 +137,17 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           const int r = 32 * pw + 4 * q + sub;
           tc::cp_async16(st + tc::sw128_off(r, chunk), ab + static_cast<int64_t>(s_rows[pw][j][4 * q + sub]) * 64);
         }
-        // W: BN rows of block b, this warp's quarter (contiguous in global)
-        const tc::elem* wb = a.w + (static_cast<int64_t>(b) * a.n_pad + nt * BN) * 64 + chunk * 8;
-        for (int r = pw * 4 + sub; r < BN; r += 16)
-          tc::cp_async16(st + kABytes + tc::sw128_off(r, chunk), wb + static_cast<int64_t>(r) * 64);
+        // W: BN rows of block b (contiguous in global)
+        if (a.w_tma) {
+          if (pw == 0 && lane == 0) {
+            tc::mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(BN) * 128u);
+            tc::tma_load_2d(&a.wmap, &full[s], st + kABytes, 0, static_cast<int32_t>(b * a.n_pad + nt * BN));
+          }
+        } else {
+          const tc::elem* wb = a.w + (static_cast<int64_t>(b) * a.n_pad + nt * BN) * 64 + chunk * 8;
+          for (int r = pw * 4 + sub; r < BN; r += 16)
+            tc::cp_async16(st + kABytes + tc::sw128_off(r, chunk), wb + static_cast<int64_t>(r) * 64);
+        }
         tc::cp_async_arrive_noinc(&full[s]);
       }
       __syncwarp();  // s_rows reuse
@@ -369,6 +382,8 @@ int laq_tc_gemm(laq_ctx* ctx, const laq_tc_features* f, const int32_t* const* d_
     a.BN = BN;
     a.w = w.get();
     a.n_pad = n_pad;
+    a.w_tma = !std::getenv("LAQ_GEMM_NO_TMA") &&
+              tc::encode_rows128(&a.wmap, w.get(), static_cast<uint64_t>(f->n_blocks * n_pad), static_cast<uint32_t>(BN));
     a.c = d_out;
     a.unscale = static_cast<float>(1.0 / (f->scale * sw));
     a.m_tiles = (m + gemm::kRows - 1) / gemm::kRows;

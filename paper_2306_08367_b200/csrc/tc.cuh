@@ -11,6 +11,7 @@
 #pragma once
 
 #include <cuda_fp16.h>
+#include <cudaTypedefs.h>
 
 #include <cmath>
 #include <stdint.h>
@@ -99,6 +100,15 @@ __device__ __forceinline__ void tma_gather4(const void* tmap, uint64_t* bar, uin
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
+// Tile load: box {inner, rows} of a 2-D tensor map at (c0, r0) -> smem with the
+// map's swizzle (SASS UTMALDG); completion counted in bytes on `bar`.
+__device__ __forceinline__ void tma_load_2d(const void* tmap, uint64_t* bar, uint32_t dst, int32_t c0, int32_t r0) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(r0)
       : "memory");
 }
 __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
@@ -327,6 +337,29 @@ __global__ void split_w1_kernel(const double* __restrict__ W, int64_t n, const i
   }
 }
 }  // namespace
+
+// Host: a 2-D tensor map over rows of 128 bytes (64 fp16) -- the split block
+// layout -- with box {64, box_rows} and the 128-byte swizzle the UMMA smem
+// descriptors expect (sw128_off).  cuTensorMapEncodeTiled comes from the driver
+// through the runtime's entry-point query (no -lcuda).  false if unavailable.
+inline bool encode_rows128(CUtensorMap* m, const void* base, uint64_t rows, uint32_t box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  if (!enc || box_rows < 1 || box_rows > 256 || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+  const cuuint64_t dims[2] = {64, rows};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {64, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 }  // namespace tc
 }  // namespace laq
