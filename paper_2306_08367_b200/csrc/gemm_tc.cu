@@ -50,7 +50,9 @@ constexpr uint32_t kABytes = kRows * 128u;
 
 struct Args {
   CUtensorMap wmap;                   // W as a 2-D fp16 tensor [n_blocks * n_pad rows][64], box {64, BN}, 128B swizzle
+  CUtensorMap amap[kMaxBlocks];       // identity rows: A block b as [rows][64], box {64, 128}
   int w_tma;                          // 1: W tiles by TMA (wmap), 0: by cp.async
+  int a_tma;                          // 1: A tiles by TMA too (identity rows, prefuse); one producer thread
   const tc::elem* block[kMaxBlocks];  // A block b: [rows_j x 64]
   int block_dim[kMaxBlocks];
   int block_steps[kMaxBlocks];
@@ -93,7 +95,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   if (warp == kMmaWarp) {
     if (lane == 0) {
       for (int s = 0; s < S; ++s) {
-        tc::mbar_init(&full[s], kProdWarps * 32 + a.w_tma);  // + the TMA issuer's expect_tx arrive
+        // cp.async arrivals of the producer warps + the TMA issuer's expect_tx arrive
+        tc::mbar_init(&full[s], a.a_tma ? 1 : kProdWarps * 32 + a.w_tma);
         tc::mbar_init(&empty[s], 1);
       }
       for (int b = 0; b < 2; ++b) {
@@ -110,7 +113,23 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp >= kProdWarp0 && warp < kProdWarp0 + kProdWarps) {
+  if (warp >= kProdWarp0 && warp < kProdWarp0 + kProdWarps && a.a_tma) {
+    // ================= TMA producer (identity rows: A and W tiles dense) =================
+    if (warp == kProdWarp0 && lane == 0) {
+      int it = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+        const int64_t nt = a.m_major ? t % a.n_tiles : t / a.m_tiles, mt = a.m_major ? t / a.n_tiles : t % a.m_tiles;
+        for (int b = 0; b < NB; ++b, ++it) {
+          const int s = it % S;
+          tc::mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+          const uint32_t st = sbase + s * SB;
+          tc::mbar_arrive_expect_tx(&full[s], kABytes + static_cast<uint32_t>(BN) * 128u);
+          tc::tma_load_2d(&a.amap[b], &full[s], st, 0, static_cast<int32_t>(mt * kRows));  // rows past m: zero fill
+          tc::tma_load_2d(&a.wmap, &full[s], st + kABytes, 0, static_cast<int32_t>(b * a.n_pad + nt * BN));
+        }
+      }
+    }
+  } else if (warp >= kProdWarp0 && warp < kProdWarp0 + kProdWarps) {
     // ================= cp.async producers =================
     const int pw = warp - kProdWarp0;
     __shared__ int32_t s_rows[kProdWarps][kMaxDims][32];
@@ -280,6 +299,8 @@ struct laq_tc_features {
   int n_blocks = 0;
   int block_dim[gemm::kMaxBlocks] = {}, block_steps[gemm::kMaxBlocks] = {};
   DevMem<tc::elem> blocks[gemm::kMaxBlocks];
+  CUtensorMap amap[gemm::kMaxBlocks];  // block b as a TMA tensor (identity-row GEMMs)
+  bool amap_ok = false;
   std::vector<int64_t> perm;  // 32 * n_blocks entries, -1 = padding
   DevMem<int64_t> dperm;
 };
@@ -329,6 +350,11 @@ int laq_tc_features_create(laq_ctx* ctx, int32_t n_dims, const double* const* d_
           launched(ctx);
         }
       }
+      f->amap_ok = true;
+      for (int b = 0; b < f->n_blocks; ++b)
+        f->amap_ok = f->amap_ok && tc::encode_rows128(&f->amap[b], f->blocks[b].get(),
+                                                      static_cast<uint64_t>(std::max<int64_t>(h_dim_rows[src[b].first], 1)),
+                                                      gemm::kRows);
       f->dperm = DevMem<int64_t>(f->perm.size());
       LAQ_CUDA(cudaMemcpyAsync(f->dperm.get(), f->perm.data(), f->perm.size() * sizeof(int64_t),
                                cudaMemcpyHostToDevice, ctx->stream));
@@ -384,6 +410,9 @@ int laq_tc_gemm(laq_ctx* ctx, const laq_tc_features* f, const int32_t* const* d_
     a.n_pad = n_pad;
     a.w_tma = !std::getenv("LAQ_GEMM_NO_TMA") &&
               tc::encode_rows128(&a.wmap, w.get(), static_cast<uint64_t>(f->n_blocks * n_pad), static_cast<uint32_t>(BN));
+    a.a_tma = a.w_tma && !d_rows && f->amap_ok && !std::getenv("LAQ_GEMM_NO_TMA_A");
+    if (a.a_tma)
+      for (int b = 0; b < f->n_blocks; ++b) a.amap[b] = f->amap[b];
     a.c = d_out;
     a.unscale = static_cast<float>(1.0 / (f->scale * sw));
     a.m_tiles = (m + gemm::kRows - 1) / gemm::kRows;

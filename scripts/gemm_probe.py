@@ -1,6 +1,7 @@
 """tcgen05 GEMM (K5/K7, csrc/gemm_tc.cu) throughput on the complexity-sweep
 shapes, W tiles by TMA (default) vs cp.async (LAQ_GEMM_NO_TMA=1): device ms
-(CUDA events, median of 5), algorithmic TFLOP/s (2 m k n) and the tensor-pipe
+(CUDA events, median of 5; prefuse = identity rows: A tiles by TMA too unless
+LAQ_GEMM_NO_TMA_A=1), algorithmic TFLOP/s (2 m k n) and the tensor-pipe
 rate (x3: the hi.hi + hi.lo + lo.hi fp16 split); results must be bit-identical."""
 import json
 import os
@@ -39,20 +40,20 @@ for r, k, l in [(1_000_000, 1024, 4096), (1_000_000, 512, 1024), (100_000, 1024,
     P = torch.empty((r, l), dtype=torch.float32, device="cuda")
     Y = torch.empty((F, l), dtype=torch.float32, device="cuda")
     cell = {}
-    for name, env in (("tma", None), ("cp_async", "1")):
-        if env:
-            os.environ["LAQ_GEMM_NO_TMA"] = env
-        else:
-            os.environ.pop("LAQ_GEMM_NO_TMA", None)
+    for name, env in (("tma", {}), ("tma_w_only", {"LAQ_GEMM_NO_TMA_A": "1"}), ("cp_async", {"LAQ_GEMM_NO_TMA": "1"})):
+        for key in ("LAQ_GEMM_NO_TMA", "LAQ_GEMM_NO_TMA_A"):
+            os.environ.pop(key, None)
+        os.environ.update(env)
         ms_p = timed(lambda: feats.gemm(W, out=P))
         ms_n = timed(lambda: feats.gemm(W, row_maps=[fk], out=Y))
         cell[name] = {"prefuse_ms": round(ms_p, 3), "prefuse_alg_tflops": round(2 * r * k * l / ms_p / 1e9, 1),
                       "nonfused_ms": round(ms_n, 3), "nonfused_alg_tflops": round(2 * F * k * l / ms_n / 1e9, 1),
                       "nonfused_pipe_tflops": round(6 * F * k * l / ms_n / 1e9, 1),
                       "P_sum": float(P.double().sum()), "Y_sum": float(Y.double().sum())}
-    os.environ.pop("LAQ_GEMM_NO_TMA", None)
-    cell["bit_identical"] = cell["tma"]["P_sum"] == cell["cp_async"]["P_sum"] and \
-        cell["tma"]["Y_sum"] == cell["cp_async"]["Y_sum"]
+    for key in ("LAQ_GEMM_NO_TMA", "LAQ_GEMM_NO_TMA_A"):
+        os.environ.pop(key, None)
+    cell["bit_identical"] = all(cell[v]["P_sum"] == cell["cp_async"]["P_sum"] and
+                                cell[v]["Y_sum"] == cell["cp_async"]["Y_sum"] for v in ("tma", "tma_w_only"))
     out[f"r={r} k={k} l={l}"] = cell
     print(json.dumps({f"r={r} k={k} l={l}": cell}), flush=True)
     del B, fk, W, feats, P, Y
