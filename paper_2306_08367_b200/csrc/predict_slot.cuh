@@ -213,6 +213,10 @@ __global__ void __launch_bounds__(BT, 1) direct_chunks_kernel(const Args a, int6
   double* s_p = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(s_bits) + ((a.smem_words * 4 + 15) & ~15));
   __shared__ __align__(8) uint64_t s_bar;
   bool staged = a.bulk_bytes <= 0;  // bulk copies in flight until the first wait
+  // Programmatic dependent launch (the host sets it for back-to-back calls on
+  // a probe whose tables did not change): the next call may start its own
+  // table staging on free SMs while this grid finishes.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (a.bulk_bytes > 0) {
     // One thread hands every staged table (bitmaps, slot-ordered partials) to
     // the TMA engine; the CTA waits once on the mbarrier.  (A per-thread copy
@@ -239,6 +243,10 @@ __global__ void __launch_bounds__(BT, 1) direct_chunks_kernel(const Args a, int6
         for (int64_t s = threadIdx.x; s < a.size[j]; s += BT) s_p[a.p_off[j] + s] = __ldg(a.pslot[j] + s);
     __syncthreads();
   }
+  // Everything below (keys, Y, counters) may depend on the previous kernel in
+  // the stream: wait for it (a no-op without programmatic dependent launch).
+  // Only the probe's own constant tables are read above.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   constexpr int64_t kRows = int64_t{SEGS} * kSegRows;
   const int lane = threadIdx.x & 31;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (BT / 32);

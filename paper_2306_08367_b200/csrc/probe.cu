@@ -464,6 +464,7 @@ struct laq_probe {
   // [2] CTAs finished (the one-launch form's last-CTA counter, reset by that CTA)
   DevMem<unsigned long long> miss{3};
   std::unique_ptr<HostPipe> host;  // laq_probe_fused_predict_host's streams and buffers
+  bool tables_stable = false;      // staged tables unchanged since the last one-launch predict (PDL is safe)
 };
 
 namespace laq {
@@ -496,6 +497,7 @@ void bind_slots(laq_ctx* ctx, laq_probe* p, const double* const* d_P, int64_t l)
   }
   p->pslot_l = l;
   p->bound = true;
+  p->tables_stable = false;  // the bind kernels just wrote the staged tables: the next predict launches normally
 }
 
 // Fused predict over slot-ordered partials; every probe must be DIRECT.
@@ -536,7 +538,7 @@ void run_slot_predict(laq_ctx* ctx, laq_probe* p, const int32_t* const* d_fks, i
   // l == 1: stage the slot-ordered partials too when they fit in 96 KB
   // (shared-memory gathers instead of one L1 wavefront per lane).
   int64_t doubles = 0;
-  if (l == 1)
+  if (l == 1 && !std::getenv("LAQ_PREDICT_NO_PSTAGE"))
     for (int j = 0; j < p->n_links; ++j) {
       const int64_t d = (std::max<int64_t>(a.size[j], 1) + 1) & ~int64_t{1};
       if ((doubles + d) * 8 <= 96 * 1024) {
@@ -602,8 +604,25 @@ void run_slot_predict(laq_ctx* ctx, laq_probe* p, const int32_t* const* d_fks, i
         }
         LAQ_CUDA(cudaFuncSetAttribute(direct_one_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_w)));
         const unsigned g1 = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((chunks1 + 31) / 32, ctx->sm_count)));
-        direct_one_k<<<g1, slot::kDirectBT, smem_w, ctx->stream>>>(a, chunks1, p->chunk_counts.get(), miss,
-                                                                   p->miss.get() + 2, p->chunk_offsets.get());
+        // Programmatic dependent launch once the staged tables are stable (no
+        // bind since the previous call): this call's table staging overlaps the
+        // previous kernel's tail; it waits (griddepcontrol.wait) before reading
+        // keys or writing anything.  LAQ_PREDICT_PDL=0 disables.
+        const char* pdl_env = std::getenv("LAQ_PREDICT_PDL");
+        const bool pdl = p->tables_stable && !(pdl_env && std::string(pdl_env) == "0");
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(g1);
+        cfg.blockDim = dim3(slot::kDirectBT);
+        cfg.dynamicSmemBytes = smem_w;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl ? 1 : 0;
+        LAQ_CUDA(cudaLaunchKernelEx(&cfg, direct_one_k, a, static_cast<int64_t>(chunks1), p->chunk_counts.get(), miss,
+                                    p->miss.get() + 2, p->chunk_offsets.get()));
+        p->tables_stable = true;
         return;
       }
       direct_small_k<<<g0, slot::kWarpThreads, smem_w, ctx->stream>>>(a, n_chunks, p->chunk_counts.get(), miss,

@@ -1,5 +1,5 @@
-"""A/B of the cfg1 fused join+predict call forms (one launch vs three) at 1M
-and 1e8 rows, CUDA-graph replay timing, plus a miss-path exactness check of
+"""A/B of the cfg1 fused join+predict call forms (one launch vs three; staged
+vs L1-gathered partials; programmatic dependent launch on/off) at 1M and 1e8 rows, CUDA-graph replay timing, plus a miss-path exactness check of
 the one-launch form (dangling keys -> last-CTA compaction) vs the oracle.
 
   python scripts/predict_ab.py   (on a GPU box)
@@ -62,8 +62,13 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         out["calibration: " + name] = {"us": round(e0.elapsed_time(e1) / 100 * 1e3, 2)}
-    for mode in ("1", "0"):
+    for mode, env in (("1", {}), ("0", {}), ("1", {"LAQ_PREDICT_NO_PSTAGE": "1"}), ("1", {"LAQ_PREDICT_PDL": "0"})):
         os.environ["LAQ_PREDICT_ONE_LAUNCH"] = mode
+        os.environ.pop("LAQ_PREDICT_NO_PSTAGE", None)
+        os.environ.pop("LAQ_PREDICT_PDL", None)
+        os.environ.update(env)
+        if env:
+            mode += "+" + ",".join(f"{k}={v}" for k, v in env.items())
         pred = fusion.FusedStarPredictor([pk], f.partials)
         for n in (1_000_000, 4_000_000, 100_000_000):
             fkd = torch.from_numpy(fk.astype(np.int32)).cuda() if n == 1_000_000 else \
