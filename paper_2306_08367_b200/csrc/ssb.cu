@@ -1468,9 +1468,9 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
     mode = std::max(mode, p->mode);
   }
   // Bins with a positive measure: sums only (a group is present iff its sum
-  // is non-zero), half the shared atomics of (count, sum) bins.  Decided after
-  // the layout: measured faster when every link is staged (SF=100 Q3 group
-  // 1.77 -> 1.44 ms), slower with L2-gathered links (Q4 group 3.22 -> 3.40 ms).
+  // is non-zero), half the shared atomics of (count, sum) bins: SF=100 Q3
+  // group 1.77 -> 1.45 ms; Q4 group (L2-gathered part ids) 3.13 -> 3.10 ms,
+  // same box, with the current kernel (an earlier one measured it slower there).
   bool positive_measure = false;
   if (mode == 1 && p0->scan.measure) {
     bool positive = true;
@@ -1641,9 +1641,7 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
     if (const char* e = std::getenv("LAQ_BATCH_DEC_REP")) rep = std::max(1, std::min(rep, std::atoi(e)));
   }
 
-  bool all_staged = true;
-  for (int j = 0; j < b->nl; ++j) all_staged = all_staged && staged[j];
-  if (positive_measure && (all_staged || std::getenv("LAQ_BATCH_SUM_BINS"))) mode = 2;
+  if (positive_measure) mode = 2;
   b->mode = mode;
   const int64_t final_bin_words = mode == 1 ? 2 : 1;
   // Final dictionaries: exact capacities and id widths.

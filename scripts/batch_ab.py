@@ -28,7 +28,7 @@ def main():
                       for grp in (3, 4)}
     settings = [("default", {}), ("prefetch=0", {"LAQ_PREFETCH": "0"}), ("prefetch=1", {"LAQ_PREFETCH": "1"}),
                 ("prefetch=2", {"LAQ_PREFETCH": "2"}), ("prefetch=4", {"LAQ_PREFETCH": "4"}),
-                ("dec_rep=1", {"LAQ_BATCH_DEC_REP": "1"}), ("count_bins", {"LAQ_BATCH_COUNT_BINS": "1"}), ("sum_bins", {"LAQ_BATCH_SUM_BINS": "1"}),
+                ("dec_rep=1", {"LAQ_BATCH_DEC_REP": "1"}), ("count_bins", {"LAQ_BATCH_COUNT_BINS": "1"}),
                 ("bitmap_first", {"LAQ_BATCH_BITMAP_FIRST": "1"}),
                 ("bitmap_first+pipe", {"LAQ_BATCH_BITMAP_FIRST": "1", "LAQ_BATCH_PIPE": "1"}),
                 ("pipe", {"LAQ_BATCH_PIPE": "1"}), ("dec64", {"LAQ_BATCH_DEC64": "1"}),

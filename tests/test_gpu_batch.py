@@ -179,7 +179,7 @@ def test_sf10_bench_groups_fused_vs_golden(gpu_ctx):
 
 
 @pytest.mark.parametrize("env", [{"LAQ_NOSMEMTAB": "1"}, {"LAQ_NOSMEMTAB": "1", "LAQ_BATCH_PIPE": "1"},
-                                 {"LAQ_BATCH_COUNT_BINS": "1"}, {"LAQ_BATCH_SUM_BINS": "1", "LAQ_NOSMEMTAB": "1"},
+                                 {"LAQ_BATCH_COUNT_BINS": "1"}, {"LAQ_BATCH_COUNT_BINS": "1", "LAQ_NOSMEMTAB": "1"},
                                  {"LAQ_BATCH_DEC64": "1"}, {"LAQ_BATCH_DEC64": "1", "LAQ_NOSMEMTAB": "1"}])
 def test_layout_variants_match_oracle(gpu_ctx, monkeypatch, env):
     """Every kernel form the layout can pick: all links gathered through L2
