@@ -109,6 +109,9 @@ int laq_ctx_attach_nccl(laq_ctx* ctx, int32_t nranks, int32_t rank, const uint8_
     ncclUniqueId id;
     std::memcpy(id.internal, h_id, sizeof(id.internal));
     ncclComm_t comm = nullptr;
+    // ncclCommInitRank binds the communicator to the calling thread's current
+    // device: make that the context's device whatever the caller last set.
+    LAQ_CUDA(cudaSetDevice(ctx->device));
     check(n, n.comm_init_rank(&comm, nranks, id, rank), "ncclCommInitRank");
     ctx->nccl = comm;
     ctx->nranks = nranks;

@@ -239,3 +239,58 @@ def test_wide_dictionaries_and_fallbacks(gpu_ctx):
         assert b.fused == fused, (name, b.why)
         for qq, m in zip(qs, got):
             assert np.array_equal(m, O.run_query(tables, qq)), (name, qq.id)
+
+
+def test_four_link_batches(gpu_ctx, monkeypatch, capfd):
+    """SSB Q4.x's shape: three queries over four links with a 175-group space,
+    dangling keys (miss tuples fail every link) and a ragged tail; a second
+    four-link batch with an empty fact interval (one more fail in the initial
+    lane) and small group spaces.  Both run fused; every result equals the
+    oracle."""
+    from paper_2306_08367_b200 import query as Q, star
+    monkeypatch.setenv("LAQ_BATCH_VERBOSE", "1")
+    rng = np.random.default_rng(404)
+    n = 4096 * 148 * 2 + 777
+    sizes = (3000, 20000, 1400, 2555)
+    fact = {"lo_m": rng.integers(1, 10_000, n).astype(np.int64), "lo_a": rng.integers(0, 50, n).astype(np.int64)}
+    tables, kinds, links = {}, {}, []
+    fk_kinds = {"lo_m": 1, "lo_a": 1}
+    for d, rows in enumerate(sizes):
+        name = f"d{d}"
+        tables[name] = {"pk": np.arange(rows, dtype=np.int64), "x": rng.integers(0, 7, rows).astype(np.int64),
+                        "y": rng.integers(0, 25, rows).astype(np.int64),
+                        "z": rng.integers(0, 1000, rows).astype(np.int64)}
+        kinds[name] = {"pk": 0, "x": 1, "y": 1, "z": 1}
+        fk = rng.integers(0, rows, n).astype(np.int64)
+        miss = rng.random(n) < 0.01
+        fk[miss] = rows + rng.integers(0, 50, miss.sum())
+        fact[f"lo_fk{d}"] = fk
+        fk_kinds[f"lo_fk{d}"] = 0
+        links.append((f"lo_fk{d}", name, "pk"))
+    tables = {"lineorder": fact, **tables}
+    kinds = {"lineorder": fk_kinds, **kinds}
+    joins = [Q.StarLink(*l) for l in links]
+    ds = star.DeviceStar.from_tables(tables, kinds, links)
+
+    def q4(i, dial):
+        return Q.QuerySpec(id=f"n{i}", group=0, joins=joins,
+                           filters=[Q.FilterSpec(0, "z", Q.Pred.lt(dial)), Q.FilterSpec(1, "x", Q.Pred.lt(5)),
+                                    Q.FilterSpec(3, "z", Q.Pred.between(100, 900))],
+                           measure="lo_m", group_by=[Q.GroupRef(3, "x"), Q.GroupRef(1, "y")], order_by=True)
+
+    batches = [[q4(0, 300), q4(1, 500), q4(2, 700)],
+               [Q.QuerySpec(id="e", group=0, joins=joins, filters=[Q.FilterSpec(-1, "lo_a", Q.Pred.between(30, 10))],
+                            measure="lo_m", group_by=[Q.GroupRef(2, "x")]),
+                Q.QuerySpec(id="f", group=0, joins=joins, filters=[Q.FilterSpec(0, "x", Q.Pred.lt(3))],
+                            measure="lo_m", group_by=[Q.GroupRef(2, "x")]),
+                Q.QuerySpec(id="g", group=0, joins=joins, filters=[Q.FilterSpec(-1, "lo_a", Q.Pred.lt(25))],
+                            measure="lo_m", group_by=[Q.GroupRef(1, "x")])]]
+    for qs in batches:
+        capfd.readouterr()
+        b, got = _run_batch(ds, qs)
+        assert b.fused, b.why
+        err = capfd.readouterr().err
+        assert "nl=4" in err, err
+        for q, m in zip(qs, got):
+            want = O.run_query(tables, q)
+            assert m.shape == want.shape and np.array_equal(m, want), q.id
