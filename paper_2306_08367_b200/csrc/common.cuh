@@ -105,26 +105,56 @@ struct DevBuf {
   T* get() const { return p; }
 };
 
-// Persistent device allocation (plans, probe tables): plain cudaMalloc.
+// Persistent device allocation (plans, probe tables): plain cudaMalloc.  The
+// (count, ctx) form takes the memory from the context stream's pool instead
+// and frees it stream-ordered: for per-call temporaries (a probe built and
+// dropped inside one C-ABI call) that would otherwise pay a synchronising
+// cudaMalloc/cudaFree each call.
 template <class T>
 struct DevMem {
   T* p = nullptr;
   size_t n = 0;
+  bool pooled = false;
+  cudaStream_t s = nullptr;
   DevMem() = default;
   explicit DevMem(size_t count) : n(count) {
     if (count) LAQ_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
   }
+  DevMem(size_t count, const laq_ctx* ctx) : n(count), pooled(true), s(ctx->stream) {
+    if (count) LAQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
+  }
   DevMem(const DevMem&) = delete;
   DevMem& operator=(const DevMem&) = delete;
-  DevMem(DevMem&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; }
+  DevMem(DevMem&& o) noexcept : p(o.p), n(o.n), pooled(o.pooled), s(o.s) { o.p = nullptr; }
   DevMem& operator=(DevMem&& o) noexcept {
-    if (p) cudaFree(p);
-    p = o.p; n = o.n; o.p = nullptr;
+    release();
+    p = o.p; n = o.n; pooled = o.pooled; s = o.s; o.p = nullptr;
     return *this;
   }
-  ~DevMem() { if (p) cudaFree(p); }
+  ~DevMem() { release(); }
+  void release() {
+    if (p) {
+      if (pooled) cudaFreeAsync(p, s);
+      else cudaFree(p);
+    }
+    p = nullptr;
+  }
   T* get() const { return p; }
 };
+
+template <class T>
+DevMem<T> dev_mem(int64_t count, const laq_ctx* ctx, bool pooled) {
+  return pooled ? DevMem<T>(static_cast<size_t>(count), ctx) : DevMem<T>(static_cast<size_t>(count));
+}
+
+// Bits needed for every value in [0, max_val] (>= 1; 64 for a negative max_val):
+// the end_bit of a radix sort over keys known to lie in that range.
+inline int bits_for(int64_t max_val) {
+  if (max_val < 0) return 64;
+  int b = 1;
+  while (b < 63 && (max_val >> b) != 0) ++b;
+  return b;
+}
 
 inline int grid_for(int64_t n, int per_block, int max_blocks) {
   int64_t b = (n + per_block - 1) / per_block;

@@ -10,9 +10,10 @@
 // groupby_sum_multi = sort-unique over tuples + segmented sum in row order.
 // Tuples are ranked per column (distinct values -> dense ranks), packed into
 // one mixed-radix code (first column most significant = lexicographic
-// order), stably radix-sorted with the row index, and every segment is summed
-// sequentially in ascending row order by one thread — the reference's exact
-// accumulation order, so fp64 sums are bit-identical.
+// order), stably radix-sorted with the row index (only the code's significant
+// bits), and every segment is folded sequentially in ascending row order by
+// one warp (segsum_kernel) -- the reference's exact accumulation order, so
+// fp64 sums are bit-identical.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -33,20 +34,52 @@ __device__ __forceinline__ int64_t find_sorted(const int64_t* __restrict__ d, in
   return (a < n && __ldg(d + a) == v) ? a : -1;
 }
 
-__global__ void rank_kernel(const int64_t* __restrict__ v, int64_t n, const int64_t* __restrict__ distinct,
-                            int64_t nd, int64_t stride, int64_t* code, int accumulate) {
+// Tuple codes for groupby_sum_multi: code[i] = sum over columns of
+// rank(col[c][i]) * stride[c] (every value is present in its column's
+// distinct array), plus the row index for the stable sort -- all columns in
+// one pass (8 B per column in, 16 B out per row).
+constexpr int kRankCols = 8;
+struct RankArgs {
+  int n_cols;
+  const int64_t* col[kRankCols];
+  const int64_t* distinct[kRankCols];
+  int64_t nd[kRankCols], stride[kRankCols];
+};
+
+__global__ void rank_kernel(const __grid_constant__ RankArgs a, int64_t n, int64_t* __restrict__ code,
+                            int64_t* __restrict__ row) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = find_sorted(distinct, nd, v[i]);
-    code[i] = (accumulate ? code[i] : 0) + r * stride;
+    int64_t c = 0;
+#pragma unroll 1
+    for (int k = 0; k < a.n_cols; ++k) c += find_sorted(a.distinct[k], a.nd[k], __ldcs(a.col[k] + i)) * a.stride[k];
+    code[i] = c;
+    row[i] = i;
   }
 }
 
+// Row-ordered segmented sums: segment s = vals[rows[t]] for t in
+// [seg_off[s], seg_off[s+1]), folded left to right exactly as the reference's
+// sequential loop (laqops.cpp:446-451) -- fp64 addition is not associative,
+// so the fold itself stays serial.  One warp per segment: the lanes load 32
+// consecutive row ids (coalesced) and gather their values (32 independent
+// loads in flight), then lane 0 folds them in order from shuffles.
 __global__ void segsum_kernel(const int64_t* __restrict__ seg_off, int64_t n_seg, const int64_t* __restrict__ rows,
                               const double* __restrict__ vals, double* __restrict__ out) {
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_seg; s += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = warp; s < n_seg; s += warps) {
+    const int64_t b = seg_off[s], e = seg_off[s + 1];
     double acc = 0.0;
-    for (int64_t t = seg_off[s]; t < seg_off[s + 1]; ++t) acc = __dadd_rn(acc, __ldg(vals + rows[t]));
-    out[s] = acc;
+    for (int64_t t = b; t < e; t += 32) {
+      const int m = e - t < 32 ? static_cast<int>(e - t) : 32;
+      const double v = lane < m ? __ldg(vals + rows[t + lane]) : 0.0;
+      for (int j = 0; j < m; ++j) {
+        const double x = __shfl_sync(0xffffffffu, v, j);
+        acc = __dadd_rn(acc, x);
+      }
+    }
+    if (lane == 0) out[s] = acc;
   }
 }
 
@@ -112,9 +145,9 @@ __global__ void key_of_pair(const int64_t* __restrict__ codes, int64_t n, int64_
     out[i] = codes[i] / G;
 }
 
-__global__ void iota_kernel(int64_t* out, int64_t n) {
+__global__ void add_kernel(int64_t* __restrict__ a, const int64_t* __restrict__ b, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = i;
+    a[i] += b[i];
 }
 
 int64_t run_length(laq_ctx* ctx, const int64_t* sorted, int64_t n, int64_t* uniq, int64_t* counts) {
@@ -139,30 +172,27 @@ void sort_keys(laq_ctx* ctx, const int64_t* kin, int64_t* kout, int64_t n) {
   ++ctx->launches;
 }
 
-void sort_pairs(laq_ctx* ctx, const int64_t* kin, int64_t* kout, const int64_t* vin, int64_t* vout, int64_t n) {
+// Stable sort of (key, value) pairs.  max_key >= 0: every key lies in
+// [0, max_key], so only its significant bits are sorted (a 7,000-tuple space
+// is 13 bits: two onesweep passes instead of eight).
+void sort_pairs(laq_ctx* ctx, const int64_t* kin, int64_t* kout, const int64_t* vin, int64_t* vout, int64_t n,
+                int64_t max_key = -1) {
   if (n == 0) return;
+  const int end_bit = bits_for(max_key);
   size_t b = 0;
-  LAQ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, kin, kout, vin, vout, n, 0, 64, ctx->stream));
+  LAQ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, kin, kout, vin, vout, n, 0, end_bit, ctx->stream));
   DevBuf<char> tmp(ctx, b);
-  LAQ_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), b, kin, kout, vin, vout, n, 0, 64, ctx->stream));
+  LAQ_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), b, kin, kout, vin, vout, n, 0, end_bit, ctx->stream));
   ++ctx->launches;
 }
 
-// Sorted distinct values of a column (signed int64; radix sort is signed-aware).
+// Sorted distinct values of a column (signed int64): the bitmap kernels when
+// the value range is below 2^31 (group-by columns usually are), else radix
+// sort + unique (signed-aware).
 int64_t distinct_of(laq_ctx* ctx, const int64_t* col, int64_t n, DevBuf<int64_t>& out) {
   out = DevBuf<int64_t>(ctx, std::max<int64_t>(n, 1));
   if (n == 0) return 0;
-  DevBuf<int64_t> sorted(ctx, n);
-  sort_keys(ctx, col, sorted.get(), n);
-  int64_t* d_num = ctx->d_flags + 49;
-  size_t b = 0;
-  LAQ_CUDA(cub::DeviceSelect::Unique(nullptr, b, sorted.get(), out.get(), d_num, n, ctx->stream));
-  DevBuf<char> tmp(ctx, b);
-  LAQ_CUDA(cub::DeviceSelect::Unique(tmp.get(), b, sorted.get(), out.get(), d_num, n, ctx->stream));
-  ++ctx->launches;
-  LAQ_CUDA(cudaMemcpyAsync(ctx->h_pinned, d_num, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
-  sync(ctx);
-  return ctx->h_pinned[0];
+  return distinct_sorted(ctx, col, n, nullptr, 0, out.get(), nullptr);
 }
 
 }  // namespace
@@ -222,14 +252,14 @@ int laq_groupby_sum_single(laq_ctx* ctx, const int64_t* kr, const double* vr, in
                                                                     uniq.get(), cnt.get(), G, roff.get(), tg.get(),
                                                                     tv.get(), ti.get());
         launched(ctx);
-        sort_pairs(ctx, tg.get(), sg.get(), ti.get(), si.get(), nt);  // stable: row order kept per group
+        sort_pairs(ctx, tg.get(), sg.get(), ti.get(), si.get(), nt, G - 1);  // stable: row order kept per group
         const int64_t ng = run_length(ctx, sg.get(), nt, ug.get(), uc.get());
         int64_t tot = 0;
         exclusive_scan_i64(ctx, uc.get(), so.get(), ng, &tot);
         ctx->h_pinned[8] = tot;
         LAQ_CUDA(cudaMemcpyAsync(so.get() + ng, &ctx->h_pinned[8], sizeof(int64_t), cudaMemcpyHostToDevice,
                                  ctx->stream));
-        segsum_kernel<<<grid_for(ng, 128, g), 128, 0, ctx->stream>>>(so.get(), ng, si.get(), tv.get(), ss.get());
+        segsum_kernel<<<grid_for(32 * ng, 256, g), 256, 0, ctx->stream>>>(so.get(), ng, si.get(), tv.get(), ss.get());
         launched(ctx);
         scatter_sums<<<grid_for(ng, 256, g), 256, 0, ctx->stream>>>(ug.get(), ss.get(), ng, out_sums);
         launched(ctx);
@@ -257,15 +287,27 @@ int laq_groupby_sum_multi(laq_ctx* ctx, int32_t n_cols, const int64_t* const* d_
       s *= nd[c];
     }
     DevBuf<int64_t> code(ctx, n), iota(ctx, n), scode(ctx, n), srow(ctx, n);
-    for (int c = 0; c < n_cols; ++c) {
-      rank_kernel<<<grid_for(n, 256, g), 256, 0, ctx->stream>>>(d_cols[c], n, distinct[c].get(), nd[c], stride[c],
-                                                               code.get(), c > 0);
+    for (int c0 = 0; c0 < n_cols; c0 += kRankCols) {  // > 8 columns: accumulate over several passes
+      RankArgs ra{};
+      ra.n_cols = std::min(kRankCols, n_cols - c0);
+      for (int k = 0; k < ra.n_cols; ++k) {
+        ra.col[k] = d_cols[c0 + k];
+        ra.distinct[k] = distinct[c0 + k].get();
+        ra.nd[k] = nd[c0 + k];
+        ra.stride[k] = stride[c0 + k];
+      }
+      if (c0 == 0) {
+        rank_kernel<<<grid_for(n, 256, g), 256, 0, ctx->stream>>>(ra, n, code.get(), iota.get());
+      } else {
+        DevBuf<int64_t> part(ctx, n);
+        rank_kernel<<<grid_for(n, 256, g), 256, 0, ctx->stream>>>(ra, n, part.get(), iota.get());
+        add_kernel<<<grid_for(n, 256, g), 256, 0, ctx->stream>>>(code.get(), part.get(), n);
+        launched(ctx);
+      }
       launched(ctx);
     }
-    iota_kernel<<<grid_for(n, 256, g), 256, 0, ctx->stream>>>(iota.get(), n);
-    launched(ctx);
     // Stable: rows stay ascending within a tuple (laqops.cpp:424-429).
-    sort_pairs(ctx, code.get(), scode.get(), iota.get(), srow.get(), n);
+    sort_pairs(ctx, code.get(), scode.get(), iota.get(), srow.get(), n, s - 1);
     DevBuf<int64_t> uniq(ctx, n), cnt(ctx, n), off(ctx, n + 1);
     const int64_t G = run_length(ctx, scode.get(), n, uniq.get(), cnt.get());
     if (G > capacity) fail(LAQ_ERR_CAPACITY, "groupby_sum_multi: output capacity");
@@ -273,7 +315,7 @@ int laq_groupby_sum_multi(laq_ctx* ctx, int32_t n_cols, const int64_t* const* d_
     exclusive_scan_i64(ctx, cnt.get(), off.get(), G, &total);
     ctx->h_pinned[8] = total;
     LAQ_CUDA(cudaMemcpyAsync(off.get() + G, &ctx->h_pinned[8], sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
-    segsum_kernel<<<grid_for(G, 128, g), 128, 0, ctx->stream>>>(off.get(), G, srow.get(), d_vals, d_out_sums);
+    segsum_kernel<<<grid_for(32 * G, 256, g), 256, 0, ctx->stream>>>(off.get(), G, srow.get(), d_vals, d_out_sums);
     launched(ctx);
     for (int c = 0; c < n_cols; ++c) {
       decode_kernel<<<grid_for(G, 256, g), 256, 0, ctx->stream>>>(uniq.get(), G, distinct[c].get(), stride[c], nd[c],

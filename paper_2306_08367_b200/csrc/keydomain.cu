@@ -28,6 +28,53 @@ __global__ void bitmap_set(const int64_t* __restrict__ k, int64_t n, int64_t bas
   }
 }
 
+// Key ranges whose bitmap fits one CTA's shared memory (<= kSmemBitmapWords
+// words, ~1.6M keys): every CTA sets bits in its own shared copy (shared
+// atomics, no L2 contention -- 60M keys over a 1M range put ~1,900 global
+// atomics on every word), then ORs its non-zero words into the global bitmap.
+// Both key arrays in one launch; 16-byte streaming loads of two keys.
+constexpr int kBitmapThreads = 1024;
+constexpr int64_t kSmemBitmapWords = 50 * 1024;
+
+__device__ __forceinline__ void smem_set_bit(unsigned* sb, int64_t key, int64_t base) {
+  // Skip the atomic when the bit is already set (a plain shared load): with
+  // few distinct keys every CTA's atomics would otherwise serialise on a
+  // handful of words.  A stale read only costs a redundant atomic.
+  const uint32_t o = static_cast<uint32_t>(key - base);
+  const unsigned bit = 1u << (o & 31);
+  if (!(*reinterpret_cast<volatile unsigned*>(sb + (o >> 5)) & bit)) atomicOr(sb + (o >> 5), bit);
+}
+
+__device__ __forceinline__ void smem_set_keys(unsigned* sb, const int64_t* __restrict__ k, int64_t n, int64_t base) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  int64_t head = 0;
+  if (reinterpret_cast<uintptr_t>(k) & 15) {  // align the vector loop to 16 bytes
+    head = 1;
+    if (tid == 0 && n > 0) smem_set_bit(sb, k[0], base);
+  }
+  const int64_t pairs = (n - head) / 2;
+  const longlong2* v = reinterpret_cast<const longlong2*>(k + head);
+  for (int64_t i = tid; i < pairs; i += nt) {
+    const longlong2 x = __ldcs(v + i);
+    smem_set_bit(sb, x.x, base);
+    smem_set_bit(sb, x.y, base);
+  }
+  if (tid == 0 && head + 2 * pairs < n) smem_set_bit(sb, k[n - 1], base);
+}
+
+__global__ void __launch_bounds__(kBitmapThreads) bitmap_set_smem(const int64_t* __restrict__ a, int64_t na,
+                                                                  const int64_t* __restrict__ b, int64_t nb,
+                                                                  int64_t base, int64_t words, unsigned* bits) {
+  extern __shared__ unsigned sb[];
+  for (int64_t w = threadIdx.x; w < words; w += blockDim.x) sb[w] = 0;
+  __syncthreads();
+  smem_set_keys(sb, a, na, base);
+  smem_set_keys(sb, b, nb, base);
+  __syncthreads();
+  for (int64_t w = threadIdx.x; w < words; w += blockDim.x)
+    if (const unsigned x = sb[w]) atomicOr(bits + w, x);
+}
+
 __global__ void bitmap_popc(const unsigned* __restrict__ bits, int64_t words, int64_t* cnt) {
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x)
     cnt[w] = __popc(bits[w]);
@@ -52,7 +99,11 @@ __global__ void copy_i64(const int64_t* __restrict__ a, int64_t na, const int64_
     out[i] = i < na ? a[i] : b[i - na];
 }
 
+}  // namespace
+
 // Sorted distinct keys of the concatenation a ++ b into out; returns count.
+// what != nullptr: negative keys raise DomainError (join keys); nullptr: any
+// int64 values (group-by columns).
 int64_t distinct_sorted(laq_ctx* ctx, const int64_t* a, int64_t na, const int64_t* b, int64_t nb, int64_t* out,
                         const char* what) {
   const int64_t n = na + nb;
@@ -60,16 +111,27 @@ int64_t distinct_sorted(laq_ctx* ctx, const int64_t* a, int64_t na, const int64_
   int64_t mn = INT64_MAX, mx = INT64_MIN, t0, t1;
   if (na) { minmax_i64(ctx, a, na, &t0, &t1); mn = std::min(mn, t0); mx = std::max(mx, t1); }
   if (nb) { minmax_i64(ctx, b, nb, &t0, &t1); mn = std::min(mn, t0); mx = std::max(mx, t1); }
-  if (mn < 0) fail(LAQ_ERR_DOMAIN, std::string(what) + std::to_string(mn));
-  const int64_t range = mx - mn + 1;
-  if (range <= (int64_t{1} << 31)) {
+  if (what && mn < 0) fail(LAQ_ERR_DOMAIN, std::string(what) + std::to_string(mn));
+  const bool narrow = static_cast<uint64_t>(mx) - static_cast<uint64_t>(mn) < (uint64_t{1} << 31);
+  const int64_t range = narrow ? mx - mn + 1 : 0;
+  if (narrow) {
     const int64_t words = (range + 31) / 32;
     DevBuf<unsigned> bits(ctx, words);
     DevBuf<int64_t> cnt(ctx, words);
     LAQ_CUDA(cudaMemsetAsync(bits.get(), 0, words * sizeof(unsigned), ctx->stream));
     const int g = ctx->sm_count * 8;
-    if (na) { bitmap_set<<<grid_for(na, 256, g), 256, 0, ctx->stream>>>(a, na, mn, bits.get()); launched(ctx); }
-    if (nb) { bitmap_set<<<grid_for(nb, 256, g), 256, 0, ctx->stream>>>(b, nb, mn, bits.get()); launched(ctx); }
+    if (words <= kSmemBitmapWords && n >= 64 * words) {
+      // Dense keys (many keys per bitmap word): per-CTA shared-memory bitmaps.
+      const size_t smem = static_cast<size_t>(words) * sizeof(unsigned);
+      LAQ_CUDA(cudaFuncSetAttribute(bitmap_set_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kSmemBitmapWords * sizeof(unsigned))));
+      const int blocks = static_cast<int>(std::min<int64_t>(ctx->sm_count, (n + 2 * kBitmapThreads - 1) / (2 * kBitmapThreads)));
+      bitmap_set_smem<<<blocks, kBitmapThreads, smem, ctx->stream>>>(a, na, b, nb, mn, words, bits.get());
+      launched(ctx);
+    } else {
+      if (na) { bitmap_set<<<grid_for(na, 256, g), 256, 0, ctx->stream>>>(a, na, mn, bits.get()); launched(ctx); }
+      if (nb) { bitmap_set<<<grid_for(nb, 256, g), 256, 0, ctx->stream>>>(b, nb, mn, bits.get()); launched(ctx); }
+    }
     bitmap_popc<<<grid_for(words, 256, g), 256, 0, ctx->stream>>>(bits.get(), words, cnt.get());
     launched(ctx);
     int64_t total = 0;
@@ -98,24 +160,68 @@ int64_t distinct_sorted(laq_ctx* ctx, const int64_t* a, int64_t na, const int64_
   return ctx->h_pinned[0];
 }
 
+namespace {
+
+// Keys -> domain positions.  A contiguous domain (its sorted distinct keys are
+// exactly base .. base + d - 1, e.g. dense surrogate keys) needs no table:
+// position = key - base, so the kernel streams 8 B in and 8 B out per key with
+// 16-byte loads/stores (CONTIG).  Otherwise each key gathers its slot from the
+// probe table (L2-resident; one key per thread per step measured fastest --
+// four independent gathers per thread were 1.2-1.4x slower, bound by L2
+// sector throughput).  One flag write per warp that saw a miss.
+template <bool CONTIG>
 __global__ void positions_kernel(const int64_t* __restrict__ keys, int64_t n, const ProbeView pv, int64_t* pos,
                                  int* missing) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t r = keys[i] < 0 ? -1 : pv.row(keys[i]);
-    if (r < 0) atomicOr(missing, 1);
-    pos[i] = r;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  bool miss = false;
+  auto contig = [&](int64_t key) -> int64_t {
+    const uint64_t s = static_cast<uint64_t>(key - pv.base);
+    const bool in = s < static_cast<uint64_t>(pv.size);
+    miss = miss || !in;
+    return in ? static_cast<int64_t>(s) : -1;
+  };
+  int64_t done = 0;
+  if constexpr (CONTIG) {
+    if (((reinterpret_cast<uintptr_t>(keys) | reinterpret_cast<uintptr_t>(pos)) & 15) == 0) {
+      const int64_t pairs = n / 2;
+      const longlong2* kv = reinterpret_cast<const longlong2*>(keys);
+      longlong2* pv2 = reinterpret_cast<longlong2*>(pos);
+      for (int64_t i = tid; i < pairs; i += nt) {
+        const longlong2 x = __ldcs(kv + i);
+        longlong2 p;
+        p.x = contig(x.x);
+        p.y = contig(x.y);
+        __stcs(pv2 + i, p);
+      }
+      done = 2 * pairs;
+    }
+    for (int64_t i = done + tid; i < n; i += nt) pos[i] = contig(keys[i]);
+  } else {
+    for (int64_t i = tid; i < n; i += nt) {
+      const int64_t k = keys[i];
+      const int32_t r = k < 0 ? -1 : pv.row(k);
+      miss = miss || r < 0;
+      pos[i] = r;
+    }
   }
+  if (__any_sync(0xffffffffu, miss) && (threadIdx.x & 31) == 0) atomicOr(missing, 1);
 }
 
 // Positions of keys in a sorted distinct domain (DomainError if absent).
 void positions(laq_ctx* ctx, const int64_t* keys, int64_t n, const int64_t* domain, int64_t d, int64_t* pos,
                Probe& probe_out) {
-  build_probe(ctx, domain, nullptr, d, probe_out, "key domain has duplicate keys");
+  build_probe(ctx, domain, nullptr, d, probe_out, "key domain has duplicate keys", /*pooled=*/true);
   int* missing = reinterpret_cast<int*>(ctx->d_flags + 41);
   LAQ_CUDA(cudaMemsetAsync(missing, 0, sizeof(int), ctx->stream));
   if (n) {
-    positions_kernel<<<grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(keys, n, probe_out.view(), pos,
-                                                                                  missing);
+    // build_probe rejected duplicates, so a DIRECT probe whose key range equals
+    // the domain size holds every key of [base, base + d): a contiguous domain.
+    if (probe_out.kind == PROBE_DIRECT && probe_out.size == d)
+      positions_kernel<true><<<grid_for(n, 256 * 2, ctx->sm_count * 8), 256, 0, ctx->stream>>>(
+          keys, n, probe_out.view(), pos, missing);
+    else
+      positions_kernel<false><<<grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(
+          keys, n, probe_out.view(), pos, missing);
     launched(ctx);
   }
   LAQ_CUDA(cudaMemcpyAsync(ctx->h_pinned, missing, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
@@ -176,7 +282,8 @@ struct Buckets {
   Probe probe;  // over uniq keys: row = run index
 };
 
-void bucket_by_key(laq_ctx* ctx, const int64_t* keys, int64_t n, Buckets& b) {
+// keys are non-negative and <= max_key (max_key < 0: unknown, sort all 64 bits).
+void bucket_by_key(laq_ctx* ctx, const int64_t* keys, int64_t n, Buckets& b, int64_t max_key) {
   b.sorted_keys = DevBuf<int64_t>(ctx, std::max<int64_t>(n, 1));
   b.sorted_idx = DevBuf<int64_t>(ctx, std::max<int64_t>(n, 1));
   b.uniq = DevBuf<int64_t>(ctx, std::max<int64_t>(n, 1));
@@ -184,18 +291,19 @@ void bucket_by_key(laq_ctx* ctx, const int64_t* keys, int64_t n, Buckets& b) {
   if (n == 0) {
     LAQ_CUDA(cudaMemsetAsync(b.run_off.get(), 0, sizeof(int64_t), ctx->stream));
     b.n_uniq = 0;
-    build_probe(ctx, b.uniq.get(), nullptr, 0, b.probe, "");
+    build_probe(ctx, b.uniq.get(), nullptr, 0, b.probe, "", /*pooled=*/true);
     return;
   }
   DevBuf<int64_t> iota(ctx, n);
   iota_i64<<<grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(iota.get(), n);
   launched(ctx);
   size_t bytes = 0;
+  const int bits = max_key < 0 ? 64 : bits_for(max_key);
   LAQ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, b.sorted_keys.get(), iota.get(), b.sorted_idx.get(), n,
-                                           0, 64, ctx->stream));
+                                           0, bits, ctx->stream));
   DevBuf<char> tmp(ctx, bytes);
   LAQ_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, keys, b.sorted_keys.get(), iota.get(), b.sorted_idx.get(),
-                                           n, 0, 64, ctx->stream));
+                                           n, 0, bits, ctx->stream));
   ++ctx->launches;
   DevBuf<int64_t> counts(ctx, n);
   int64_t* d_runs = ctx->d_flags + 42;
@@ -215,7 +323,7 @@ void bucket_by_key(laq_ctx* ctx, const int64_t* keys, int64_t n, Buckets& b) {
   LAQ_CUDA(cudaMemcpyAsync(b.run_off.get() + b.n_uniq, &ctx->h_pinned[8], sizeof(int64_t), cudaMemcpyHostToDevice,
                            ctx->stream));
   sync(ctx);
-  build_probe(ctx, b.uniq.get(), nullptr, b.n_uniq, b.probe, "");
+  build_probe(ctx, b.uniq.get(), nullptr, b.n_uniq, b.probe, "", /*pooled=*/true);
 }
 
 }  // namespace laq
@@ -280,10 +388,11 @@ int laq_key_matrix_dbr(laq_ctx* ctx, const int64_t* keys, int64_t n, const int64
     DevBuf<int64_t> spos(ctx, std::max<int64_t>(m, 1));
     if (m) {
       size_t bytes = 0;
-      LAQ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kpos.get(), spos.get(), kidx.get(), col_idx, m, 0, 64,
+      const int bits = bits_for(d - 1);  // positions lie in [0, d): sort only their significant bits
+      LAQ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kpos.get(), spos.get(), kidx.get(), col_idx, m, 0, bits,
                                                ctx->stream));
       DevBuf<char> tmp(ctx, bytes);
-      LAQ_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, kpos.get(), spos.get(), kidx.get(), col_idx, m, 0, 64,
+      LAQ_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, kpos.get(), spos.get(), kidx.get(), col_idx, m, 0, bits,
                                                ctx->stream));
       ++ctx->launches;
     }
@@ -307,11 +416,12 @@ int laq_mm_join(laq_ctx* ctx, const int64_t* r, int64_t nr, const int64_t* s, in
                 int64_t* out_s, int64_t capacity, int64_t* h_nnz) {
   return guard(ctx, [&] {
     // Domain validation as build_key_domain(keys_r, keys_s) (negative keys).
-    int64_t mn, mx;
+    int64_t mn, mx = -1;
     if (nr) { minmax_i64(ctx, r, nr, &mn, &mx); if (mn < 0) fail(LAQ_ERR_DOMAIN, "negative join key " + std::to_string(mn)); }
+    mx = -1;
     if (ns) { minmax_i64(ctx, s, ns, &mn, &mx); if (mn < 0) fail(LAQ_ERR_DOMAIN, "negative join key " + std::to_string(mn)); }
     Buckets b;
-    bucket_by_key(ctx, s, ns, b);
+    bucket_by_key(ctx, s, ns, b, mx);  // S keys in [0, mx]
     DevBuf<int64_t> cnt(ctx, std::max<int64_t>(nr, 1)), run_of_r(ctx, std::max<int64_t>(nr, 1)),
         off(ctx, std::max<int64_t>(nr, 1));
     int64_t total = 0;

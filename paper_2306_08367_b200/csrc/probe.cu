@@ -69,7 +69,7 @@ __global__ void hash_insert(const K* __restrict__ pk, int64_t n, int64_t cap, un
 }  // namespace
 
 void build_probe(laq_ctx* ctx, const int64_t* d_pk64, const int32_t* d_pk32, int64_t n, Probe& out,
-                 const std::string& what) {
+                 const std::string& what, bool pooled) {
   out = Probe();
   out.n_rows = n;
   if (n == 0) return;  // DIRECT with size 0: every probe misses
@@ -81,13 +81,13 @@ void build_probe(laq_ctx* ctx, const int64_t* d_pk64, const int32_t* d_pk32, int
   const int64_t range = mx - mn + 1;
   int* dup = reinterpret_cast<int*>(ctx->d_flags + 8);
   LAQ_CUDA(cudaMemsetAsync(dup, 0, sizeof(int), ctx->stream));
-  out.row_slot = DevMem<int32_t>(n);
+  out.row_slot = dev_mem<int32_t>(n, ctx, pooled);
   const int grid = grid_for(n, 256, ctx->sm_count * 8);
   if (range <= std::max<int64_t>(4 * n, int64_t{1} << 20) && range < (int64_t{1} << 31)) {
     out.kind = PROBE_DIRECT;
     out.base = mn;
     out.size = range;
-    out.rows = DevMem<int32_t>(range);
+    out.rows = dev_mem<int32_t>(range, ctx, pooled);
     LAQ_CUDA(cudaMemsetAsync(out.rows.get(), 0xFF, range * sizeof(int32_t), ctx->stream));
     if (d_pk64) direct_insert<<<grid, 256, 0, ctx->stream>>>(d_pk64, n, mn, out.rows.get(), out.row_slot.get(), dup);
     else direct_insert<<<grid, 256, 0, ctx->stream>>>(d_pk32, n, mn, out.rows.get(), out.row_slot.get(), dup);
@@ -97,8 +97,8 @@ void build_probe(laq_ctx* ctx, const int64_t* d_pk64, const int32_t* d_pk32, int
     while (cap < 2 * n) cap <<= 1;
     out.kind = PROBE_HASH;
     out.size = cap;
-    out.keys = DevMem<int64_t>(cap);
-    out.rows = DevMem<int32_t>(cap);
+    out.keys = dev_mem<int64_t>(cap, ctx, pooled);
+    out.rows = dev_mem<int32_t>(cap, ctx, pooled);
     LAQ_CUDA(cudaMemsetAsync(out.keys.get(), 0xFF, cap * sizeof(int64_t), ctx->stream));
     LAQ_CUDA(cudaMemsetAsync(out.rows.get(), 0xFF, cap * sizeof(int32_t), ctx->stream));
     auto* k = reinterpret_cast<unsigned long long*>(out.keys.get());
@@ -670,7 +670,8 @@ int laq_star_join(laq_ctx* ctx, int32_t n_links, const int64_t* const* d_fks, in
     }
     Probe probes[kMaxLinks];
     for (int j = 0; j < n_links; ++j)
-      build_probe(ctx, d_pks[j], nullptr, h_pk_rows[j], probes[j], "multiway_star_join: duplicate keys in dim " + std::to_string(j));
+      build_probe(ctx, d_pks[j], nullptr, h_pk_rows[j], probes[j], "multiway_star_join: duplicate keys in dim " + std::to_string(j),
+                  /*pooled=*/true);
     StarArgs<int64_t> a{};
     a.n_links = n_links;
     a.n = n_fact;

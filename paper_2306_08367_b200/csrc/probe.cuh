@@ -66,7 +66,15 @@ struct Probe {
 int probe_links(const laq_probe* p);
 ProbeView probe_view(const laq_probe* p, int j);
 
+// pooled: the tables come from the context stream's pool (a probe that lives
+// only inside one call; see DevMem).
 void build_probe(laq_ctx* ctx, const int64_t* d_pk64, const int32_t* d_pk32, int64_t n, Probe& out,
-                 const std::string& what);
+                 const std::string& what, bool pooled = false);
+
+// Sorted distinct values of a ++ b into out (count returned): a bitmap over
+// [min, max] when the range is below 2^31, else radix sort + unique
+// (keydomain.cu).  what != nullptr: negative values raise DomainError.
+int64_t distinct_sorted(laq_ctx* ctx, const int64_t* a, int64_t na, const int64_t* b, int64_t nb, int64_t* out,
+                        const char* what);
 
 }  // namespace laq

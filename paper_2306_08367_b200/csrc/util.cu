@@ -7,6 +7,7 @@
 #include <cmath>
 
 #include <cstring>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -19,11 +20,35 @@ __global__ void minmax_kernel(const T* __restrict__ d, int64_t n, unsigned long 
                               unsigned long long* out_max_biased) {
   // Bias by 2^63 so signed order == unsigned order for atomicMin/Max.
   int64_t mn = LLONG_MAX, mx = LLONG_MIN;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = static_cast<int64_t>(d[i]);
+  auto take = [&](int64_t v) {
     mn = v < mn ? v : mn;
     mx = v > mx ? v : mx;
+  };
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  int64_t done = 0;
+  if ((reinterpret_cast<uintptr_t>(d) & 15) == 0) {
+    // 16-byte loads, two per thread per step (64 B in flight per thread)
+    constexpr int kPer = 16 / sizeof(T);
+    using V = typename std::conditional<sizeof(T) == 8, longlong2, int4>::type;
+    const V* v = reinterpret_cast<const V*>(d);
+    const int64_t nv = n / kPer;
+    int64_t i = tid;
+    for (; i + nt < nv; i += 2 * nt) {
+      const V a = __ldcs(v + i), b = __ldcs(v + i + nt);
+      const T* pa = reinterpret_cast<const T*>(&a);
+      const T* pb = reinterpret_cast<const T*>(&b);
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) take(static_cast<int64_t>(pa[k])), take(static_cast<int64_t>(pb[k]));
+    }
+    for (; i < nv; i += nt) {
+      const V a = __ldcs(v + i);
+      const T* pa = reinterpret_cast<const T*>(&a);
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) take(static_cast<int64_t>(pa[k]));
+    }
+    done = nv * kPer;
   }
+  for (int64_t i = done + tid; i < n; i += nt) take(static_cast<int64_t>(d[i]));
   for (int o = 16; o; o >>= 1) {
     const int64_t a = __shfl_xor_sync(0xffffffffu, mn, o);
     const int64_t b = __shfl_xor_sync(0xffffffffu, mx, o);
@@ -46,7 +71,7 @@ void minmax_impl(laq_ctx* ctx, const T* d, int64_t n, int64_t* mn, int64_t* mx) 
   unsigned long long* f = reinterpret_cast<unsigned long long*>(ctx->d_flags);
   unsigned long long init[2] = {~0ull, 0ull};
   LAQ_CUDA(cudaMemcpyAsync(f, init, sizeof init, cudaMemcpyHostToDevice, ctx->stream));
-  minmax_kernel<T><<<grid_for(n, 256 * 8, ctx->sm_count * 4), 256, 0, ctx->stream>>>(d, n, f, f + 1);
+  minmax_kernel<T><<<grid_for(n, 256 * 16, ctx->sm_count * 8), 256, 0, ctx->stream>>>(d, n, f, f + 1);
   launched(ctx);
   LAQ_CUDA(cudaMemcpyAsync(ctx->h_pinned, f, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
   sync(ctx);

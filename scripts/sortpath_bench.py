@@ -59,7 +59,15 @@ def main():
     pos = torch.empty(n, dtype=torch.int64, device="cuda")
     ms = timed(lambda: ctx.check(ctx.lib.laq_key_positions(ctx.h, dense.data_ptr(), n, d.data_ptr(), nd,
                                                              pos.data_ptr())))
-    out["a4 key_matrix RowsByDomain (laq_key_positions: bitmap rank)"] = {"ms": ms, "alg_GBs": 16 * n / ms / 1e6}
+    out["a4 key_matrix RowsByDomain, contiguous domain (laq_key_positions: key - base)"] = {
+        "ms": ms, "alg_GBs": 16 * n / ms / 1e6}
+    even = dense * 2  # every other key: a domain with gaps -> probe-table gathers
+    de = ops.build_key_domain(even, s).sorted_keys
+    de = de if isinstance(de, torch.Tensor) else torch.from_numpy(de).cuda()
+    ms = timed(lambda: ctx.check(ctx.lib.laq_key_positions(ctx.h, even.data_ptr(), n, de.data_ptr(), de.numel(),
+                                                             pos.data_ptr())))
+    out["a4 key_matrix RowsByDomain, domain with gaps (laq_key_positions: probe gather)"] = {
+        "ms": ms, "alg_GBs": 16 * n / ms / 1e6}
     row_ptr = torch.empty(nd + 1, dtype=torch.int64, device="cuda")
     col = torch.empty(n, dtype=torch.int64, device="cuda")
     ov = torch.empty(n, dtype=torch.float64, device="cuda")

@@ -45,6 +45,30 @@ def test_key_domain_large_and_wide(lib):
         assert np.array_equal(ops.build_key_domain(a, b).sorted_keys, O.build_key_domain(a, b))
 
 
+def test_key_encoding_dense_unaligned(lib):
+    """The shared-memory bitmap path (a dense key range whose bitmap fits one
+    CTA: 1.5M keys, 4M rows) and the vectorised position lookups, on device
+    views 8 bytes off a 16-byte boundary (scalar head/tail) and with odd
+    lengths; a key outside the domain still raises DomainError."""
+    import torch
+    ops, _, errors = lib
+    rng = np.random.default_rng(5)
+    for hi, na, nb in ((1_500_000, 4_000_001, 3), (1000, 70_001, 0), (50_000, 3_333_333, 17)):
+        a = rng.integers(0, hi, na)
+        b = rng.integers(0, hi, nb)
+        da = torch.from_numpy(np.concatenate([[0], a])).cuda()[1:]
+        db = torch.from_numpy(np.concatenate([[0], b])).cuda()[1:]
+        want = O.build_key_domain(a, b)
+        d = ops.build_key_domain(da, db)
+        got = d.sorted_keys.cpu().numpy() if hasattr(d.sorted_keys, "cpu") else d.sorted_keys
+        assert np.array_equal(got, want), hi
+        m = ops.key_matrix(da, ops.KeyDomain(want), "RowsByDomain")
+        assert np.array_equal(np.asarray(m.col_idx), np.searchsorted(want, a)), hi
+    with pytest.raises(errors.DomainError):
+        keys = torch.from_numpy(np.concatenate([[0], np.arange(1000), [5000]])).cuda()[1:]
+        ops.key_matrix(keys, ops.KeyDomain(np.arange(1000)), "RowsByDomain")
+
+
 def test_key_matrix(lib):
     ops, _, errors = lib
     g = OPS["key_matrix_example"]
@@ -139,6 +163,26 @@ def test_groupby(lib):
     assert np.array_equal(s, ws)  # R-row-ordered sums: bit-identical, run to run too
     g2, s2 = ops.groupby_sum_single(kr, vr, ks, gs)
     assert np.array_equal(s2, s)
+
+
+def test_groupby_multi_large_signed_wide(lib):
+    """groupby_sum_multi at scale vs the oracle, bit-exact: long fp64 segments
+    (thousands of rows, lengths not multiples of 32: the warp fold's partial
+    chunks), a negative-valued column (the bitmap distinct path with a negative
+    base), a column spanning more than 2^31 (the radix-sort distinct path) and
+    a single-column case."""
+    ops, _, _ = lib
+    rng = np.random.default_rng(9)
+    n = 400_003
+    a = rng.integers(-3, 4, n)
+    b = rng.integers(0, 25, n)
+    w = rng.choice(np.array([-(1 << 40), 5, 1 << 41]), n)
+    v = rng.normal(size=n) * 1e3
+    for cols in ([a, b], [w, a], [b]):
+        k, sums = ops.groupby_sum_multi(cols, v)
+        wk, ws = O.groupby_sum_multi(cols, v)
+        assert all(np.array_equal(np.asarray(x), np.asarray(y)) for x, y in zip(k, wk))
+        assert np.array_equal(sums, ws)
 
 
 def _star(c):
