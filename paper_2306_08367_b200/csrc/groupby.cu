@@ -46,12 +46,33 @@ struct RankArgs {
   int64_t nd[kRankCols], stride[kRankCols];
 };
 
+// A column whose values span at most kRankLut gets a shared-memory rank
+// table (value - lo -> rank, built per CTA from its distinct array): one
+// shared load per row instead of a binary search of dependent L1 loads.
+constexpr int kRankLut = 4096;
+
 __global__ void rank_kernel(const __grid_constant__ RankArgs a, int64_t n, int64_t* __restrict__ code,
                             int64_t* __restrict__ row) {
+  extern __shared__ int32_t lut[];  // kRankLut entries per column
+  uint32_t use_lut = 0;
+  int64_t lo[kRankCols];
+  for (int k = 0; k < a.n_cols; ++k) {
+    lo[k] = a.distinct[k][0];
+    if (static_cast<uint64_t>(a.distinct[k][a.nd[k] - 1]) - static_cast<uint64_t>(lo[k]) < kRankLut) {
+      use_lut |= 1u << k;
+      for (int64_t j = threadIdx.x; j < a.nd[k]; j += blockDim.x)
+        lut[k * kRankLut + (a.distinct[k][j] - lo[k])] = static_cast<int32_t>(j);
+    }
+  }
+  __syncthreads();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t c = 0;
 #pragma unroll 1
-    for (int k = 0; k < a.n_cols; ++k) c += find_sorted(a.distinct[k], a.nd[k], __ldcs(a.col[k] + i)) * a.stride[k];
+    for (int k = 0; k < a.n_cols; ++k) {
+      const int64_t v = __ldcs(a.col[k] + i);
+      const int64_t r = (use_lut >> k) & 1u ? lut[k * kRankLut + (v - lo[k])] : find_sorted(a.distinct[k], a.nd[k], v);
+      c += r * a.stride[k];
+    }
     code[i] = c;
     row[i] = i;
   }
@@ -296,11 +317,14 @@ int laq_groupby_sum_multi(laq_ctx* ctx, int32_t n_cols, const int64_t* const* d_
         ra.nd[k] = nd[c0 + k];
         ra.stride[k] = stride[c0 + k];
       }
+      const size_t lut = static_cast<size_t>(ra.n_cols) * kRankLut * sizeof(int32_t);
+      LAQ_CUDA(cudaFuncSetAttribute(rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lut)));
+      const int rg = grid_for(n, 512, ctx->sm_count * 4);
       if (c0 == 0) {
-        rank_kernel<<<grid_for(n, 256, g), 256, 0, ctx->stream>>>(ra, n, code.get(), iota.get());
+        rank_kernel<<<rg, 512, lut, ctx->stream>>>(ra, n, code.get(), iota.get());
       } else {
         DevBuf<int64_t> part(ctx, n);
-        rank_kernel<<<grid_for(n, 256, g), 256, 0, ctx->stream>>>(ra, n, part.get(), iota.get());
+        rank_kernel<<<rg, 512, lut, ctx->stream>>>(ra, n, part.get(), iota.get());
         add_kernel<<<grid_for(n, 256, g), 256, 0, ctx->stream>>>(code.get(), part.get(), n);
         launched(ctx);
       }
