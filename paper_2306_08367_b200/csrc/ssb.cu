@@ -1627,6 +1627,38 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
     if (!std::getenv("LAQ_NOSMEMTAB") && !use_bm[j] && idb[j] <= room) staged[j] = 1, room -= idb[j];
   for (int j : by)
     if (!staged[j] && !use_bm[j] && bmb[j] <= room && frac[j] < 0.75) use_bm[j] = 1, room -= bmb[j];
+  // Probe order: shared-memory links first, then L2 gathers; most selective first.
+  std::vector<int> order(b->nl);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+    if (staged[x] != staged[y]) return staged[x] > staged[y];
+    return frac[x] < frac[y];
+  });
+  // Joint pair: the first two probe-order links, both staged, share one decode
+  // table of n0 x n1 entries (one decode load per row instead of two) when it
+  // is small and fits; sum-bin (positive measure) batches, the instantiated form.
+  std::vector<int64_t> dec_n(b->n_dec.begin(), b->n_dec.end());  // entries staged per link
+  bool joint = false;
+  // Only when every link is staged: with an L2-gathered link the pass is bound by
+  // the gathers and the smaller decode replication the joint table leaves costs
+  // more than the saved load (SF=100 Q4 group 3.14 vs 3.10 ms; Q3 group 1.38 vs
+  // 1.45 ms with it, profiles/round2/batch_ab_joint_pair.json).
+  bool all_staged = true;
+  for (int j = 0; j < b->nl; ++j) all_staged = all_staged && staged[j];
+  if (positive_measure && b->nl >= 2 && all_staged && !std::getenv("LAQ_BATCH_PIPE") &&
+      !std::getenv("LAQ_BATCH_NOJOINT")) {
+    const int o0 = order[0], o1 = order[1];
+    const int64_t nj = int64_t{b->n_dec[o0]} * b->n_dec[o1];
+    const int64_t jb = (dec_entry * nj + 15) & ~int64_t{15};
+    if (nj <= 1024 && jb - decb[o0] - decb[o1] <= room) {
+      room -= jb - decb[o0] - decb[o1];
+      decb[o0] = 0;
+      decb[o1] = jb;
+      dec_n[o0] = 0;
+      dec_n[o1] = nj;
+      joint = true;
+    }
+  }
   // Decode tables replicated `rep` times (entry-interleaved) with what room is
   // left: lane l reads copy l % rep, so a warp's 32 random decodes conflict at
   // most 32/rep-way on a bank instead of colliding on the few entries' banks.
@@ -1648,13 +1680,6 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
   for (int j = 0; j < b->nl; ++j) cap[j] = b->n_dec[j];
   batch_alloc_dict(b, cap, idw, use_bm);
 
-  // Probe order: shared-memory links first, then L2 gathers; most selective first.
-  std::vector<int> order(b->nl);
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
-    if (staged[x] != staged[y]) return staged[x] > staged[y];
-    return frac[x] < frac[y];
-  });
   BatchScan& B = b->B;
   B = BatchScan{};
   B.n = p0->fact_rows;
@@ -1673,7 +1698,7 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
     K.bm = L.bm;
     K.fmt = staged[j] ? (idw[j] == 1 ? kIdSmemU8 : kIdSmemU16) : (idw[j] == 1 ? kIdGlobU8 : kIdGlobU16);
     K.dec_byte = static_cast<int>(off);
-    K.n_dec = b->n_dec[j];
+    K.n_dec = static_cast<int>(dec_n[j]);
     off += decb[j] * rep;
     B.fkc[t] = links[j].c;
     gathers = gathers || !staged[j];
@@ -1713,6 +1738,8 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
   }
   B.init_lo = B.init_hi = B.fail_lo = B.fail_hi = 0;
   B.dec32 = dec32 ? 1 : 0;
+  B.joint01 = joint ? 1 : 0;
+  B.n_tup1 = joint ? static_cast<uint32_t>(b->n_dec[order[1]]) : 1u;
   B.fail32 = static_cast<uint32_t>(f32);
   for (int q = 0; q < nq; ++q) {
     if (dec32) {
@@ -1741,8 +1768,8 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
   b->fused = true;
   b->why.clear();
   if (std::getenv("LAQ_BATCH_VERBOSE")) {
-    std::fprintf(stderr, "[laq batch] nq=%d nl=%d nf=%d mode=%d dec32=%d rep=%d smem=%lld\n", nq, b->nl, b->nf, mode,
-                 dec32 ? 1 : 0, rep, static_cast<long long>(off));
+    std::fprintf(stderr, "[laq batch] nq=%d nl=%d nf=%d mode=%d dec32=%d rep=%d smem=%lld joint01=%d\n", nq, b->nl,
+                 b->nf, mode, dec32 ? 1 : 0, rep, static_cast<long long>(off), joint ? 1 : 0);
     for (int t = 0; t < b->nl; ++t) {
       const int j = order[t];
       std::fprintf(stderr, "[laq batch]   link %d: slots=%lld tuples=%d frac=%.3f fmt=%d id_bytes=%d bm_bytes=%d\n", t,

@@ -76,6 +76,9 @@ struct BatchScan {
   uint32_t dec_shift;         // log2(8 * decode-table replication)
   int pipe;                   // the last link is L2-gathered: software-pipelined 2-row kernel
   int dec32;                  // narrow decode: 3 x 10-bit lanes in 4-byte entries (<= 3 queries, <= 3 links)
+  int joint01;                // kernel links 0 and 1 (both staged) share ONE decode table at link 1, indexed
+                              // id0 * n_tup1 + id1 (entry = dec0 + dec1): one decode load per row for the pair
+  uint32_t n_tup1;            // link 1's tuple ids (the joint index's radix)
   uint32_t fail32;            // the narrow lanes' fail value (a power of two >= every G)
 };
 

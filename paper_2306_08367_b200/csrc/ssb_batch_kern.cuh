@@ -96,7 +96,7 @@ __device__ __forceinline__ int4 ld4_nb(const Col& c, int64_t row0) {
 // MODE 0: per-thread register sums (every query has one group); MODE 1: u32
 // (count, sum) bins; MODE 2: u32 sum bins only -- the measure is positive, so
 // a group is present iff its sum is non-zero (half the shared atomics).
-template <int NQ, int NL, int NF, int MODE, int DW, bool TAIL>
+template <int NQ, int NL, int NF, int MODE, int DW, bool JP, bool TAIL>
 __device__ __forceinline__ void batch_rows(const BatchScan& B, int64_t row0, const int4 (&kv)[NL],
                                            const int4 (&fv)[NF > 0 ? NF : 1], const int4& mv, uint32_t s_base,
                                            uint32_t dec_base, uint32_t (&r_cnt)[NQ],
@@ -120,6 +120,7 @@ __device__ __forceinline__ void batch_rows(const BatchScan& B, int64_t row0, con
         add_fail<DW>(B, lo[r], hi[r], q, static_cast<uint32_t>(comp(fv[f], r)) - flo > span);
     }
   const uint32_t sh = B.dec_shift;  // log2(entry bytes * dec_rep)
+  uint32_t jid[4];
 #pragma unroll
   for (int j = 0; j < NL; ++j) {
     const BatchLink& L = B.link[j];
@@ -155,6 +156,15 @@ __device__ __forceinline__ void batch_rows(const BatchScan& B, int64_t row0, con
 #pragma unroll
         for (int r = 0; r < 4; ++r) id[r] = ldg_u16_if(go[r], static_cast<const uint16_t*>(L.ids) + sl[r], L.miss);
       }
+    }
+    if (JP && j == 0) {  // the pair's first id waits for link 1 (compile-time after unrolling)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) jid[r] = id[r];
+      continue;
+    }
+    if (JP && j == 1) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) id[r] += jid[r] * B.n_tup1;
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
@@ -211,7 +221,7 @@ __device__ __forceinline__ void spill_all(const BatchScan& B, unsigned char* sme
   }
 }
 
-template <int NQ, int NL, int NF, int MODE, int DW>
+template <int NQ, int NL, int NF, int MODE, int DW, bool JP>
 __global__ void __launch_bounds__(kDirectThreads, 1) scan_batch_kernel(const __grid_constant__ BatchScan B) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x;
@@ -225,14 +235,22 @@ __global__ void __launch_bounds__(kDirectThreads, 1) scan_batch_kernel(const __g
   for (int j = 0; j < NL; ++j) {
     const BatchLink& L = B.link[j];
     if (L.fmt == kIdSmemU8 || L.fmt == kIdSmemU16) stage(L.ids, L.id_byte, L.id_bytes);
+    // Entry x of link j's table; with JP, link 1's table is the pair's joint
+    // table (x = id0 * n_tup1 + id1: the sum of both links' entries, i.e. the
+    // lanes the two separate adds would give) and link 0 stages none (n_dec 0).
+    auto entry = [&](int x) -> unsigned long long {
+      if (JP && j == 1)
+        return __ldg(B.link[0].dec + x / static_cast<int>(B.n_tup1)) + __ldg(L.dec + x % static_cast<int>(B.n_tup1));
+      return __ldg(L.dec + x);
+    };
     if constexpr (DW == 64) {
       unsigned long long* d = reinterpret_cast<unsigned long long*>(smem + L.dec_byte);
-      for (int w = tid; w < L.n_dec * rep; w += kDirectThreads) d[w] = __ldg(L.dec + w / rep);  // entry-interleaved copies
+      for (int w = tid; w < L.n_dec * rep; w += kDirectThreads) d[w] = entry(w / rep);  // entry-interleaved copies
     } else {
-      // 16-bit lanes (fail = 4096) -> 10-bit lanes (fail = B.fail32)
+      // 16-bit lanes (fail = 4096 per failing link) -> 10-bit lanes (fail = B.fail32)
       uint32_t* d = reinterpret_cast<uint32_t*>(smem + L.dec_byte);
       for (int w = tid; w < L.n_dec * rep; w += kDirectThreads) {
-        const unsigned long long e = __ldg(L.dec + w / rep);
+        const unsigned long long e = entry(w / rep);
         uint32_t v = 0;
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
@@ -307,9 +325,9 @@ __global__ void __launch_bounds__(kDirectThreads, 1) scan_batch_kernel(const __g
       if (B.has_measure) bulk_prefetch_l2(B.mc, row0 + pf_rows, B.n);
     }
     if (it < full)
-      batch_rows<NQ, NL, NF, MODE, DW, false>(B, row0, kv, fv, mv, s_base, dec_base, r_cnt, r_sum);
+      batch_rows<NQ, NL, NF, MODE, DW, JP, false>(B, row0, kv, fv, mv, s_base, dec_base, r_cnt, r_sum);
     else
-      batch_rows<NQ, NL, NF, MODE, DW, true>(B, row0, kv, fv, mv, s_base, dec_base, r_cnt, r_sum);
+      batch_rows<NQ, NL, NF, MODE, DW, JP, true>(B, row0, kv, fv, mv, s_base, dec_base, r_cnt, r_sum);
     if constexpr (MODE != 0) {
       if (--until_flush == 0) {
         until_flush = B.flush_every;
@@ -538,9 +556,17 @@ void launch_batch_t(laq_ctx* ctx, const BatchScan& B, size_t smem, int grid) {
       return;
     }
   }
-  auto kern = scan_batch_kernel<NQ, NL, NF, MODE, 64>;
+  auto kern = scan_batch_kernel<NQ, NL, NF, MODE, 64, false>;
   if constexpr (NQ <= 3 && NL <= 3) {
-    if (B.dec32) kern = scan_batch_kernel<NQ, NL, NF, MODE, 32>;
+    if (B.dec32) kern = scan_batch_kernel<NQ, NL, NF, MODE, 32, false>;
+  }
+  if constexpr (MODE == 2 && NL >= 2) {  // joint pair: the positive-measure (sum-bin) batches only
+    if (B.joint01) {
+      kern = scan_batch_kernel<NQ, NL, NF, MODE, 64, true>;
+      if constexpr (NQ <= 3 && NL <= 3) {
+        if (B.dec32) kern = scan_batch_kernel<NQ, NL, NF, MODE, 32, true>;
+      }
+    }
   }
   LAQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int64_t blocks_needed = (B.n + kDirectThreads * 4 - 1) / (kDirectThreads * 4);

@@ -180,13 +180,15 @@ def test_sf10_bench_groups_fused_vs_golden(gpu_ctx):
 
 @pytest.mark.parametrize("env", [{"LAQ_NOSMEMTAB": "1"}, {"LAQ_NOSMEMTAB": "1", "LAQ_BATCH_PIPE": "1"},
                                  {"LAQ_BATCH_COUNT_BINS": "1"}, {"LAQ_BATCH_COUNT_BINS": "1", "LAQ_NOSMEMTAB": "1"},
-                                 {"LAQ_BATCH_DEC64": "1"}, {"LAQ_BATCH_DEC64": "1", "LAQ_NOSMEMTAB": "1"}])
+                                 {"LAQ_BATCH_DEC64": "1"}, {"LAQ_BATCH_DEC64": "1", "LAQ_NOSMEMTAB": "1"},
+                                 {"LAQ_BATCH_NOJOINT": "1"}, {"LAQ_BATCH_NOJOINT": "1", "LAQ_BATCH_DEC64": "1"}])
 def test_layout_variants_match_oracle(gpu_ctx, monkeypatch, env):
     """Every kernel form the layout can pick: all links gathered through L2
     (the software-pipelined 2-row kernel for the last link, synchronous
     gathers for the others), the unpipelined form, (count, sum) vs sum-only
-    bins, narrow (4-byte, 10-bit lanes) vs wide (8-byte, 16-bit lanes) decode
-    -- same results as the oracle on the SSB groups and random batches."""
+    bins, narrow (4-byte, 10-bit lanes) vs wide (8-byte, 16-bit lanes) decode,
+    with and without the joint decode table of the first two staged links --
+    same results as the oracle on the SSB groups and random batches."""
     from paper_2306_08367_b200 import gen, star
     for k, v in env.items():
         monkeypatch.setenv(k, v)
