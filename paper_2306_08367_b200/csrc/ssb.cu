@@ -1643,10 +1643,35 @@ void batch_prepare(laq_ctx* ctx, laq_batch* b) {
   // the gathers and the smaller decode replication the joint table leaves costs
   // more than the saved load (SF=100 Q4 group 3.14 vs 3.10 ms; Q3 group 1.38 vs
   // 1.45 ms with it, profiles/round2/batch_ab_joint_pair.json).
+  // The pair is the two staged links with the fewest joint entries, moved to
+  // the front of the probe order (staged links commute; gathered links keep
+  // their place after them).  With a gathered link the pair must be small
+  // enough to keep the decode replication (LAQ_BATCH_JOINT_GATHER_MAX entries,
+  // default 64: SF=100 Q4's commitdate x orderdate = 45).
   bool all_staged = true;
   for (int j = 0; j < b->nl; ++j) all_staged = all_staged && staged[j];
-  if (positive_measure && b->nl >= 2 && all_staged && !std::getenv("LAQ_BATCH_PIPE") &&
-      !std::getenv("LAQ_BATCH_NOJOINT")) {
+  int64_t pair_max = all_staged ? 1024 : 64;
+  if (!all_staged)
+    if (const char* e = std::getenv("LAQ_BATCH_JOINT_GATHER_MAX")) pair_max = std::atoll(e);
+  const bool want_joint = positive_measure && b->nl >= 2 && !std::getenv("LAQ_BATCH_PIPE") &&
+                          !std::getenv("LAQ_BATCH_NOJOINT");
+  int q0 = -1, q1 = -1;
+  for (int x = 0; want_joint && x < b->nl; ++x)
+    for (int y = x + 1; y < b->nl; ++y)
+      if (staged[order[x]] && staged[order[y]] &&
+          (q0 < 0 || int64_t{b->n_dec[order[x]]} * b->n_dec[order[y]] <
+                         int64_t{b->n_dec[order[q0]]} * b->n_dec[order[q1]]))
+        q0 = x, q1 = y;
+  if (q0 >= 0 && int64_t{b->n_dec[order[q0]]} * b->n_dec[order[q1]] <= pair_max) {
+    const int a0 = order[q0], a1 = order[q1];
+    std::vector<int> rest;
+    for (int x = 0; x < b->nl; ++x)
+      if (x != q0 && x != q1) rest.push_back(order[x]);
+    order.assign({a0, a1});
+    order.insert(order.end(), rest.begin(), rest.end());
+  }
+  if (want_joint && staged[order[0]] && staged[order[1]] &&
+      int64_t{b->n_dec[order[0]]} * b->n_dec[order[1]] <= pair_max) {
     const int o0 = order[0], o1 = order[1];
     const int64_t nj = int64_t{b->n_dec[o0]} * b->n_dec[o1];
     const int64_t jb = (dec_entry * nj + 15) & ~int64_t{15};

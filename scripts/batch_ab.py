@@ -31,7 +31,8 @@ def main():
                 ("dec_rep=1", {"LAQ_BATCH_DEC_REP": "1"}), ("count_bins", {"LAQ_BATCH_COUNT_BINS": "1"}),
                 ("bitmap_first", {"LAQ_BATCH_BITMAP_FIRST": "1"}),
                 ("bitmap_first+pipe", {"LAQ_BATCH_BITMAP_FIRST": "1", "LAQ_BATCH_PIPE": "1"}),
-                ("pipe", {"LAQ_BATCH_PIPE": "1"}), ("dec64", {"LAQ_BATCH_DEC64": "1"}), ("nojoint", {"LAQ_BATCH_NOJOINT": "1"}),
+                ("pipe", {"LAQ_BATCH_PIPE": "1"}), ("dec64", {"LAQ_BATCH_DEC64": "1"}), ("nojoint", {"LAQ_BATCH_NOJOINT": "1"}), ("jgather=0", {"LAQ_BATCH_JOINT_GATHER_MAX": "0"}),
+                ("jgather=1024", {"LAQ_BATCH_JOINT_GATHER_MAX": "1024"}),
                 ("nojoint+dec64", {"LAQ_BATCH_NOJOINT": "1", "LAQ_BATCH_DEC64": "1"}),
                 ("bulkpf=-1", {"LAQ_PREFETCH": "-1"}), ("bulkpf=-2", {"LAQ_PREFETCH": "-2"}),
                 ("bulkpf=-4", {"LAQ_PREFETCH": "-4"})]
