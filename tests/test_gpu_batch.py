@@ -70,9 +70,9 @@ def test_all_twelve_queries_in_batches_of_any_mix(gpu_ctx):
             assert m.shape == want[i].shape and np.array_equal(m, want[i]), (trial, qs[i].id, b.fused, b.why)
 
 
-def _random_star(rng, n, dense=True, dangling=0.0):
+def _random_star(rng, n, dense=True, dangling=0.0, positive=False):
     from paper_2306_08367_b200 import query as Q
-    fact = {"lo_measure": rng.integers(0, 10_000, n).astype(np.int64),
+    fact = {"lo_measure": rng.integers(1 if positive else 0, 10_000, n).astype(np.int64),
             "lo_a": rng.integers(0, 50, n).astype(np.int64),
             "lo_b": rng.integers(-20, 20, n).astype(np.int64)}
     fk_kinds = {"lo_measure": 1, "lo_a": 1, "lo_b": 1}
@@ -130,7 +130,9 @@ def test_random_batches_match_oracle(gpu_ctx, seed):
     from paper_2306_08367_b200 import star
     rng = np.random.default_rng(1000 + seed)
     n = int(rng.integers(1, 400_000))
-    tables, kinds, links, joins = _random_star(rng, n, dense=seed % 4 != 3, dangling=0.03 if seed % 5 == 1 else 0.0)
+    # positive measures (every other seed): sum-only bins and the joint pair decode
+    tables, kinds, links, joins = _random_star(rng, n, dense=seed % 4 != 3, dangling=0.03 if seed % 5 == 1 else 0.0,
+                                               positive=seed % 2 == 0)
     ds = star.DeviceStar.from_tables(tables, kinds, links)
     qs = [_random_query(rng, joins, i) for i in range(int(rng.integers(1, 5)))]
     b, got = _run_batch(ds, qs)
@@ -202,7 +204,8 @@ def test_layout_variants_match_oracle(gpu_ctx, monkeypatch, env):
             assert np.array_equal(m, O.run_query(g.tables, q)), (env, q.id)
     rng = np.random.default_rng(77)
     for trial in range(6):
-        tables, kinds, links, joins = _random_star(rng, int(rng.integers(1, 300_000)), dangling=0.02 * (trial % 2))
+        tables, kinds, links, joins = _random_star(rng, int(rng.integers(1, 300_000)), dangling=0.02 * (trial % 2),
+                                                   positive=trial % 3 == 0)
         dsr = star.DeviceStar.from_tables(tables, kinds, links)
         qs = [_random_query(rng, joins, i) for i in range(int(rng.integers(2, 5)))]
         b, got = _run_batch(dsr, qs)
