@@ -234,9 +234,31 @@ __global__ void iota_i64(int64_t* out, int64_t n) {
     out[i] = i;
 }
 
-__global__ void histogram_kernel(const int64_t* __restrict__ pos, int64_t n, unsigned long long* cnt) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(cnt + pos[i], 1ull);
+// CSR row pointers from the sorted positions: row_ptr[p] = the first index
+// whose position is >= p.  Thread i owns the positions in (spos[i-1], spos[i]]
+// (with spos[-1] = -1 and spos[m] = d), so every row_ptr entry is written once
+// and empty positions get their successor's start -- no atomics, no scan.
+__global__ void row_ptr_from_sorted(const int64_t* __restrict__ spos, int64_t m, int64_t d, int64_t* row_ptr) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= m; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = i == 0 ? -1 : spos[i - 1];
+    const int64_t b = i == m ? d : spos[i];
+    for (int64_t p = a + 1; p <= b; ++p) row_ptr[p] = i;
+  }
+}
+
+// The same row pointers by one lower-bound binary search per position: for
+// domains much smaller than the entry count (d <= m / 16: d log m reads
+// instead of m), and free of the boundary form's serial loop over a long run
+// of empty positions.
+__global__ void row_ptr_by_search(const int64_t* __restrict__ spos, int64_t m, int64_t d, int64_t* row_ptr) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p <= d; p += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = m;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldg(spos + mid) < p) lo = mid + 1; else hi = mid;
+    }
+    row_ptr[p] = lo;
+  }
 }
 
 __global__ void nonzero_flags(const double* __restrict__ v, int64_t n, char* flags) {
@@ -396,13 +418,11 @@ int laq_key_matrix_dbr(laq_ctx* ctx, const int64_t* keys, int64_t n, const int64
                                                ctx->stream));
       ++ctx->launches;
     }
-    DevBuf<unsigned long long> cnt(ctx, d + 1);
-    LAQ_CUDA(cudaMemsetAsync(cnt.get(), 0, (d + 1) * sizeof(unsigned long long), ctx->stream));
-    if (m) {
-      histogram_kernel<<<grid_for(m, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(kpos.get(), m, cnt.get());
-      launched(ctx);
-    }
-    exclusive_scan_i64(ctx, reinterpret_cast<int64_t*>(cnt.get()), row_ptr, d + 1, nullptr);
+    if (d > m / 16)  // positions comparable in number to the entries: one pass over the entries
+      row_ptr_from_sorted<<<grid_for(m + 1, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(spos.get(), m, d, row_ptr);
+    else
+      row_ptr_by_search<<<grid_for(d + 1, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(spos.get(), m, d, row_ptr);
+    launched(ctx);
     if (out_values && m) {
       gather_values<<<grid_for(m, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(values, col_idx, m, out_values);
       launched(ctx);

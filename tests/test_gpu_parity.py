@@ -89,6 +89,13 @@ def test_key_matrix(lib):
     rp, ci, vv = O.key_matrix(keys, dom, "DomainByRows", vals)
     m = ops.key_matrix(keys, ops.KeyDomain(dom), "DomainByRows", vals)
     assert np.array_equal(m.row_ptr, rp) and np.array_equal(m.col_idx, ci) and np.array_equal(m.values, vv)
+    # row pointers both ways: a domain much smaller than the entries (per-position
+    # search) and a big domain with long empty runs (one pass over the entries)
+    for dom, keys in ((np.arange(64), rng.integers(0, 64, 300_000)),
+                      (np.arange(100_000), rng.choice(np.array([5, 50_000, 99_999]), 3_000))):
+        rp, ci, _ = O.key_matrix(keys, dom, "DomainByRows")
+        m = ops.key_matrix(keys, ops.KeyDomain(dom), "DomainByRows")
+        assert np.array_equal(m.row_ptr, rp) and np.array_equal(m.col_idx, ci)
 
 
 def test_mm_join(lib):
