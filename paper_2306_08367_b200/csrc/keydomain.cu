@@ -93,10 +93,18 @@ __global__ void bitmap_emit(const unsigned* __restrict__ bits, const int64_t* __
   }
 }
 
+// a ++ b, minus `base` (the minimum): the keys become offsets in [0, range]
+// so the radix sort only needs the range's significant bits.
 __global__ void copy_i64(const int64_t* __restrict__ a, int64_t na, const int64_t* __restrict__ b, int64_t nb,
-                         int64_t* out) {
+                         int64_t base, int64_t* out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < na + nb; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = i < na ? a[i] : b[i - na];
+    out[i] = static_cast<int64_t>(static_cast<uint64_t>(i < na ? a[i] : b[i - na]) - static_cast<uint64_t>(base));
+}
+
+__global__ void add_base(int64_t* __restrict__ v, const int64_t* __restrict__ n, int64_t base) {
+  const int64_t m = *n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = static_cast<int64_t>(static_cast<uint64_t>(v[i]) + static_cast<uint64_t>(base));
 }
 
 }  // namespace
@@ -140,14 +148,21 @@ int64_t distinct_sorted(laq_ctx* ctx, const int64_t* a, int64_t na, const int64_
     launched(ctx);
     return total;
   }
-  // Wide key space: radix sort + unique.
+  // Wide key space: radix sort + unique.  When the range fits 63 bits the keys
+  // are sorted as offsets from the minimum over the range's bits only (2^40
+  // keys: 5 onesweep passes instead of 8), and the minimum is added back to the
+  // distinct offsets.
+  const uint64_t urange = static_cast<uint64_t>(mx) - static_cast<uint64_t>(mn);
+  const bool offs = urange < (uint64_t{1} << 63);
+  const int64_t base = offs ? mn : 0;
+  const int bits = offs ? bits_for(static_cast<int64_t>(urange)) : 64;
   DevBuf<int64_t> cat(ctx, n), sorted(ctx, n);
-  copy_i64<<<grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(a, na, b, nb, cat.get());
+  copy_i64<<<grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(a, na, b, nb, base, cat.get());
   launched(ctx);
   size_t bytes = 0;
-  LAQ_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, cat.get(), sorted.get(), n, 0, 64, ctx->stream));
+  LAQ_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, cat.get(), sorted.get(), n, 0, bits, ctx->stream));
   DevBuf<char> tmp(ctx, bytes);
-  LAQ_CUDA(cub::DeviceRadixSort::SortKeys(tmp.get(), bytes, cat.get(), sorted.get(), n, 0, 64, ctx->stream));
+  LAQ_CUDA(cub::DeviceRadixSort::SortKeys(tmp.get(), bytes, cat.get(), sorted.get(), n, 0, bits, ctx->stream));
   ++ctx->launches;
   int64_t* d_num = ctx->d_flags + 40;
   size_t b2 = 0;
@@ -155,6 +170,10 @@ int64_t distinct_sorted(laq_ctx* ctx, const int64_t* a, int64_t na, const int64_
   DevBuf<char> tmp2(ctx, b2);
   LAQ_CUDA(cub::DeviceSelect::Unique(tmp2.get(), b2, sorted.get(), out, d_num, n, ctx->stream));
   ++ctx->launches;
+  if (base != 0) {
+    add_base<<<grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(out, d_num, base);
+    launched(ctx);
+  }
   LAQ_CUDA(cudaMemcpyAsync(ctx->h_pinned, d_num, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
   sync(ctx);
   return ctx->h_pinned[0];
