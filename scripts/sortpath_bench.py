@@ -84,6 +84,15 @@ def main():
     ms = timed(lambda: ops.groupby_sum_multi(cols, vals))
     out["a19 groupby_sum_multi 3 cols, 7000 groups (CUB sort + RLE + segsum)"] = {"ms": ms,
                                                                                  "alg_GBs": 32 * n / ms / 1e6}
+    # a7 mm_join on the device buffers: 60M R keys x 1M S keys over a 1M domain (~60M pairs)
+    sk = torch.randint(0, 1 << 20, (1 << 20,), dtype=torch.int64, device="cuda", generator=g)
+    orr = torch.empty(2 * n, dtype=torch.int64, device="cuda")
+    oss = torch.empty(2 * n, dtype=torch.int64, device="cuda")
+    nnz = C.c_int64()
+    ms = timed(lambda: ctx.check(ctx.lib.laq_mm_join(ctx.h, dense.data_ptr(), n, sk.data_ptr(), sk.numel(),
+                                                       orr.data_ptr(), oss.data_ptr(), 2 * n, C.byref(nnz))))
+    out["a7 mm_join 60M x 1M keys (bucket sort of S + probe + pair writes)"] = {
+        "ms": ms, "pairs": int(nnz.value), "alg_GBs": (8 * n + 8 * sk.numel() + 16 * nnz.value) / ms / 1e6}
     print(json.dumps(out, indent=1))
 
 
