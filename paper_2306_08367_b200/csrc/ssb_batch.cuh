@@ -21,6 +21,10 @@
 // overflows 16 bits).  Fact filters add kLaneFail to the lanes of the queries
 // they reject.  A query's row then goes to its own shared-memory u32 bins.
 //
+// Joint pair (BatchScan::joint01, the kernel's JP template flag): two staged
+// links share one decode table indexed by id0 * n_tup1 + id1 whose entries are
+// the sums of both links' entries -- one decode load per row for the pair.
+//
 // Compared with scan_shared_kernel (one code table per query and link, each
 // probed separately) this is one probe per link instead of one per (query,
 // link), and one table per link in shared memory instead of NQ: SF=100
