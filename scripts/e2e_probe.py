@@ -10,6 +10,9 @@ from paper_2306_08367_b200.device import context  # noqa: E402
 
 ctx = context(0)
 g = gen.gen_star("Ssb", 100, 42, narrow=True, max_bytes=64 << 30)
+if os.environ.get("E2E_PROBE_MAIN_DS") == "1":  # hold the bench's resident device star as well
+    main_ds = star.upload_gen_star(g, ctx=ctx)
+    torch.cuda.synchronize()
 dials = {3: (105, 79, 43), 4: (249, 199, 284)}
 qs = [Q.spec_with_dial(d, grp, x) for grp in (3, 4) for d, x in zip(Q.group_defs(grp), dials[grp])]
 used = sorted({c for q in qs for c in ({l.fact_fk for l in q.joins} | {q.measure})})
